@@ -1,0 +1,305 @@
+"""Benchmark: track segments/s on the full-core PWR (C3) at N GPUs (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl nestrack|reference]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N
+
+A step = one pass of the whole hot path (birth -> descend -> segment loop -> tally flush, plus
+the one all-reduce of the packed tallies when N > 1) over one batch of C3 histories generated on
+the device from (seed, pid).  Weak scaling: each rank tracks `--particles` histories per step
+(default 1e8, the BASELINE C3 batch) from its own contiguous pid range.  Rank 0 prints one JSON
+line.  See DESIGN.md "Measurement".
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "track segments/s, full-core PWR at 1/2/4/8 B200; ratio vs rectilinear tracker"
+UNIT = "segments/s"
+PROFILES = os.path.join(ROOT, "profiles")
+
+
+def _args():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="nestrack", choices=["nestrack", "reference"])
+    ap.add_argument("--config", default="c3")
+    ap.add_argument("--particles", type=float, default=None, help="histories per GPU per step")
+    ap.add_argument("--tracker", default="generic", choices=["generic", "rect"])
+    ap.add_argument("--pseudo-array", action="store_true")
+    ap.add_argument("--block-dim", type=int, default=0)
+    ap.add_argument("--blocks-per-sm", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def _dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+class ClockSampler:
+    """Samples SM clocks and throttle reasons (NVML) during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+               0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, index: int):
+        self.index = index
+        self.samples = []
+        self.reasons = set()
+        self.max_mhz = None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return self
+
+        def loop():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for bit, name in self.REASONS.items():
+                        if r & bit and name != "gpu_idle":
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+                time.sleep(0.1)
+
+        self._t = threading.Thread(target=loop, daemon=True)
+        self._t.start()
+        return self
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        s = sorted(self.samples)
+        return {"sm_mhz": s[len(s) // 2] if s else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(s)}
+
+
+def _load_json(name):
+    p = os.path.join(PROFILES, name)
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def fp64_peak_tflops(sm_max_mhz: float | None) -> float:
+    """fp64 FMA peak derived from unit counts: 148 SMs x 64 FP64 lanes x
+    2 flop/FMA x max SM clock (1965 MHz) = 37.2 TFLOP/s."""
+    mhz = sm_max_mhz or 1965.0
+    return 148 * 64 * 2 * mhz * 1e6 / 1e12
+
+
+def cpu_baseline(spec, seed: int, budget_s: float):
+    """The oracle as it stands, on this host's cores, on a bounded sample of the workload."""
+    import oracle
+    om = oracle.OracleModel.from_spec(spec)
+    cores = len(os.sched_getaffinity(0))
+    n = 2000
+    t = time.perf_counter()
+    r = om.run(n, seed=seed, threads=cores)
+    dt = time.perf_counter() - t
+    # scale the sample to ~budget_s of CPU work
+    n2 = int(min(max(n * budget_s / max(dt, 1e-3), n), 5_000_000))
+    t = time.perf_counter()
+    r = om.run(n2, seed=seed, pid_begin=10_000_000, threads=cores)
+    dt = time.perf_counter() - t
+    seg = r["counters"]["segments"]
+    return {"value": seg / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n2} histories of {spec['name']} (pids 1e7..), {seg} segments, {dt:.1f} s",
+            "falg_flops_per_segment": om.falg(r)}
+
+
+def run_reference(a, spec, rank, world):
+    """--impl reference: the oracle (CPU) timed on the host cores, rank 0 only."""
+    if rank != 0:
+        return
+    import oracle
+    om = oracle.OracleModel.from_spec(spec)
+    cores = len(os.sched_getaffinity(0))
+    probe = om.run(1000, seed=1, threads=cores)
+    n = 2000
+    t = time.perf_counter()
+    om.run(n, seed=1, threads=cores)
+    per = (time.perf_counter() - t) / n
+    n_step = int(max(1000, min(2_000_000, 8.0 / max(per, 1e-9))))   # ~8 s per step
+    for w in range(a.warmup):
+        om.run(min(n_step, 20000), seed=100 + w, threads=cores)
+    segs, tt = 0, 0.0
+    for s in range(a.steps):
+        t = time.perf_counter()
+        r = om.run(n_step, seed=1000 + s, pid_begin=s * n_step, threads=cores)
+        tt += time.perf_counter() - t
+        segs += r["counters"]["segments"]
+    v = segs / tt
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+            "warmup": a.warmup, "ms_per_step": 1e3 * tt / a.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": spec["name"], "histories_per_step": n_step, "tracker": "oracle (CPU)"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
+                             "sample": f"{a.steps} steps x {n_step} histories of {spec['name']}"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    del probe
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    a = _args()
+    rank, world, local = _dist_env()
+    import workloads
+    spec, n_cfg = workloads.config(a.config)
+    if a.impl == "reference":
+        run_reference(a, spec, rank, world)
+        return
+
+    import torch
+    import paper_2406_13849_b200 as nt
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = int(a.particles) if a.particles else n_cfg
+    model = nt.Model.from_spec(spec, device=local, pseudo_array=a.pseudo_array)
+    stream = torch.cuda.current_stream()
+    out = torch.zeros(model.out_len, dtype=torch.float64, device="cuda")
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    seed0 = workloads.SEED
+    kw = dict(tracker=a.tracker, block_dim=a.block_dim, blocks_per_sm=a.blocks_per_sm)
+
+    outs = [torch.zeros(model.out_len, dtype=torch.float64, device="cuda") for _ in range(a.steps)]
+
+    def step(s, o):
+        o.zero_()
+        model.track(n, seed=seed0 + s, pid_begin=rank * n, out=o, stream=stream, **kw)
+        if dist is not None:
+            dist.all_reduce(o)      # the one collective: packed [len | exits | counters]
+
+    for w in range(a.warmup):
+        step(10_000 + w, out)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clocks = ClockSampler(local).start()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(a.steps)]
+    launches = 0
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    for s in range(a.steps):
+        flush.fill_(s & 0xFF)                       # evict L2 between timed steps (untimed)
+        ev[s][0].record(stream)
+        step(s, outs[s])
+        ev[s][1].record(stream)
+        launches += model.last_launch_count()
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    ck = clocks.stop()
+    t_rank = sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3
+    t_max = t_rank
+    if dist is not None:
+        tt = torch.tensor([t_rank], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_max = float(tt)
+    per_step = [model.unpack(o) for o in outs]
+    res = per_step[-1]
+    segs = sum(p["counters"]["segments"] for p in per_step)      # all ranks (post all-reduce)
+    particles = n * world * a.steps
+    value = segs / t_max
+
+    # kernel-only time on rank 0's stream is the same region (one launch per step), so the
+    # kernel's average launch duration is t_rank / steps (all-reduce excluded only at N = 1)
+    falg_doc = _load_json("falg.json") or {}
+    falg = falg_doc.get(spec["name"])
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        cpu = cpu_baseline(spec, seed0, a.cpu_seconds)
+        falg = cpu.pop("falg_flops_per_segment")
+    peak = fp64_peak_tflops(ck["sm_max_mhz"])
+    kernel_s = t_rank / a.steps
+    achieved = (falg or 0.0) * (segs / (world * a.steps)) / kernel_s / 1e12 if falg else None
+    traffic_doc = _load_json("traffic.json") or {}
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+            "frac": (achieved / peak) if achieved else None,
+            "traffic": traffic_doc.get(spec["name"]),
+            "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz (DESIGN.md)",
+            "falg_flops_per_segment": falg, "kernel_ms_per_launch": 1e3 * kernel_s}
+
+    e2e = None
+    if not a.no_e2e:
+        hout = None
+        import numpy as np
+        hout = np.zeros(model.out_len)
+        for w in range(1):
+            model.track_host(min(n, 100000), seed=seed0, out=hout, **kw)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        esegs = 0
+        if dist is not None:
+            dist.barrier()
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for s in range(a.steps):
+            model.track_host(n, seed=seed0 + 500 + s, pid_begin=rank * n, out=hout, stream=stream, **kw)
+            esegs += int(hout[2 * model.n_mc + 1])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = max(e0.elapsed_time(e1) / 1e3, time.perf_counter() - t0)
+        if dist is not None:
+            tt = torch.tensor([te, float(esegs)], dtype=torch.float64, device="cuda")
+            dist.all_reduce(tt[:1], op=dist.ReduceOp.MAX)
+            dist.all_reduce(tt[1:], op=dist.ReduceOp.SUM)
+            te, esegs = float(tt[0]), int(tt[1])
+        e2e = {"value": esegs / te, "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": int(model.out_len * 8),
+               "api": "nt_track_host (host output buffer; births generated on device from seed/pid)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+                "warmup": a.warmup, "ms_per_step": 1e3 * t_max / a.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (histories born from Philox(seed, pid) on the device)",
+                "config": {"workload": spec["name"], "histories_per_gpu_per_step": n,
+                           "tracker": a.tracker, "pseudo_array": bool(a.pseudo_array),
+                           "parallelism": f"pid-sharded x{world}, one fp64 all-reduce per step",
+                           "l2": "256 MB buffer written between timed steps (L2 flushed)"},
+                "particles_per_s": particles / t_max,
+                "segments_per_history": segs / particles,
+                "counters_last_step": res["counters"],
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": ck}
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

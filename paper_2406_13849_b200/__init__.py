@@ -1,0 +1,359 @@
+"""nestrack: B200-native nested-geometry Monte Carlo tracking (arXiv 2406.13849 hot path).
+
+Thin Python binding over the C ABI of ``libnestrack.so`` (include/nestrack.h).  This module
+only marshals arguments: every step of the tracking path runs in the library's CUDA kernels.
+PyTorch provides device memory, streams and process groups.  There is no CPU fallback: if the
+library is missing, importing :func:`lib` raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libnestrack.so")
+
+KIND = {"PX": 0, "PY": 1, "PZ": 2, "PLANE": 3, "CZ": 4, "SPHERE": 5}
+BC = {"none": 0, "vacuum": 1, "reflect": 2}
+TRACKER = {"generic": 0, "rect": 1}
+NT_TRACE = 1
+COUNTERS = ["particles", "segments", "crossings", "reflections", "leaks", "collisions",
+            "absorptions", "lost", "capped", "flagged"] + [f"cross_l{i}" for i in range(8)]
+NC = len(COUNTERS)
+STATUS = {0: "NT_OK", -1: "NT_E_ARG", -2: "NT_E_ID", -3: "NT_E_ORDER", -4: "NT_E_GEOMETRY",
+          -5: "NT_E_UNSUPPORTED", -6: "NT_E_CUDA", -7: "NT_E_NOMEM"}
+
+TRACE_DTYPE = np.dtype([("pid", "<u8"), ("s", "<f8"), ("seg", "<u4"), ("cell_before", "<i4"),
+                        ("cell_after", "<i4"), ("j", "<i4"), ("kind", "u1"), ("level", "i1"),
+                        ("terminal", "u1"), ("pad", "u1"), ("flags", "<u4")])
+
+
+class NtError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class BuildOpts(C.Structure):
+    _fields_ = [("device", C.c_int32), ("bih_max_leaf", C.c_int32), ("pseudo_array", C.c_int32),
+                ("reserved", C.c_int32), ("sah_ct", C.c_double), ("sah_ci", C.c_double)]
+
+
+class ModelInfo(C.Structure):
+    _fields_ = [("n_surfaces", C.c_int32), ("n_cells", C.c_int32), ("n_material_cells", C.c_int32),
+                ("n_universes", C.c_int32), ("max_depth", C.c_int32),
+                ("rect_specialisable", C.c_int32), ("rect_levels", C.c_int32),
+                ("n_bih_nodes", C.c_int32), ("out_len", C.c_int64), ("device_bytes", C.c_size_t)]
+
+
+class Run(C.Structure):
+    _fields_ = [("seed", C.c_uint64), ("pid_begin", C.c_uint64), ("n", C.c_uint64),
+                ("src_lo", C.c_double * 3), ("src_hi", C.c_double * 3),
+                ("max_segments", C.c_uint64), ("tracker", C.c_int32), ("flags", C.c_uint32),
+                ("block_dim", C.c_int32), ("blocks_per_sm", C.c_int32)]
+
+
+class Outputs(C.Structure):
+    _fields_ = [("out", C.c_void_p), ("pflags", C.c_void_p), ("pnseg", C.c_void_p),
+                ("pterm", C.c_void_p), ("trace", C.c_void_p),
+                ("trace_cap", C.c_uint64), ("trace_count", C.c_void_p)]
+
+
+_lib = None
+
+SYMBOLS = ["nt_last_error", "nt_abi_version", "nt_model_create", "nt_model_destroy", "nt_add_surface",
+           "nt_add_material", "nt_add_csg_universe", "nt_add_cell", "nt_add_rect_array",
+           "nt_add_hex_array", "nt_set_root", "nt_build_opts_default", "nt_finalize",
+           "nt_model_info_get", "nt_material_cell_ids", "nt_bih_info", "nt_track",
+           "nt_track_states", "nt_track_host", "nt_find_cells", "nt_last_launch_count"]
+
+
+def lib():
+    """Load libnestrack.so (raises if it was not built: there is no fallback path)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} missing: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = C.CDLL(LIB_PATH)
+        vp, i32, u64, dp = C.c_void_p, C.c_int32, C.c_uint64, C.c_void_p
+        L.nt_last_error.restype = C.c_char_p
+        L.nt_model_create.argtypes = [C.POINTER(vp)]
+        L.nt_model_destroy.argtypes = [vp]
+        L.nt_add_surface.argtypes = [vp, i32, dp, i32, C.POINTER(i32)]
+        L.nt_add_material.argtypes = [vp, C.c_double, C.c_double, C.POINTER(i32)]
+        L.nt_add_csg_universe.argtypes = [vp, C.POINTER(i32)]
+        L.nt_add_cell.argtypes = [vp, i32, dp, i32, i32, i32, dp, C.POINTER(i32)]
+        L.nt_add_rect_array.argtypes = [vp, dp, dp, dp, dp, i32, C.POINTER(i32)]
+        L.nt_add_hex_array.argtypes = [vp, i32, dp, C.c_double, i32, C.c_double, C.c_double, i32, dp,
+                                       i32, C.POINTER(i32)]
+        L.nt_set_root.argtypes = [vp, i32]
+        L.nt_build_opts_default.argtypes = [C.POINTER(BuildOpts)]
+        L.nt_finalize.argtypes = [vp, C.POINTER(BuildOpts)]
+        L.nt_model_info_get.argtypes = [vp, C.POINTER(ModelInfo)]
+        L.nt_material_cell_ids.argtypes = [vp, dp, i32]
+        L.nt_bih_info.argtypes = [vp, i32, C.POINTER(i32), C.POINTER(i32), dp, i32, C.POINTER(i32)]
+        L.nt_track.argtypes = [vp, C.POINTER(Run), C.POINTER(Outputs), vp]
+        L.nt_track_states.argtypes = [vp, C.POINTER(Run), dp, C.POINTER(Outputs), vp]
+        L.nt_track_host.argtypes = [vp, C.POINTER(Run), dp, vp]
+        L.nt_find_cells.argtypes = [vp, dp, u64, dp, dp, vp]
+        L.nt_last_launch_count.argtypes = [vp]
+        _lib = L
+    return _lib
+
+
+def _check(st: int):
+    if st != 0:
+        raise NtError(st, lib().nt_last_error().decode())
+
+
+def _p(a: np.ndarray):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def _stream_handle(stream):
+    import torch
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return C.c_void_p(stream.cuda_stream)
+
+
+class Model:
+    """A nested CSG model: builder calls (nt_add_*), finalize, then tracking on one GPU."""
+
+    def __init__(self):
+        self.L = lib()
+        self.h = C.c_void_p()
+        _check(self.L.nt_model_create(C.byref(self.h)))
+        self.info = None
+        self.spec = None
+
+    def __del__(self):
+        try:
+            self.L.nt_model_destroy(self.h)
+        except Exception:
+            pass
+
+    # ---------------------------------------------------------------- builder
+    def add_surface(self, kind: str, coef, bc: str = "none") -> int:
+        c = np.zeros(4)
+        c[:len(coef)] = coef
+        i = C.c_int32()
+        _check(self.L.nt_add_surface(self.h, KIND[kind], _p(c), BC[bc], C.byref(i)))
+        return i.value
+
+    def add_material(self, sigma_t: float, sigma_a: float) -> int:
+        i = C.c_int32()
+        _check(self.L.nt_add_material(self.h, sigma_t, sigma_a, C.byref(i)))
+        return i.value
+
+    def add_csg_universe(self) -> int:
+        i = C.c_int32()
+        _check(self.L.nt_add_csg_universe(self.h, C.byref(i)))
+        return i.value
+
+    def add_cell(self, uid: int, halfspaces, material: int | None = None, fill: int | None = None,
+                 translation=None) -> int:
+        hs = np.asarray(halfspaces, dtype=np.int32)
+        tr = None if translation is None else np.asarray(translation, dtype=np.float64)
+        fk, f = (0, material) if material is not None else (1, fill)
+        i = C.c_int32()
+        _check(self.L.nt_add_cell(self.h, uid, _p(hs) if len(hs) else None, len(hs), fk, f,
+                                  _p(tr) if tr is not None else None, C.byref(i)))
+        return i.value
+
+    def add_rect_array(self, ll, pitch, shape, fill, outer: int = -1) -> int:
+        a = np.asarray(ll, dtype=np.float64)
+        p = np.asarray(pitch, dtype=np.float64)
+        s = np.asarray(shape, dtype=np.int32)
+        f = np.asarray(fill, dtype=np.int32)
+        i = C.c_int32()
+        _check(self.L.nt_add_rect_array(self.h, _p(a), _p(p), _p(s), _p(f), outer, C.byref(i)))
+        return i.value
+
+    def add_hex_array(self, orient: str, center, pitch: float, rings: int, fill, outer: int = -1,
+                      z_lower: float = 0.0, z_pitch: float = 0.0, nz: int = 0) -> int:
+        c = np.asarray(center, dtype=np.float64)
+        f = np.asarray(fill, dtype=np.int32)
+        i = C.c_int32()
+        _check(self.L.nt_add_hex_array(self.h, 0 if orient == "pointy" else 1, _p(c), pitch, rings,
+                                       z_lower, z_pitch, nz, _p(f), outer, C.byref(i)))
+        return i.value
+
+    def set_root(self, uid: int):
+        _check(self.L.nt_set_root(self.h, uid))
+
+    def finalize(self, device: int = 0, pseudo_array: bool = False, bih_max_leaf: int = 4):
+        o = BuildOpts()
+        self.L.nt_build_opts_default(C.byref(o))
+        o.device = device
+        o.pseudo_array = int(pseudo_array)
+        o.bih_max_leaf = bih_max_leaf
+        _check(self.L.nt_finalize(self.h, C.byref(o)))
+        inf = ModelInfo()
+        _check(self.L.nt_model_info_get(self.h, C.byref(inf)))
+        self.info = {k: getattr(inf, k) for k, _ in ModelInfo._fields_}
+        self.device = device
+        self.n_mc = inf.n_material_cells
+        self.out_len = inf.out_len
+        ids = np.zeros(max(self.n_mc, 1), dtype=np.int32)
+        _check(self.L.nt_material_cell_ids(self.h, _p(ids), self.n_mc))
+        self.mc_cell = ids[:self.n_mc]
+        return self
+
+    @classmethod
+    def from_spec(cls, spec: dict, device: int = 0, pseudo_array: bool = False,
+                  bih_max_leaf: int = 4) -> "Model":
+        """Build from a workloads spec dict (surfaces, materials, universes in list order)."""
+        m = cls()
+        m.spec = spec
+        for s in spec["surfaces"]:
+            m.add_surface(s["kind"], s["coef"], s["bc"])
+        for mt in spec["materials"]:
+            m.add_material(mt["sigma_t"], mt["sigma_a"])
+        for u in spec["universes"]:
+            if u["kind"] == "csg":
+                uid = m.add_csg_universe()
+                for c in u["cells"]:
+                    if "material" in c:
+                        m.add_cell(uid, c["hs"], material=c["material"])
+                    else:
+                        m.add_cell(uid, c["hs"], fill=c["fill"], translation=c.get("translation"))
+            elif u["kind"] == "rect":
+                m.add_rect_array(u["ll"], u["pitch"], u["shape"], u["fill"], u["outer"])
+            else:
+                m.add_hex_array(u["orient"], u["center"], u["pitch"], u["rings"], u["fill"], u["outer"],
+                                u["z_lower"], u["z_pitch"], u["nz"])
+        m.set_root(spec["root"])
+        return m.finalize(device=device, pseudo_array=pseudo_array, bih_max_leaf=bih_max_leaf)
+
+    def bih_info(self, uid: int):
+        nn, dep, cnt = C.c_int32(), C.c_int32(), C.c_int32()
+        _check(self.L.nt_bih_info(self.h, uid, C.byref(nn), C.byref(dep), None, 0, C.byref(cnt)))
+        cells = np.zeros(max(cnt.value, 1), dtype=np.int32)
+        _check(self.L.nt_bih_info(self.h, uid, C.byref(nn), C.byref(dep), _p(cells), cnt.value,
+                                  C.byref(cnt)))
+        return {"n_nodes": nn.value, "depth": dep.value, "leaf_cells": cells[:cnt.value]}
+
+    # ---------------------------------------------------------------- tracking
+    def make_run(self, n: int, seed: int, pid_begin: int = 0, lo=None, hi=None, max_segments: int = 0,
+                 tracker: str = "generic", trace: bool = False, block_dim: int = 0,
+                 blocks_per_sm: int = 0) -> Run:
+        r = Run()
+        r.seed, r.pid_begin, r.n = seed, pid_begin, n
+        src = (self.spec or {}).get("source", {"lo": [0, 0, 0], "hi": [0, 0, 0]})
+        lo = src["lo"] if lo is None else lo
+        hi = src["hi"] if hi is None else hi
+        for a in range(3):
+            r.src_lo[a], r.src_hi[a] = lo[a], hi[a]
+        r.max_segments = max_segments
+        r.tracker = TRACKER[tracker]
+        r.flags = NT_TRACE if trace else 0
+        r.block_dim, r.blocks_per_sm = block_dim, blocks_per_sm
+        return r
+
+    def track(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
+              max_segments: int = 0, tracker: str = "generic", pflags: bool = False,
+              trace_cap: int = 0, states=None, out=None, stream=None, block_dim: int = 0,
+              blocks_per_sm: int = 0, per_history: bool = False):
+        """Track histories [pid_begin, pid_begin+n) on this model's GPU (async on `stream`).
+        Returns a dict of device tensors: out (accumulated), pflags, trace, trace_count."""
+        import torch
+        dev = torch.device("cuda", self.device)
+        if out is None:
+            out = torch.zeros(self.out_len, dtype=torch.float64, device=dev)
+        res = {"out": out}
+        o = Outputs()
+        o.out = out.data_ptr()
+        if pflags:
+            pf = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+            o.pflags = pf.data_ptr()
+            res["pflags"] = pf
+        if per_history:
+            ps = torch.zeros(max(n, 1), dtype=torch.int32, device=dev)
+            pt = torch.zeros(max(n, 1), dtype=torch.uint8, device=dev)
+            o.pnseg, o.pterm = ps.data_ptr(), pt.data_ptr()
+            res["pnseg"], res["pterm"] = ps, pt
+        if trace_cap:
+            tr = torch.zeros(trace_cap * TRACE_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+            tc = torch.zeros(1, dtype=torch.int64, device=dev)
+            o.trace, o.trace_cap, o.trace_count = tr.data_ptr(), trace_cap, tc.data_ptr()
+            res["trace"], res["trace_count"] = tr, tc
+        run = self.make_run(n, seed, pid_begin, lo, hi, max_segments, tracker, bool(trace_cap),
+                            block_dim, blocks_per_sm)
+        sh = _stream_handle(stream)
+        if states is not None:
+            assert states.dtype == torch.float64 and states.is_cuda and tuple(states.shape) == (6, n)
+            states = states.contiguous()
+            res["_states"] = states
+            _check(self.L.nt_track_states(self.h, C.byref(run), C.c_void_p(states.data_ptr()),
+                                          C.byref(o), sh))
+        else:
+            _check(self.L.nt_track(self.h, C.byref(run), C.byref(o), sh))
+        return res
+
+    def track_host(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
+                   max_segments: int = 0, tracker: str = "generic", out: np.ndarray | None = None,
+                   stream=None, block_dim: int = 0, blocks_per_sm: int = 0) -> np.ndarray:
+        """End-to-end call with a HOST output buffer (synchronous)."""
+        if out is None:
+            out = np.zeros(self.out_len)
+        run = self.make_run(n, seed, pid_begin, lo, hi, max_segments, tracker, False, block_dim,
+                            blocks_per_sm)
+        _check(self.L.nt_track_host(self.h, C.byref(run), _p(out), _stream_handle(stream)))
+        return out
+
+    def find_cells(self, xyz, stream=None):
+        import torch
+        xyz = xyz.contiguous()
+        n = xyz.shape[1]
+        cell = torch.empty(n, dtype=torch.int32, device=xyz.device)
+        fl = torch.empty(n, dtype=torch.uint8, device=xyz.device)
+        _check(self.L.nt_find_cells(self.h, C.c_void_p(xyz.data_ptr()), n, C.c_void_p(cell.data_ptr()),
+                                    C.c_void_p(fl.data_ptr()), _stream_handle(stream)))
+        return cell, fl
+
+    def last_launch_count(self) -> int:
+        return self.L.nt_last_launch_count(self.h)
+
+    # ---------------------------------------------------------------- results
+    def unpack(self, out) -> dict:
+        o = out.detach().cpu().numpy() if hasattr(out, "detach") else np.asarray(out)
+        n = self.n_mc
+        return {"out": o, "len": o[:n], "exits": o[n:2 * n],
+                "counters": {k: int(o[2 * n + i]) for i, k in enumerate(COUNTERS)}}
+
+    @staticmethod
+    def trace_records(res) -> np.ndarray:
+        cnt = int(res["trace_count"].item())
+        buf = res["trace"].cpu().numpy()
+        cap = buf.size // TRACE_DTYPE.itemsize
+        assert cnt <= cap, f"trace overflow: {cnt} > {cap}"
+        t = buf[:cnt * TRACE_DTYPE.itemsize].view(TRACE_DTYPE)
+        return np.sort(t, order=["pid", "seg", "terminal"])
+
+
+def shard(n_total: int, rank: int, world: int) -> tuple[int, int]:
+    """Contiguous pid shard of rank g of G: [floor(gN/G), floor((g+1)N/G))."""
+    b = n_total * rank // world
+    e = n_total * (rank + 1) // world
+    return b, e - b
+
+
+def track_distributed(model: Model, n_total: int, seed: int, pid_begin: int = 0, group=None,
+                      tracker_fn=None, **kw):
+    """Multi-GPU tracking: each rank tracks its contiguous pid shard on its own GPU, then ONE
+    all-reduce (sum) of the packed fp64 [len | exits | counters] buffer combines the tallies.
+    `tracker_fn(n, pid_begin) -> out tensor` overrides the per-rank tracker (CPU tests)."""
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    b, n = shard(n_total, rank, world)
+    if tracker_fn is None:
+        out = model.track(n, seed=seed, pid_begin=pid_begin + b, **kw)["out"]
+    else:
+        out = tracker_fn(n, pid_begin + b)
+    if world > 1:
+        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+    return out

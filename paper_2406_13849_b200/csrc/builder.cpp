@@ -1,0 +1,565 @@
+// Host model builder: validation, universe bounding boxes, cell AABBs by truncation,
+// per-universe SAH bounding interval hierarchy, optional pseudo-array conversion, and
+// flattening into the device tables of nt_layout.hpp.
+//
+// Paper: CSG cells from surface half-spaces (§1); universes and arrays
+// (P:133-145); pseudo-array universes (§4.3 ST method); cell bounding boxes by
+// successive truncation; BIH construction with SAH over three equally spaced
+// candidate partitions per axis.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <functional>
+#include <map>
+#include <numeric>
+
+#include "nt_model.hpp"
+
+namespace nt {
+namespace {
+
+constexpr double kBig = 1e7;   // finite stand-in for "unbounded" in bounding boxes (cm)
+
+[[noreturn]] void fail(const char* fmt, long a = 0, long b = 0) {
+  char buf[256];
+  std::snprintf(buf, sizeof buf, fmt, a, b);
+  throw GeomError(buf);
+}
+
+bool finite(double v) { return std::isfinite(v); }
+
+// ---------------------------------------------------------------- validation
+int depth_below(const std::vector<HCell>& C, const std::vector<HUniv>& U, int u,
+                std::vector<int>& memo, std::vector<int>& state) {
+  if (state[u] == 1) fail("universe cycle through universe %ld", u);
+  if (state[u] == 2) return memo[u];
+  state[u] = 1;
+  int best = 0;
+  const HUniv& X = U[u];
+  if (X.kind == U_CSG) {
+    for (int c : X.cells) {
+      int d = C[c].fill_kind == 0 ? 1 : 1 + depth_below(C, U, C[c].fill, memo, state);
+      best = std::max(best, d);
+    }
+  } else {
+    for (size_t i = 0; i <= X.fill.size(); ++i) {
+      int f = i < X.fill.size() ? X.fill[i] : X.outer;
+      if (f < 0) continue;
+      best = std::max(best, 1 + depth_below(C, U, f, memo, state));
+    }
+  }
+  state[u] = 2;
+  memo[u] = best;
+  return best;
+}
+
+void validate(const std::vector<HSurf>& S, const std::vector<HMat>& M, const std::vector<HCell>& C,
+              const std::vector<HUniv>& U, int root, int& max_depth) {
+  const int ns = (int)S.size(), nm = (int)M.size(), nu = (int)U.size();
+  if (root < 0 || root >= nu) fail("root universe not set or out of range (%ld)", root);
+  for (int i = 0; i < ns; ++i) {
+    const HSurf& s = S[i];
+    for (double v : s.c) if (!finite(v)) fail("surface %ld has a non-finite coefficient", i);
+    if ((s.kind == S_CZ && !(s.c[2] > 0)) || (s.kind == S_SPHERE && !(s.c[3] > 0)))
+      fail("surface %ld: radius must be > 0", i);
+    if (s.kind == S_PLANE && s.c[0] == 0 && s.c[1] == 0 && s.c[2] == 0)
+      fail("surface %ld: zero plane normal", i);
+    if (s.bc == 2 && s.kind > S_PZ) fail("surface %ld: REFLECT only on PX/PY/PZ", i);
+  }
+  for (int i = 0; i < nm; ++i)
+    if (!finite(M[i].st) || !finite(M[i].sa) || M[i].st < 0 || M[i].sa < 0 || M[i].sa > M[i].st)
+      fail("material %ld: need 0 <= sigma_a <= sigma_t", i);
+  for (int i = 0; i < (int)C.size(); ++i) {
+    const HCell& c = C[i];
+    std::vector<int> ids = c.sid;
+    std::sort(ids.begin(), ids.end());
+    for (size_t k = 0; k < ids.size(); ++k) {
+      if (ids[k] < 0 || ids[k] >= ns) fail("cell %ld: surface reference out of range", i);
+      if (k && ids[k] == ids[k - 1]) fail("cell %ld references surface %ld twice", i, ids[k]);
+      if (S[ids[k]].bc != 0 && c.uid != root)
+        fail("surface %ld has a boundary condition but is used outside the root universe", ids[k]);
+    }
+    if (c.fill_kind == 0 && (c.fill < 0 || c.fill >= nm)) fail("cell %ld: bad material", i);
+    if (c.fill_kind == 1 && (c.fill < 0 || c.fill >= nu)) fail("cell %ld: bad fill universe", i);
+    for (double v : c.tr) if (!finite(v)) fail("cell %ld: non-finite translation", i);
+  }
+  for (int i = 0; i < nu; ++i) {
+    const HUniv& u = U[i];
+    if (u.kind == U_RECT) {
+      if (!(u.p[0] > 0) || !(u.p[1] > 0) || u.p[2] < 0) fail("rect array %ld: bad pitch", i);
+      for (int a = 0; a < 3; ++a) {
+        if (u.n[a] < 1) fail("rect array %ld: bad shape", i);
+        if (!finite(u.ll[a])) fail("rect array %ld: bad lower-left", i);
+      }
+    } else if (u.kind == U_HEX) {
+      if (!(u.pitch > 0) || u.rings < 1 || u.zp < 0 || (u.zp > 0 && u.nz < 1))
+        fail("hex array %ld: bad parameters", i);
+    }
+    if (u.kind != U_CSG) {
+      for (int f : u.fill) if (f < 0 || f >= nu) fail("array %ld: bad fill universe", i);
+      if (u.outer < -1 || u.outer >= nu) fail("array %ld: bad outer universe", i);
+    }
+  }
+  std::vector<int> memo(nu, 0), state(nu, 0);
+  max_depth = depth_below(C, U, root, memo, state);
+  if (max_depth > kMaxDepth) fail("nesting depth %ld exceeds %ld", max_depth, kMaxDepth);
+  if (max_depth < 1) fail("root universe has no material cells");
+}
+
+// ---------------------------------------------------------------- bounding boxes (O23)
+Aabb truncate(const std::vector<HSurf>& S, const HCell& c, const Aabb& start) {
+  Aabb b = start;
+  for (size_t h = 0; h < c.sid.size(); ++h) {
+    const HSurf& s = S[c.sid[h]];
+    const bool neg = c.sense[h] == 0;
+    if (s.kind <= S_PZ) {
+      const int a = s.kind;
+      if (neg) b.hi[a] = std::min(b.hi[a], s.c[0]);
+      else b.lo[a] = std::max(b.lo[a], s.c[0]);
+    } else if (s.kind == S_CZ && neg) {
+      for (int a = 0; a < 2; ++a) {
+        b.lo[a] = std::max(b.lo[a], s.c[a] - s.c[2]);
+        b.hi[a] = std::min(b.hi[a], s.c[a] + s.c[2]);
+      }
+    } else if (s.kind == S_SPHERE && neg) {
+      for (int a = 0; a < 3; ++a) {
+        b.lo[a] = std::max(b.lo[a], s.c[a] - s.c[3]);
+        b.hi[a] = std::min(b.hi[a], s.c[a] + s.c[3]);
+      }
+    }
+  }
+  return b;
+}
+
+Aabb shift(const Aabb& b, const double t[3]) {
+  Aabb r = b;
+  for (int a = 0; a < 3; ++a) { r.lo[a] -= t[a]; r.hi[a] -= t[a]; }
+  return r;
+}
+
+void topo_order(const std::vector<HCell>& C, const std::vector<HUniv>& U, int u,
+                std::vector<int>& seen, std::vector<int>& post) {
+  if (seen[u]) return;
+  seen[u] = 1;
+  const HUniv& X = U[u];
+  if (X.kind == U_CSG) {
+    for (int c : X.cells) if (C[c].fill_kind == 1) topo_order(C, U, C[c].fill, seen, post);
+  } else {
+    for (int f : X.fill) topo_order(C, U, f, seen, post);
+    if (X.outer >= 0) topo_order(C, U, X.outer, seen, post);
+  }
+  post.push_back(u);
+}
+
+std::vector<Aabb> universe_boxes(const std::vector<HSurf>& S, const std::vector<HCell>& C,
+                                 const std::vector<HUniv>& U, int root) {
+  std::vector<Aabb> box(U.size(), Aabb::empty());
+  std::vector<int> seen(U.size(), 0), post;
+  topo_order(C, U, root, seen, post);
+  std::reverse(post.begin(), post.end());   // parents before children
+  Aabb big{{-kBig, -kBig, -kBig}, {kBig, kBig, kBig}};
+  if (U[root].kind == U_CSG) {
+    for (int c : U[root].cells) {
+      Aabb a = truncate(S, C[c], big);
+      if (a.valid()) box[root].grow(a);
+    }
+  } else {
+    box[root] = big;
+  }
+  for (int u : post) {
+    if (!box[u].valid()) continue;
+    const HUniv& X = U[u];
+    if (X.kind == U_CSG) {
+      for (int c : X.cells) {
+        if (C[c].fill_kind != 1) continue;
+        Aabb a = truncate(S, C[c], box[u]);
+        if (a.valid()) box[C[c].fill].grow(shift(a, C[c].tr));
+      }
+    } else {
+      Aabb t;
+      if (X.kind == U_RECT) {
+        for (int a = 0; a < 3; ++a) { t.lo[a] = -0.5 * X.p[a]; t.hi[a] = 0.5 * X.p[a]; }
+        if (X.is2d) { t.lo[2] = box[u].lo[2]; t.hi[2] = box[u].hi[2]; }
+      } else {
+        const double rho = X.pitch / std::sqrt(3.0) * (1.0 + 1e-9);
+        t.lo[0] = t.lo[1] = -rho;
+        t.hi[0] = t.hi[1] = rho;
+        if (X.nz > 0) { t.lo[2] = -0.5 * X.zp; t.hi[2] = 0.5 * X.zp; }
+        else { t.lo[2] = box[u].lo[2]; t.hi[2] = box[u].hi[2]; }
+      }
+      for (int f : X.fill) box[f].grow(t);
+      if (X.outer >= 0) box[X.outer].grow(t);
+    }
+  }
+  return box;
+}
+
+Aabb pad(Aabb b) {
+  for (int a = 0; a < 3; ++a) {
+    b.lo[a] -= 1e-9 * (1.0 + std::fabs(b.lo[a]));
+    b.hi[a] += 1e-9 * (1.0 + std::fabs(b.hi[a]));
+  }
+  return b;
+}
+
+double area(const Aabb& b) {
+  double e[3];
+  for (int a = 0; a < 3; ++a) e[a] = std::max(0.0, b.hi[a] - b.lo[a]);
+  return 2.0 * (e[0] * e[1] + e[1] * e[2] + e[0] * e[2]);
+}
+
+// ---------------------------------------------------------------- BIH
+struct BihBuilder {
+  std::vector<BihNode>& nodes;
+  std::vector<int32_t>& leaf;
+  const std::vector<Aabb>& cb;   // per global cell (padded)
+  int max_leaf;
+  double ct, ci;
+  int depth = 0;
+
+  void make_leaf(int node, const std::vector<int>& idx) {
+    nodes[node].meta = -1 - (int)idx.size();
+    nodes[node].a = (int)leaf.size();
+    nodes[node].lmax = nodes[node].rmin = 0;
+    for (int c : idx) leaf.push_back(c);
+  }
+
+  void fill(int node, std::vector<int> idx, int d) {
+    depth = std::max(depth, d);
+    if ((int)idx.size() <= max_leaf || d >= 40) { make_leaf(node, idx); return; }
+    Aabb nb = Aabb::empty(), cen = Aabb::empty();
+    for (int c : idx) {
+      nb.grow(cb[c]);
+      Aabb p;
+      for (int a = 0; a < 3; ++a) p.lo[a] = p.hi[a] = 0.5 * (cb[c].lo[a] + cb[c].hi[a]);
+      cen.grow(p);
+    }
+    auto centre = [&](int c, int a) { return 0.5 * (cb[c].lo[a] + cb[c].hi[a]); };
+    const double sa_node = std::max(area(nb), 1e-300);
+    double best = 1e308;
+    int bax = -1;
+    double bpos = 0;
+    // SAH: three equally spaced candidate partitions per axis
+    for (int a = 0; a < 3; ++a) {
+      const double ext = cen.hi[a] - cen.lo[a];
+      if (!(ext > 0)) continue;
+      for (int k = 1; k <= 3; ++k) {
+        const double pos = cen.lo[a] + 0.25 * k * ext;
+        Aabb L = Aabb::empty(), R = Aabb::empty();
+        int nl = 0, nr = 0;
+        for (int c : idx) {
+          if (centre(c, a) < pos) { L.grow(cb[c]); ++nl; } else { R.grow(cb[c]); ++nr; }
+        }
+        if (!nl || !nr) continue;
+        const double cost = ct + ci * (area(L) * nl + area(R) * nr) / sa_node;
+        if (cost < best) { best = cost; bax = a; bpos = pos; }
+      }
+    }
+    std::vector<int> li, ri;
+    if (bax < 0) {   // degenerate: median split on the widest centroid axis
+      int a = 0;
+      for (int k = 1; k < 3; ++k) if (cen.hi[k] - cen.lo[k] > cen.hi[a] - cen.lo[a]) a = k;
+      if (!(cen.hi[a] > cen.lo[a])) { make_leaf(node, idx); return; }
+      std::sort(idx.begin(), idx.end(), [&](int x, int y) { return centre(x, a) < centre(y, a); });
+      li.assign(idx.begin(), idx.begin() + idx.size() / 2);
+      ri.assign(idx.begin() + idx.size() / 2, idx.end());
+      bax = a;
+    } else {
+      for (int c : idx) (centre(c, bax) < bpos ? li : ri).push_back(c);
+    }
+    double lmax = -1e308, rmin = 1e308;
+    for (int c : li) lmax = std::max(lmax, cb[c].hi[bax]);
+    for (int c : ri) rmin = std::min(rmin, cb[c].lo[bax]);
+    const int a0 = (int)nodes.size();
+    nodes.push_back({});
+    nodes.push_back({});
+    nodes[node].meta = bax;
+    nodes[node].a = a0;
+    nodes[node].lmax = lmax;
+    nodes[node].rmin = rmin;
+    fill(a0, li, d + 1);
+    fill(a0 + 1, ri, d + 1);
+  }
+};
+
+// ---------------------------------------------------------------- pseudo-arrays
+// Replace every rect/hex array universe by a CSG universe of explicit tile cells (same uid,
+// same depth), covering the in-lattice tiles and every out-of-lattice tile that meets the
+// universe bounding box; out-of-lattice tiles take `outer` (skipped when there is none).
+void convert_pseudo_arrays(std::vector<HSurf>& S, std::vector<HCell>& C, std::vector<HUniv>& U,
+                           const std::vector<Aabb>& box) {
+  for (int u = 0; u < (int)U.size(); ++u) {
+    HUniv& X = U[u];
+    if (X.kind == U_CSG || !box[u].valid()) continue;
+    if (X.kind == U_RECT) {
+      const int na = X.is2d ? 2 : 3;
+      int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
+      std::vector<int> plane0[3];
+      for (int a = 0; a < na; ++a) {
+        lo[a] = std::min(0, (int)std::floor((box[u].lo[a] - X.ll[a]) / X.p[a]) - 1);
+        hi[a] = std::max(X.n[a] - 1, (int)std::floor((box[u].hi[a] - X.ll[a]) / X.p[a]) + 1);
+        for (int i = lo[a]; i <= hi[a] + 1; ++i) {   // e(i) = LL + i p  (O8: mul then add)
+          HSurf s{a, 0, {X.ll[a] + (double)i * X.p[a], 0, 0, 0}};
+          plane0[a].push_back((int)S.size());
+          S.push_back(s);
+        }
+      }
+      HUniv Y;
+      Y.kind = U_CSG;
+      for (int k = lo[2]; k <= hi[2]; ++k)
+        for (int j = lo[1]; j <= hi[1]; ++j)
+          for (int i = lo[0]; i <= hi[0]; ++i) {
+            const int ijk[3] = {i, j, k};
+            bool in = true;
+            for (int a = 0; a < na; ++a) in = in && ijk[a] >= 0 && ijk[a] < X.n[a];
+            const int d = in ? X.fill[i + X.n[0] * (j + X.n[1] * (na == 3 ? k : 0))] : X.outer;
+            if (d < 0) continue;
+            HCell c;
+            c.uid = u;
+            c.fill_kind = 1;
+            c.fill = d;
+            for (int a = 0; a < 3; ++a)
+              c.tr[a] = a < na ? X.ll[a] + ((double)ijk[a] + 0.5) * X.p[a] : 0.0;
+            for (int a = 0; a < na; ++a) {
+              c.sid.push_back(plane0[a][ijk[a] - lo[a]]);
+              c.sense.push_back(1);
+              c.sid.push_back(plane0[a][ijk[a] - lo[a] + 1]);
+              c.sense.push_back(0);
+            }
+            Y.cells.push_back((int)C.size());
+            C.push_back(c);
+          }
+      X = Y;
+    } else {   // HEX: tile (q,r) = intersection over k of m_k - 1/2 <= t_k < m_k + 1/2 (O9)
+      const double H = kHexH, p = X.pitch, pH = p * H;
+      double n[3][2];
+      if (X.orient == 0) { double v[3][2] = {{1.0, 0.0}, {0.5, H}, {-0.5, H}}; std::copy(&v[0][0], &v[0][0] + 6, &n[0][0]); }
+      else { double v[3][2] = {{H, 0.5}, {0.0, 1.0}, {-H, 0.5}}; std::copy(&v[0][0], &v[0][0] + 6, &n[0][0]); }
+      double a1[2], a2[2];
+      if (X.orient == 0) { a1[0] = p; a1[1] = 0.0; a2[0] = p * 0.5; a2[1] = pH; }
+      else { a1[0] = pH; a1[1] = p * 0.5; a2[0] = 0.0; a2[1] = p; }
+      const int R = X.rings - 1;
+      const double reach = std::max({std::fabs(box[u].lo[0] - X.C[0]), std::fabs(box[u].hi[0] - X.C[0]),
+                                     std::fabs(box[u].lo[1] - X.C[1]), std::fabs(box[u].hi[1] - X.C[1])});
+      const int W = std::max(R, (int)std::ceil(reach / (0.5 * p)) + 2);
+      // collect tiles whose hexagon meets the box (centre within box + circumradius)
+      const double rho = p / std::sqrt(3.0) + 1e-9;
+      std::vector<std::array<int, 2>> tiles;
+      for (int r = -W; r <= W; ++r)
+        for (int q = -W; q <= W; ++q) {
+          const double cx = X.C[0] + ((double)q * a1[0] + (double)r * a2[0]);
+          const double cy = X.C[1] + ((double)q * a1[1] + (double)r * a2[1]);
+          const bool inl = std::max({std::abs(q), std::abs(r), std::abs(q + r)}) <= R;
+          if (inl || (cx + rho >= box[u].lo[0] && cx - rho <= box[u].hi[0] && cy + rho >= box[u].lo[1] &&
+                      cy - rho <= box[u].hi[1]))
+            tiles.push_back({q, r});
+        }
+      // planes n_k . x = n_k . C + p * b for half-integer b (2b integer key), family order
+      std::map<std::pair<int, int>, int> plane;
+      auto m_of = [](int q, int r, int k) {
+        return k == 0 ? (double)q + (double)r * 0.5
+                      : (k == 1 ? (double)q * 0.5 + (double)r : -((double)q * 0.5) + (double)r * 0.5);
+      };
+      for (int k = 0; k < 3; ++k) {
+        std::vector<int> keys;
+        for (auto& t : tiles) {
+          const double m = m_of(t[0], t[1], k);
+          keys.push_back((int)std::lround(2.0 * (m - 0.5)));
+          keys.push_back((int)std::lround(2.0 * (m + 0.5)));
+        }
+        std::sort(keys.begin(), keys.end());
+        keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+        for (int key : keys) {
+          HSurf s{S_PLANE, 0, {n[k][0], n[k][1], 0.0,
+                               (n[k][0] * X.C[0] + n[k][1] * X.C[1]) + p * (0.5 * key)}};
+          plane[{k, key}] = (int)S.size();
+          S.push_back(s);
+        }
+      }
+      const int nzl = X.nz > 0 ? X.nz : 1;
+      int klo = 0, khi = 0;
+      std::vector<int> zpl;
+      if (X.nz > 0) {
+        klo = std::min(0, (int)std::floor((box[u].lo[2] - X.zlo) / X.zp) - 1);
+        khi = std::max(X.nz - 1, (int)std::floor((box[u].hi[2] - X.zlo) / X.zp) + 1);
+        for (int k = klo; k <= khi + 1; ++k) {
+          HSurf s{S_PZ, 0, {X.zlo + (double)k * X.zp, 0, 0, 0}};
+          zpl.push_back((int)S.size());
+          S.push_back(s);
+        }
+      }
+      // O9 fill index of in-lattice tiles
+      std::map<std::pair<int, int>, int> order;
+      int cnt = 0;
+      for (int r = -R; r <= R; ++r)
+        for (int q = -R; q <= R; ++q)
+          if (std::max({std::abs(q), std::abs(r), std::abs(q + r)}) <= R) order[{q, r}] = cnt++;
+      HUniv Y;
+      Y.kind = U_CSG;
+      for (int kz = klo; kz <= khi; ++kz)
+        for (auto& t : tiles) {
+          const int q = t[0], r = t[1];
+          auto it = order.find({q, r});
+          const bool in = it != order.end() && (X.nz == 0 || (kz >= 0 && kz < X.nz));
+          const int d = in ? X.fill[it->second + (X.nz > 0 ? kz * (int)(X.fill.size() / nzl) : 0)] : X.outer;
+          if (d < 0) continue;
+          HCell c;
+          c.uid = u;
+          c.fill_kind = 1;
+          c.fill = d;
+          c.tr[0] = X.C[0] + ((double)q * a1[0] + (double)r * a2[0]);
+          c.tr[1] = X.C[1] + ((double)q * a1[1] + (double)r * a2[1]);
+          c.tr[2] = X.nz > 0 ? X.zlo + ((double)kz + 0.5) * X.zp : 0.0;
+          for (int k = 0; k < 3; ++k) {
+            const double m = m_of(q, r, k);
+            c.sid.push_back(plane[{k, (int)std::lround(2.0 * (m - 0.5))}]);
+            c.sense.push_back(1);
+            c.sid.push_back(plane[{k, (int)std::lround(2.0 * (m + 0.5))}]);
+            c.sense.push_back(0);
+          }
+          if (X.nz > 0) {
+            c.sid.push_back(zpl[kz - klo]);
+            c.sense.push_back(1);
+            c.sid.push_back(zpl[kz - klo + 1]);
+            c.sense.push_back(0);
+          }
+          Y.cells.push_back((int)C.size());
+          C.push_back(c);
+        }
+      X = Y;
+    }
+  }
+}
+
+double surf_tol(const HSurf& s) {   // O16: 1e-10 x |grad f| scale (same formula as documented)
+  if (s.kind == S_CZ) return kFlagDist * (2.0 * s.c[2]);
+  if (s.kind == S_SPHERE) return kFlagDist * (2.0 * s.c[3]);
+  if (s.kind == S_PLANE) return kFlagDist * std::sqrt((s.c[0] * s.c[0] + s.c[1] * s.c[1]) + s.c[2] * s.c[2]);
+  return kFlagDist;
+}
+
+}  // namespace
+
+void build_rect_tables(const std::vector<HSurf>& S, const std::vector<HMat>& M,
+                       const std::vector<HCell>& C, const std::vector<HUniv>& U, int root,
+                       Flat& F);   // rect_spec.cpp
+
+void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
+                const std::vector<HCell>& c_in, const std::vector<HUniv>& u_in, int root,
+                const BuildOpts& opts, Flat& F) {
+  F = Flat();
+  int depth = 0;
+  validate(s_in, M, c_in, u_in, root, depth);
+  std::vector<HSurf> S = s_in;
+  std::vector<HCell> C = c_in;
+  std::vector<HUniv> U = u_in;
+  std::vector<Aabb> ubox = universe_boxes(S, C, U, root);
+  if (opts.pseudo) {
+    convert_pseudo_arrays(S, C, U, ubox);
+    ubox = universe_boxes(S, C, U, root);
+  } else {
+    build_rect_tables(S, M, C, U, root, F);
+  }
+  F.root = root;
+  F.max_depth = depth;
+
+  // surfaces
+  for (const HSurf& s : S) {
+    DSurf d{};
+    if (s.kind <= S_PZ) d.c[0] = s.c[0];
+    else if (s.kind == S_PLANE) for (int k = 0; k < 4; ++k) d.c[k] = s.c[k];
+    else if (s.kind == S_CZ) { d.c[0] = s.c[0]; d.c[1] = s.c[1]; d.c[2] = s.c[2] * s.c[2]; }
+    else { d.c[0] = s.c[0]; d.c[1] = s.c[1]; d.c[2] = s.c[2]; d.c[3] = s.c[3] * s.c[3]; }
+    F.surf.push_back(d);
+    F.surf_tol.push_back(surf_tol(s));
+    F.surf_meta.push_back((uint8_t)(s.kind | (s.bc << 4)));
+  }
+  // cells: half-spaces sorted by surface id (O13), material-cell bins in cell-id order (O20)
+  F.cell_hs.push_back(0);
+  for (int i = 0; i < (int)C.size(); ++i) {
+    const HCell& c = C[i];
+    std::vector<int> o(c.sid.size());
+    std::iota(o.begin(), o.end(), 0);
+    std::sort(o.begin(), o.end(), [&](int a, int b) { return c.sid[a] < c.sid[b]; });
+    for (int k : o) F.hs.push_back(hs_pack(c.sid[k], S[c.sid[k]].kind, c.sense[k]));
+    F.cell_hs.push_back((int32_t)F.hs.size());
+    if (c.fill_kind == 0) {
+      F.cell_fill.push_back(F.n_mc++);
+      const HMat& m = M[c.fill];
+      F.mc_st.push_back(m.st);
+      F.mc_pabs.push_back(m.st > 0.0 ? m.sa / m.st : 0.0);
+      F.mc_cell.push_back(i);
+    } else {
+      F.cell_fill.push_back(-1 - c.fill);
+    }
+    for (int a = 0; a < 3; ++a) F.cell_tr.push_back(c.tr[a]);
+  }
+  // cell AABBs by truncation of the universe box, padded
+  std::vector<Aabb> cb(C.size(), Aabb::empty());
+  for (int u = 0; u < (int)U.size(); ++u)
+    if (U[u].kind == U_CSG)
+      for (int c : U[u].cells) {
+        Aabb a = ubox[u].valid() ? truncate(S, C[c], ubox[u])
+                                 : Aabb{{-kBig, -kBig, -kBig}, {kBig, kBig, kBig}};
+        if (!a.valid()) a = ubox[u].valid() ? ubox[u] : Aabb{{0, 0, 0}, {0, 0, 0}};
+        cb[c] = pad(a);
+      }
+  // universes
+  F.bih_depth.assign(U.size(), 0);
+  for (int u = 0; u < (int)U.size(); ++u) {
+    const HUniv& X = U[u];
+    DUniv d{};
+    d.kind = X.kind;
+    d.outer = X.outer;
+    d.fill_off = (int32_t)F.fills.size();
+    if (X.kind == U_CSG) {
+      BihBuilder B{F.bih, F.bih_leaf, cb, std::max(1, opts.max_leaf), opts.ct, opts.ci};
+      const int node = (int)F.bih.size();
+      F.bih.push_back({});
+      B.fill(node, X.cells, 0);
+      F.bih_depth[u] = B.depth;
+      d.i0 = node;
+      d.i1 = X.cells.empty() ? 0 : X.cells.front();
+      d.i2 = (int)X.cells.size();
+    } else if (X.kind == U_RECT) {
+      d.i0 = X.n[0]; d.i1 = X.n[1]; d.i2 = X.is2d ? 1 : X.n[2];
+      d.is2d = X.is2d;
+      for (int a = 0; a < 3; ++a) { d.d[a] = X.ll[a]; d.d[3 + a] = X.p[a]; }
+      for (int f : X.fill) F.fills.push_back(f);
+    } else {
+      const double H = kHexH, p = X.pitch;
+      const int R = X.rings - 1, W = 2 * R + 1;
+      d.i0 = R; d.i1 = X.zp > 0 ? X.nz : 0; d.i2 = X.orient;
+      d.ntile = W * W;
+      d.d[0] = X.C[0]; d.d[1] = X.C[1]; d.d[2] = p; d.d[3] = p * H;
+      d.d[4] = X.zlo; d.d[5] = X.zp;
+      if (X.orient == 0) {
+        d.d[6] = p; d.d[7] = 0.0; d.d[8] = p * 0.5; d.d[9] = d.d[3];
+        const double nv[6] = {1.0, 0.0, 0.5, H, -0.5, H};
+        for (int k = 0; k < 6; ++k) d.d[10 + k] = nv[k];
+      } else {
+        d.d[6] = d.d[3]; d.d[7] = p * 0.5; d.d[8] = 0.0; d.d[9] = p;
+        const double nv[6] = {H, 0.5, 0.0, 1.0, -H, 0.5};
+        for (int k = 0; k < 6; ++k) d.d[10 + k] = nv[k];
+      }
+      const int nzl = d.i1 > 0 ? d.i1 : 1;
+      const int per = (int)X.fill.size() / nzl;
+      std::vector<int32_t> map(W * W, -1);
+      int cnt = 0;
+      for (int r = -R; r <= R; ++r)
+        for (int q = -R; q <= R; ++q)
+          if (std::max({std::abs(q), std::abs(r), std::abs(q + r)}) <= R) map[(r + R) * W + (q + R)] = cnt++;
+      if (cnt != per) fail("hex array %ld: fill has the wrong length", u);
+      for (int kz = 0; kz < nzl; ++kz)
+        for (int e = 0; e < W * W; ++e) F.fills.push_back(map[e] < 0 ? -1 : X.fill[kz * per + map[e]]);
+    }
+    F.univ.push_back(d);
+  }
+  if (F.bih.empty()) F.bih.push_back({});
+  if (F.bih_leaf.empty()) F.bih_leaf.push_back(0);
+  if (F.fills.empty()) F.fills.push_back(-1);
+  if (F.hs.empty()) F.hs.push_back(0);
+  if (F.mc_st.empty()) fail("model has no material cells");
+}
+
+}  // namespace nt

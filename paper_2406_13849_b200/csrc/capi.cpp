@@ -1,0 +1,479 @@
+// extern "C" boundary of libnestrack.so (include/nestrack.h): argument checking, status
+// codes, thread-local error text, the device copy of the model, and kernel launches.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/nestrack.h"
+#include "nt_model.hpp"
+
+#include "nt_kernels.hpp"
+
+using namespace nt;
+
+static thread_local std::string g_err;
+
+static nt_status err(nt_status s, const std::string& msg) {
+  g_err = msg;
+  return s;
+}
+static nt_status cuda_err(cudaError_t e, const char* where) {
+  return err(NT_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+constexpr int kSlots = 64;
+
+struct nt_model {
+  std::vector<HSurf> s;
+  std::vector<HMat> m;
+  std::vector<HCell> c;
+  std::vector<HUniv> u;
+  int root = -1;
+  bool finalized = false;
+  BuildOpts opts;
+  Flat F;
+  // device
+  int device = -1;
+  void* blob = nullptr;
+  size_t blob_bytes = 0;
+  DevGeom g{};
+  RectGeom rg{};
+  unsigned long long* counters = nullptr;   // kSlots work counters
+  std::atomic<unsigned> slot{0};
+  double* host_scratch_dev = nullptr;       // nt_track_host device output
+  size_t host_scratch_len = 0;
+  std::mutex host_mu;
+  int last_launches = 0;
+};
+
+// Coefficients of the spec'd transcendentals (reading R-T), computed with IEEE double ops.
+static void coef_table(double* c) {
+  for (int k = 0; k <= 11; ++k) c[k] = 1.0 / (double)(2 * k + 1);
+  double fact[20];
+  fact[0] = 1.0;
+  for (int k = 1; k < 20; ++k) fact[k] = fact[k - 1] * (double)k;
+  for (int k = 1; k <= 9; ++k) {
+    const double sk = 1.0 / fact[2 * k + 1], ck = 1.0 / fact[2 * k];
+    c[12 + k - 1] = (k & 1) ? -sk : sk;
+    c[21 + k - 1] = (k & 1) ? -ck : ck;
+  }
+}
+
+template <class T>
+static size_t place(std::vector<char>& blob, const std::vector<T>& v) {
+  size_t off = (blob.size() + 255) & ~size_t(255);
+  blob.resize(off + v.size() * sizeof(T));
+  if (!v.empty()) std::memcpy(blob.data() + off, v.data(), v.size() * sizeof(T));
+  return off;
+}
+
+extern "C" {
+
+const char* nt_last_error(void) { return g_err.c_str(); }
+int32_t nt_abi_version(void) { return NT_ABI_VERSION; }
+
+nt_status nt_model_create(nt_model** out) {
+  if (!out) return err(NT_E_ARG, "nt_model_create: out is NULL");
+  *out = new (std::nothrow) nt_model();
+  if (!*out) return err(NT_E_NOMEM, "nt_model_create: out of host memory");
+  return NT_OK;
+}
+
+void nt_model_destroy(nt_model* m) {
+  if (!m) return;
+  if (m->blob || m->counters || m->host_scratch_dev) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(m->device);
+    if (m->blob) cudaFree(m->blob);
+    if (m->counters) cudaFree(m->counters);
+    if (m->host_scratch_dev) cudaFree(m->host_scratch_dev);
+    cudaSetDevice(prev);
+  }
+  delete m;
+}
+
+#define CHECK_BUILDER(m)                                                        \
+  do {                                                                          \
+    if (!(m)) return err(NT_E_ARG, std::string(__func__) + ": model is NULL");  \
+    if ((m)->finalized) return err(NT_E_ORDER, std::string(__func__) + ": model already finalized"); \
+  } while (0)
+
+nt_status nt_add_surface(nt_model* m, nt_surface_kind kind, const double* coef, nt_bc bc, int32_t* id) {
+  CHECK_BUILDER(m);
+  if (!coef) return err(NT_E_ARG, "nt_add_surface: coef is NULL");
+  if ((int)kind < 0 || (int)kind > NT_SPHERE) return err(NT_E_ARG, "nt_add_surface: bad kind");
+  if ((int)bc < 0 || (int)bc > NT_BC_REFLECT) return err(NT_E_ARG, "nt_add_surface: bad bc");
+  HSurf s{(int)kind, (int)bc, {0, 0, 0, 0}};
+  const int nco = kind <= NT_PZ ? 1 : (kind == NT_CZ ? 3 : 4);
+  for (int i = 0; i < nco; ++i) s.c[i] = coef[i];
+  m->s.push_back(s);
+  if (id) *id = (int32_t)m->s.size() - 1;
+  return NT_OK;
+}
+
+nt_status nt_add_material(nt_model* m, double st, double sa, int32_t* id) {
+  CHECK_BUILDER(m);
+  m->m.push_back({st, sa});
+  if (id) *id = (int32_t)m->m.size() - 1;
+  return NT_OK;
+}
+
+nt_status nt_add_csg_universe(nt_model* m, int32_t* uid) {
+  CHECK_BUILDER(m);
+  HUniv u;
+  u.kind = U_CSG;
+  m->u.push_back(u);
+  if (uid) *uid = (int32_t)m->u.size() - 1;
+  return NT_OK;
+}
+
+nt_status nt_add_cell(nt_model* m, int32_t uid, const int32_t* hs, int32_t n, nt_fill_kind fk,
+                      int32_t fill, const double tr[3], int32_t* cell_id) {
+  CHECK_BUILDER(m);
+  if (uid < 0 || uid >= (int)m->u.size()) return err(NT_E_ID, "nt_add_cell: universe id out of range");
+  if (m->u[uid].kind != U_CSG) return err(NT_E_ARG, "nt_add_cell: universe is not a CSG universe");
+  if (n < 0 || (n > 0 && !hs)) return err(NT_E_ARG, "nt_add_cell: bad half-space list");
+  if ((int)fk != 0 && (int)fk != 1) return err(NT_E_ARG, "nt_add_cell: bad fill kind");
+  HCell c;
+  c.uid = uid;
+  for (int i = 0; i < n; ++i) {
+    if (hs[i] == 0) return err(NT_E_ARG, "nt_add_cell: half-space 0 is invalid (use +-(surf+1))");
+    c.sid.push_back((hs[i] > 0 ? hs[i] : -hs[i]) - 1);
+    c.sense.push_back(hs[i] > 0 ? 1 : 0);
+  }
+  c.fill_kind = (int)fk;
+  c.fill = fill;
+  for (int a = 0; a < 3; ++a) c.tr[a] = tr ? tr[a] : 0.0;
+  m->c.push_back(c);
+  m->u[uid].cells.push_back((int)m->c.size() - 1);
+  if (cell_id) *cell_id = (int32_t)m->c.size() - 1;
+  return NT_OK;
+}
+
+nt_status nt_add_rect_array(nt_model* m, const double ll[3], const double p[3], const int32_t shape[3],
+                            const int32_t* fill, int32_t outer, int32_t* uid) {
+  CHECK_BUILDER(m);
+  if (!ll || !p || !shape || !fill) return err(NT_E_ARG, "nt_add_rect_array: NULL argument");
+  HUniv u;
+  u.kind = U_RECT;
+  for (int a = 0; a < 3; ++a) { u.ll[a] = ll[a]; u.p[a] = p[a]; u.n[a] = shape[a]; }
+  u.is2d = p[2] == 0.0;
+  if (u.is2d) u.n[2] = 1;
+  for (int a = 0; a < 3; ++a)
+    if (u.n[a] < 1 || u.n[a] > (1 << 20)) return err(NT_E_GEOMETRY, "nt_add_rect_array: bad shape");
+  const long n = (long)u.n[0] * u.n[1] * u.n[2];
+  u.fill.assign(fill, fill + n);
+  u.outer = outer;
+  m->u.push_back(u);
+  if (uid) *uid = (int32_t)m->u.size() - 1;
+  return NT_OK;
+}
+
+nt_status nt_add_hex_array(nt_model* m, nt_hex_orient orient, const double center[2], double pitch,
+                           int32_t rings, double zlo, double zp, int32_t nz, const int32_t* fill,
+                           int32_t outer, int32_t* uid) {
+  CHECK_BUILDER(m);
+  if (!center || !fill) return err(NT_E_ARG, "nt_add_hex_array: NULL argument");
+  if ((int)orient != 0 && (int)orient != 1) return err(NT_E_ARG, "nt_add_hex_array: bad orientation");
+  if (rings < 1 || rings > 1000) return err(NT_E_GEOMETRY, "nt_add_hex_array: bad ring count");
+  HUniv u;
+  u.kind = U_HEX;
+  u.orient = (int)orient;
+  u.C[0] = center[0];
+  u.C[1] = center[1];
+  u.pitch = pitch;
+  u.rings = rings;
+  u.zlo = zlo;
+  u.zp = zp;
+  u.nz = zp > 0 ? nz : 0;
+  if (zp > 0 && nz < 1) return err(NT_E_GEOMETRY, "nt_add_hex_array: nz must be >= 1 with z_pitch > 0");
+  const long ntile = 1 + 3L * rings * (rings - 1);
+  u.fill.assign(fill, fill + ntile * (u.nz > 0 ? u.nz : 1));
+  u.outer = outer;
+  m->u.push_back(u);
+  if (uid) *uid = (int32_t)m->u.size() - 1;
+  return NT_OK;
+}
+
+nt_status nt_set_root(nt_model* m, int32_t uid) {
+  CHECK_BUILDER(m);
+  if (uid < 0 || uid >= (int)m->u.size()) return err(NT_E_ID, "nt_set_root: universe id out of range");
+  m->root = uid;
+  return NT_OK;
+}
+
+void nt_build_opts_default(nt_build_opts* o) {
+  if (!o) return;
+  o->device = 0;
+  o->bih_max_leaf = 4;
+  o->pseudo_array = 0;
+  o->reserved = 0;
+  o->sah_ct = 1.0;
+  o->sah_ci = 1.0;
+}
+
+nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
+  CHECK_BUILDER(m);
+  nt_build_opts d;
+  nt_build_opts_default(&d);
+  if (!o) o = &d;
+  m->opts.device = o->device;
+  m->opts.max_leaf = o->bih_max_leaf > 0 ? o->bih_max_leaf : 4;
+  m->opts.pseudo = o->pseudo_array;
+  m->opts.ct = o->sah_ct > 0 ? o->sah_ct : 1.0;
+  m->opts.ci = o->sah_ci > 0 ? o->sah_ci : 1.0;
+  try {
+    build_flat(m->s, m->m, m->c, m->u, m->root, m->opts, m->F);
+  } catch (const GeomError& e) {
+    return err(NT_E_GEOMETRY, std::string("nt_finalize: ") + e.what());
+  } catch (const std::bad_alloc&) {
+    return err(NT_E_NOMEM, "nt_finalize: out of host memory");
+  }
+  const Flat& F = m->F;
+  // one contiguous blob of 256-byte aligned arrays
+  std::vector<char> blob;
+  const size_t o_surf = place(blob, F.surf), o_tol = place(blob, F.surf_tol), o_meta = place(blob, F.surf_meta),
+               o_hs = place(blob, F.hs), o_chs = place(blob, F.cell_hs), o_cf = place(blob, F.cell_fill),
+               o_ctr = place(blob, F.cell_tr), o_univ = place(blob, F.univ), o_bih = place(blob, F.bih),
+               o_leaf = place(blob, F.bih_leaf), o_fills = place(blob, F.fills), o_st = place(blob, F.mc_st),
+               o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell);
+  size_t o_rr2 = 0, o_rtol = 0, o_rsid = 0, o_rcell = 0, o_rmc = 0, o_rbc = 0, o_pou = 0, o_poff = 0, o_pr2 = 0,
+         o_ptol = 0, o_psid = 0, o_pmc = 0;
+  if (F.rect_ok) {
+    o_rr2 = place(blob, F.r_root_r2); o_rtol = place(blob, F.r_root_tol); o_rsid = place(blob, F.r_root_sid);
+    o_rcell = place(blob, F.r_root_cell); o_rmc = place(blob, F.r_root_mc); o_rbc = place(blob, F.r_root_bc);
+    o_pou = place(blob, F.r_pin_of_univ); o_poff = place(blob, F.r_pin_off); o_pr2 = place(blob, F.r_pin_r2);
+    o_ptol = place(blob, F.r_pin_tol); o_psid = place(blob, F.r_pin_sid); o_pmc = place(blob, F.r_pin_mc);
+  }
+  m->blob_bytes = blob.size();
+  m->device = o->device;
+  if (o->device >= 0) {
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaError_t e = cudaSetDevice(o->device);
+    if (e != cudaSuccess) return cuda_err(e, "nt_finalize: cudaSetDevice");
+    e = cudaMalloc(&m->blob, blob.size());
+    if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_err(e, "nt_finalize: cudaMalloc"); }
+    e = cudaMemcpy(m->blob, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess) e = cudaMalloc(&m->counters, sizeof(unsigned long long) * kSlots);
+    if (e == cudaSuccess) e = cudaMemset(m->counters, 0, sizeof(unsigned long long) * kSlots);
+    double coef[30];
+    coef_table(coef);
+    if (e == cudaSuccess) e = upload_coefficients(coef, 30);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) return cuda_err(e, "nt_finalize: upload");
+    char* b = static_cast<char*>(m->blob);
+    DevGeom& g = m->g;
+    g.surf = (const DSurf*)(b + o_surf);
+    g.surf_tol = (const double*)(b + o_tol);
+    g.surf_meta = (const uint8_t*)(b + o_meta);
+    g.hs = (const int32_t*)(b + o_hs);
+    g.cell_hs = (const int32_t*)(b + o_chs);
+    g.cell_fill = (const int32_t*)(b + o_cf);
+    g.cell_tr = (const double*)(b + o_ctr);
+    g.univ = (const DUniv*)(b + o_univ);
+    g.bih = (const BihNode*)(b + o_bih);
+    g.bih_leaf = (const int32_t*)(b + o_leaf);
+    g.fills = (const int32_t*)(b + o_fills);
+    g.mc_st = (const double*)(b + o_st);
+    g.mc_pabs = (const double*)(b + o_pabs);
+    g.mc_cell = (const int32_t*)(b + o_mcc);
+    if (F.rect_ok) {
+      m->rg = F.rg;
+      m->rg.root_r2 = (const double*)(b + o_rr2);
+      m->rg.root_tol = (const double*)(b + o_rtol);
+      m->rg.root_sid = (const int32_t*)(b + o_rsid);
+      m->rg.root_cell = (const int32_t*)(b + o_rcell);
+      m->rg.root_mc = (const int32_t*)(b + o_rmc);
+      m->rg.root_bc = (const uint8_t*)(b + o_rbc);
+      m->rg.pin_of_univ = (const int32_t*)(b + o_pou);
+      m->rg.pin_off = (const int32_t*)(b + o_poff);
+      m->rg.pin_r2 = (const double*)(b + o_pr2);
+      m->rg.pin_tol = (const double*)(b + o_ptol);
+      m->rg.pin_sid = (const int32_t*)(b + o_psid);
+      m->rg.pin_mc = (const int32_t*)(b + o_pmc);
+    }
+  }
+  DevGeom& g = m->g;
+  g.root = F.root;
+  g.n_mc = F.n_mc;
+  g.max_depth = F.max_depth;
+  g.n_univ = (int)F.univ.size();
+  g.n_cells = (int)F.cell_fill.size();
+  g.n_surf = (int)F.surf.size();
+  g.root_kind = F.univ[F.root].kind;
+  m->finalized = true;
+  return NT_OK;
+}
+
+nt_status nt_model_info_get(const nt_model* m, nt_model_info* info) {
+  if (!m || !info) return err(NT_E_ARG, "nt_model_info_get: NULL argument");
+  if (!m->finalized) return err(NT_E_ORDER, "nt_model_info_get: model not finalized");
+  const Flat& F = m->F;
+  info->n_surfaces = (int)F.surf.size();
+  info->n_cells = (int)F.cell_fill.size();
+  info->n_material_cells = F.n_mc;
+  info->n_universes = (int)F.univ.size();
+  info->max_depth = F.max_depth;
+  info->rect_specialisable = F.rect_ok ? 1 : 0;
+  info->rect_levels = F.rect_K;
+  info->n_bih_nodes = (int)F.bih.size();
+  info->out_len = 2 * (int64_t)F.n_mc + NT_NC;
+  info->device_bytes = m->blob_bytes;
+  return NT_OK;
+}
+
+nt_status nt_material_cell_ids(const nt_model* m, int32_t* out, int32_t cap) {
+  if (!m || (!out && cap > 0)) return err(NT_E_ARG, "nt_material_cell_ids: NULL argument");
+  if (!m->finalized) return err(NT_E_ORDER, "nt_material_cell_ids: model not finalized");
+  for (int i = 0; i < m->F.n_mc && i < cap; ++i) out[i] = m->F.mc_cell[i];
+  return NT_OK;
+}
+
+nt_status nt_bih_info(const nt_model* m, int32_t uid, int32_t* n_nodes, int32_t* depth, int32_t* leaf_cells,
+                      int32_t cap, int32_t* n_leaf_cells) {
+  if (!m) return err(NT_E_ARG, "nt_bih_info: model is NULL");
+  if (!m->finalized) return err(NT_E_ORDER, "nt_bih_info: model not finalized");
+  if (uid < 0 || uid >= (int)m->F.univ.size()) return err(NT_E_ID, "nt_bih_info: universe id out of range");
+  const DUniv& U = m->F.univ[uid];
+  if (U.kind != U_CSG) return err(NT_E_ARG, "nt_bih_info: not a CSG universe");
+  // walk the subtree
+  std::vector<int> todo{U.i0};
+  int nodes = 0, cnt = 0;
+  while (!todo.empty()) {
+    const int n = todo.back();
+    todo.pop_back();
+    ++nodes;
+    const BihNode& b = m->F.bih[n];
+    if (b.meta < 0) {
+      for (int q = 0; q < -b.meta - 1; ++q) {
+        if (leaf_cells && cnt < cap) leaf_cells[cnt] = m->F.bih_leaf[b.a + q];
+        ++cnt;
+      }
+    } else {
+      todo.push_back(b.a + 1);
+      todo.push_back(b.a);
+    }
+  }
+  if (n_nodes) *n_nodes = nodes;
+  if (depth) *depth = m->F.bih_depth[uid];
+  if (n_leaf_cells) *n_leaf_cells = cnt;
+  return NT_OK;
+}
+
+static nt_status run_common(nt_model* m, const nt_run* run, const double* d_states, const nt_outputs* o,
+                            void* stream, const char* who) {
+  if (!m || !run || !o) return err(NT_E_ARG, std::string(who) + ": NULL argument");
+  if (!m->finalized) return err(NT_E_ORDER, std::string(who) + ": model not finalized");
+  if (m->device < 0 || !m->blob) return err(NT_E_ORDER, std::string(who) + ": host-only model (device = -1)");
+  if (!o->out) return err(NT_E_ARG, std::string(who) + ": outputs.out is NULL");
+  const bool trace = (run->flags & NT_TRACE) != 0;
+  if (trace && (!o->trace_count || (!o->trace && o->trace_cap))) return err(NT_E_ARG, std::string(who) + ": trace buffers");
+  if (run->tracker != NT_TRACKER_GENERIC && run->tracker != NT_TRACKER_RECT)
+    return err(NT_E_ARG, std::string(who) + ": bad tracker");
+  if (run->tracker == NT_TRACKER_RECT && !m->F.rect_ok)
+    return err(NT_E_UNSUPPORTED, std::string(who) + ": model is not rect-specialisable: " + m->F.rect_why);
+  if (run->max_segments > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": max_segments >= 2^32");
+  const int block = run->block_dim > 0 ? run->block_dim : 256;
+  if (block % 32 || block > 256) return err(NT_E_ARG, std::string(who) + ": block_dim must be a multiple of 32, <= 256");
+  m->last_launches = 0;
+  if (run->n == 0) return NT_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != m->device) cudaSetDevice(m->device);
+  KRun R{};
+  R.seed = run->seed;
+  R.pid0 = run->pid_begin;
+  R.n = run->n;
+  R.max_seg = run->max_segments ? run->max_segments : 1000000;
+  for (int a = 0; a < 3; ++a) { R.lo[a] = run->src_lo[a]; R.w[a] = run->src_hi[a] - run->src_lo[a]; }
+  R.states = d_states;
+  R.out = o->out;
+  R.pflags = o->pflags;
+  R.pnseg = o->pnseg;
+  R.pterm = o->pterm;
+  R.trace = o->trace;
+  R.trace_cap = trace ? o->trace_cap : 0;
+  R.trace_count = reinterpret_cast<unsigned long long*>(o->trace_count);
+  const unsigned slot = m->slot.fetch_add(1) % kSlots;
+  R.counter = m->counters + slot;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = cudaMemsetAsync(R.counter, 0, sizeof(unsigned long long), s);
+  int grid = 0;
+  if (e == cudaSuccess) {
+    if (run->tracker == NT_TRACKER_RECT)
+      e = launch_rect(m->g, m->rg, R, trace, d_states != nullptr, block, run->blocks_per_sm, s, &grid);
+    else
+      e = launch_generic(m->g, R, trace, d_states != nullptr, block, run->blocks_per_sm, s, &grid);
+  }
+  if (prev != m->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_err(e, who);
+  m->last_launches = 1;
+  return NT_OK;
+}
+
+nt_status nt_track(nt_model* m, const nt_run* run, const nt_outputs* o, void* stream) {
+  return run_common(m, run, nullptr, o, stream, "nt_track");
+}
+
+nt_status nt_track_states(nt_model* m, const nt_run* run, const double* d_states, const nt_outputs* o,
+                          void* stream) {
+  if (!d_states) return err(NT_E_ARG, "nt_track_states: d_states is NULL");
+  return run_common(m, run, d_states, o, stream, "nt_track_states");
+}
+
+nt_status nt_track_host(nt_model* m, const nt_run* run, double* host_out, void* stream) {
+  if (!m || !run || !host_out) return err(NT_E_ARG, "nt_track_host: NULL argument");
+  if (!m->finalized || !m->blob) return err(NT_E_ORDER, "nt_track_host: model not finalized on a device");
+  if (run->flags & NT_TRACE) return err(NT_E_ARG, "nt_track_host: tracing needs device buffers");
+  std::lock_guard<std::mutex> lk(m->host_mu);
+  const size_t len = 2 * (size_t)m->F.n_mc + NT_NC;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != m->device) cudaSetDevice(m->device);
+  cudaError_t e = cudaSuccess;
+  if (m->host_scratch_len < len) {
+    if (m->host_scratch_dev) cudaFree(m->host_scratch_dev);
+    e = cudaMalloc(&m->host_scratch_dev, len * sizeof(double));
+    m->host_scratch_len = e == cudaSuccess ? len : 0;
+  }
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (e == cudaSuccess) e = cudaMemsetAsync(m->host_scratch_dev, 0, len * sizeof(double), s);
+  if (prev != m->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_err(e, "nt_track_host");
+  nt_outputs o{};
+  o.out = m->host_scratch_dev;
+  nt_status st = run_common(m, run, nullptr, &o, stream, "nt_track_host");
+  if (st != NT_OK) return st;
+  if (prev != m->device) cudaSetDevice(m->device);
+  e = cudaMemcpyAsync(host_out, m->host_scratch_dev, len * sizeof(double), cudaMemcpyDeviceToHost, s);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+  if (prev != m->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_err(e, "nt_track_host");
+  return NT_OK;
+}
+
+nt_status nt_find_cells(nt_model* m, const double* d_xyz, uint64_t n, int32_t* d_cell, uint8_t* d_flag,
+                        void* stream) {
+  if (!m || (n && (!d_xyz || !d_cell))) return err(NT_E_ARG, "nt_find_cells: NULL argument");
+  if (!m->finalized || !m->blob) return err(NT_E_ORDER, "nt_find_cells: model not finalized on a device");
+  if (n == 0) return NT_OK;
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != m->device) cudaSetDevice(m->device);
+  cudaError_t e = launch_find_cells(m->g, d_xyz, n, d_cell, d_flag, static_cast<cudaStream_t>(stream));
+  if (prev != m->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_err(e, "nt_find_cells");
+  return NT_OK;
+}
+
+int32_t nt_last_launch_count(const nt_model* m) { return m ? m->last_launches : 0; }
+
+}  // extern "C"

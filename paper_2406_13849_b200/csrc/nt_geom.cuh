@@ -1,0 +1,240 @@
+// Device geometry primitives for the generic tracker (sm_100a, fp64, -fmad=false):
+// implicit functions and senses (readings O3/O4), cell-aware forward distances
+// (Table 1 distance_to_surface, reading O11), BIH point location, rect
+// (Alg. 5-6) and hex (reading O9) tile location, and the per-level distance candidates.
+#pragma once
+#include <cstdint>
+
+#include "nt_layout.hpp"
+
+namespace nt {
+
+#define NT_INF __longlong_as_double(0x7ff0000000000000ULL)
+
+template <class T>
+__device__ __forceinline__ T ld(const T* p) { return __ldg(p); }
+
+__device__ __forceinline__ double clamp0(double d) { return d > 0.0 ? d : 0.0; }
+
+__device__ __forceinline__ double sel3(int a, double x, double y, double z) {
+  return a == 0 ? x : (a == 1 ? y : z);
+}
+
+// f(r) of a surface (O3), evaluation order exactly as documented
+__device__ __forceinline__ double surf_f(int kind, const DSurf* sp, double x, double y, double z) {
+  if (kind <= S_PZ) return sel3(kind, x, y, z) - ld(&sp->c[0]);
+  const double c0 = ld(&sp->c[0]), c1 = ld(&sp->c[1]), c2 = ld(&sp->c[2]), c3 = ld(&sp->c[3]);
+  if (kind == S_PLANE) return ((c0 * x + c1 * y) + c2 * z) - c3;
+  const double dx = x - c0, dy = y - c1;
+  if (kind == S_CZ) return (dx * dx + dy * dy) - c2;
+  const double dz = z - c2;
+  return ((dx * dx + dy * dy) + dz * dz) - c3;
+}
+
+// forward distance to leave half-space (kind, sense) along (u,v,w) from (x,y,z); O11.
+// os: particle logically on this surface (quadric c := 0).  Returns +inf when no exit.
+__device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const DSurf* sp, double x,
+                                            double y, double z, double u, double v, double w) {
+  if (kind <= S_PZ) {
+    const double uu = sel3(kind, u, v, w);
+    if (sense ? !(uu < 0.0) : !(uu > 0.0)) return NT_INF;   // also uu == 0
+    return clamp0((ld(&sp->c[0]) - sel3(kind, x, y, z)) / uu);
+  }
+  const double c0 = ld(&sp->c[0]), c1 = ld(&sp->c[1]), c2 = ld(&sp->c[2]), c3 = ld(&sp->c[3]);
+  if (kind == S_PLANE) {
+    const double sd = (c0 * u + c1 * v) + c2 * w;
+    if (sense ? !(sd < 0.0) : !(sd > 0.0)) return NT_INF;
+    const double fr = (c0 * x + c1 * y) + c2 * z;
+    return clamp0((c3 - fr) / sd);
+  }
+  double a, k, c, q;
+  if (kind == S_CZ) {
+    const double dx = x - c0, dy = y - c1;
+    a = u * u + v * v;
+    if (a == 0.0) return NT_INF;
+    k = dx * u + dy * v;
+    c = os ? 0.0 : (dx * dx + dy * dy) - c2;
+    q = k * k - a * c;
+  } else {
+    const double dx = x - c0, dy = y - c1, dz = z - c2;
+    a = 1.0;
+    k = (dx * u + dy * v) + dz * w;
+    c = os ? 0.0 : ((dx * dx + dy * dy) + dz * dz) - c3;
+    q = k * k - c;
+  }
+  if (!sense) {   // inside (negative side): far root
+    if (q < 0.0) q = 0.0;
+    const double d = k <= 0.0 ? (-k + sqrt(q)) / a : -c / (k + sqrt(q));
+    return clamp0(d);
+  }
+  if (k >= 0.0 || q < 0.0) return NT_INF;   // outside: moving away or missing
+  return clamp0(c / (-k + sqrt(q)));
+}
+
+// Alg. 3 "cell contains pos" with an optional logically forced sense (O9'); on success the
+// O16 F1 proximity bit of the accepted cell is returned in `near`.
+__device__ __forceinline__ bool cell_contains(const DevGeom& g, int cell, double x, double y, double z,
+                                              int fsid, int fsense, uint32_t& near) {
+  const int h0 = ld(g.cell_hs + cell), h1 = ld(g.cell_hs + cell + 1);
+  uint32_t nb = 0;
+  for (int h = h0; h < h1; ++h) {
+    const int e = ld(g.hs + h);
+    const int sid = hs_sid(e);
+    int s;
+    if (sid == fsid) {
+      s = fsense;
+    } else {
+      const double f = surf_f(hs_kind(e), g.surf + sid, x, y, z);
+      s = f >= 0.0;
+      if (fabs(f) <= ld(g.surf_tol + sid)) nb = 1u;
+    }
+    if (s != hs_sense(e)) return false;
+  }
+  near = nb;
+  return true;
+}
+
+// BIH traversal: both children are visited when the point lies in the overlap.
+__device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, double y, double z,
+                                        int fsid, int fsense, uint32_t& flags) {
+  int stack[24];
+  int sp = 0, node = root;
+  for (;;) {
+    const BihNode* n = g.bih + node;
+    const int meta = ld(&n->meta), a = ld(&n->a);
+    if (meta < 0) {
+      const int cnt = -meta - 1;
+      for (int q = 0; q < cnt; ++q) {
+        const int cell = ld(g.bih_leaf + a + q);
+        uint32_t nb = 0;
+        if (cell_contains(g, cell, x, y, z, fsid, fsense, nb)) {
+          flags |= nb;
+          return cell;
+        }
+      }
+      if (sp == 0) return -1;
+      node = stack[--sp];
+    } else {
+      const double c = sel3(meta, x, y, z);
+      const bool gl = c <= ld(&n->lmax), gr = c >= ld(&n->rmin);
+      if (gl && gr) {
+        if (sp < 24) stack[sp++] = a + 1;
+        node = a;
+      } else if (gl) {
+        node = a;
+      } else if (gr) {
+        node = a + 1;
+      } else {
+        if (sp == 0) return -1;
+        node = stack[--sp];
+      }
+    }
+  }
+}
+
+// O8: the unique i with e(i) <= x < e(i+1), e(i) = ll + i p
+__device__ __forceinline__ int rect_index(double ll, double p, double x) {
+  int i = static_cast<int>(floor((x - ll) / p));
+  while (!(ll + static_cast<double>(i) * p <= x)) --i;
+  while (!(x < ll + static_cast<double>(i + 1) * p)) ++i;
+  return i;
+}
+
+__device__ __forceinline__ bool near_wall(double ll, double p, int i, double x) {
+  return fabs(x - (ll + static_cast<double>(i) * p)) <= kFlagDist ||
+         fabs(x - (ll + static_cast<double>(i + 1) * p)) <= kFlagDist;
+}
+
+// daughter universe of an array tile (fill inside the lattice, else outer) and the tile
+// centre (daughter translation).  Tile indices: rect (i,j,k), hex (q,r,kz).
+__device__ __forceinline__ int array_daughter(const DevGeom& g, const DUniv* U, int kind, int a, int b,
+                                              int c, double& tx, double& ty, double& tz) {
+  int idx = -1;
+  if (kind == U_RECT) {
+    const int n0 = ld(&U->i0), n1 = ld(&U->i1), n2 = ld(&U->i2), is2d = ld(&U->is2d);
+    const bool in = a >= 0 && a < n0 && b >= 0 && b < n1 && (is2d || (c >= 0 && c < n2));
+    if (in) idx = ld(g.fills + ld(&U->fill_off) + a + n0 * (b + n1 * (is2d ? 0 : c)));
+    tx = ld(&U->d[0]) + (static_cast<double>(a) + 0.5) * ld(&U->d[3]);
+    ty = ld(&U->d[1]) + (static_cast<double>(b) + 0.5) * ld(&U->d[4]);
+    tz = is2d ? 0.0 : ld(&U->d[2]) + (static_cast<double>(c) + 0.5) * ld(&U->d[5]);
+  } else {
+    const int R = ld(&U->i0), nz = ld(&U->i1);
+    const int aq = abs(a), ar = abs(b), as = abs(a + b);
+    const int dd = max(aq, max(ar, as));
+    const bool in = dd <= R && (nz == 0 || (c >= 0 && c < nz));
+    if (in) idx = ld(g.fills + ld(&U->fill_off) + (b + R) * (2 * R + 1) + (a + R) + (nz > 0 ? c * ld(&U->ntile) : 0));
+    tx = ld(&U->d[0]) + (static_cast<double>(a) * ld(&U->d[6]) + static_cast<double>(b) * ld(&U->d[8]));
+    ty = ld(&U->d[1]) + (static_cast<double>(a) * ld(&U->d[7]) + static_cast<double>(b) * ld(&U->d[9]));
+    tz = nz > 0 ? ld(&U->d[4]) + (static_cast<double>(c) + 0.5) * ld(&U->d[5]) : 0.0;
+  }
+  return idx >= 0 ? idx : ld(&U->outer);
+}
+
+// hex t-space coordinates t_k = (n_k . (x - C)) / p  (O9)
+__device__ __forceinline__ void hex_t(const DUniv* U, double x, double y, double& t0, double& t1, double& t2) {
+  const double xp = x - ld(&U->d[0]), yp = y - ld(&U->d[1]), p = ld(&U->d[2]);
+  t0 = (ld(&U->d[10]) * xp + ld(&U->d[11]) * yp) / p;
+  t1 = (ld(&U->d[12]) * xp + ld(&U->d[13]) * yp) / p;
+  t2 = (ld(&U->d[14]) * xp + ld(&U->d[15]) * yp) / p;
+}
+
+__device__ __forceinline__ void hex_m(int q, int r, double& m0, double& m1, double& m2) {
+  const double qd = static_cast<double>(q), rd = static_cast<double>(r);
+  m0 = qd + rd * 0.5;
+  m1 = qd * 0.5 + rd;
+  m2 = -(qd * 0.5) + rd * 0.5;
+}
+
+// hex tile owning (x,y): cube rounding then fix-up moves in t-space (O9); falls back to the
+// cube-rounded tile with F1 if the fix-up does not converge.  Sets F1 on proximity.
+__device__ __forceinline__ void hex_locate(const DUniv* U, double x, double y, int& qo, int& ro, uint32_t& flags) {
+  const double xp = x - ld(&U->d[0]), yp = y - ld(&U->d[1]);
+  const double p = ld(&U->d[2]), pH = ld(&U->d[3]);
+  double qf, rf;
+  if (ld(&U->i2) == 0) { rf = yp / pH; qf = (xp - rf * (p * 0.5)) / p; }
+  else { qf = xp / pH; rf = (yp - qf * (p * 0.5)) / p; }
+  const double sf = -qf - rf;
+  double qr = round(qf), rr = round(rf), sr = round(sf);
+  const double dq = fabs(qr - qf), dr = fabs(rr - rf), ds = fabs(sr - sf);
+  if (dq > dr && dq > ds) qr = -rr - sr;
+  else if (dr > ds) rr = -qr - sr;
+  const int qc = static_cast<int>(qr), rc = static_cast<int>(rr);
+  double t0, t1, t2;
+  hex_t(U, x, y, t0, t1, t2);
+  int q = qc, r = rc;
+  bool ok = false;
+  for (int it = 0; it < 4; ++it) {
+    double m0, m1, m2;
+    hex_m(q, r, m0, m1, m2);
+    if (t0 < m0 - 0.5) { q -= 1; continue; }            // face 3: delta (-1, 0)
+    if (!(t0 < m0 + 0.5)) { q += 1; continue; }         // face 0: delta (+1, 0)
+    if (t1 < m1 - 0.5) { r -= 1; continue; }            // face 4: delta (0, -1)
+    if (!(t1 < m1 + 0.5)) { r += 1; continue; }         // face 1: delta (0, +1)
+    if (t2 < m2 - 0.5) { q += 1; r -= 1; continue; }    // face 5: delta (+1, -1)
+    if (!(t2 < m2 + 0.5)) { q -= 1; r += 1; continue; } // face 2: delta (-1, +1)
+    ok = true;
+    break;
+  }
+  if (!ok) { q = qc; r = rc; flags |= 1u; }
+  double m0, m1, m2;
+  hex_m(q, r, m0, m1, m2);
+  if (p * fabs(t0 - (m0 - 0.5)) <= kFlagDist || p * fabs(t0 - (m0 + 0.5)) <= kFlagDist ||
+      p * fabs(t1 - (m1 - 0.5)) <= kFlagDist || p * fabs(t1 - (m1 + 0.5)) <= kFlagDist ||
+      p * fabs(t2 - (m2 - 0.5)) <= kFlagDist || p * fabs(t2 - (m2 + 0.5)) <= kFlagDist)
+    flags |= 1u;
+  qo = q;
+  ro = r;
+}
+
+// Distance-to-boundary bookkeeping: strict '<' keeps the top-most level / lowest id on exact
+// ties (O13); d2 = smallest other candidate (O16 F2).
+struct Best {
+  double d, d2;
+  int l, j, sense;
+  __device__ __forceinline__ void consider(double dd, int ll, int jj, int ss) {
+    if (dd < d) { d2 = d; d = dd; l = ll; j = jj; sense = ss; }
+    else if (dd < d2) d2 = dd;
+  }
+};
+
+}  // namespace nt

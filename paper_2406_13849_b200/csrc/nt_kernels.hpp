@@ -1,0 +1,34 @@
+// Kernel launch interface between capi.cpp (host, C++) and the CUDA translation units.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/nestrack.h"
+#include "nt_layout.hpp"
+
+namespace nt {
+
+struct KRun {
+  uint64_t seed, pid0, n, max_seg;
+  double lo[3], w[3];
+  const double* states;             // optional SoA [6][n] birth states
+  double* out;                      // [len | exits | counters]
+  uint8_t* pflags;
+  uint32_t* pnseg;
+  uint8_t* pterm;
+  nt_trace_rec* trace;
+  uint64_t trace_cap;
+  unsigned long long* trace_count;
+  unsigned long long* counter;      // work counter (pid claims), zeroed before launch
+};
+
+cudaError_t upload_coefficients(const double* host, int n);
+cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
+                           int blocks_per_sm, cudaStream_t stream, int* grid_out);
+cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states,
+                        int block, int blocks_per_sm, cudaStream_t stream, int* grid_out);
+cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,
+                              uint8_t* flag, cudaStream_t stream);
+
+}  // namespace nt

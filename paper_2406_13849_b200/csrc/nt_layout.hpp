@@ -1,0 +1,108 @@
+// Device geometry layout shared by the host builder (builder.cpp) and the kernels
+// (track.cu).  Everything is flattened into one contiguous device blob of plain
+// arrays (SoA where the access pattern is per-field, small AoS records where a
+// whole record is consumed at once).  DESIGN.md "Data layout" documents it.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+
+#ifdef __CUDACC__
+#define NT_HD __host__ __device__ __forceinline__
+#else
+#define NT_HD inline
+#endif
+
+namespace nt {
+
+constexpr int kMaxDepth = 8;          // builder-enforced nesting limit (reading O7)
+constexpr int kNC = 18;               // counters (NT_NC)
+constexpr double kFlagDist = 1e-10;   // O16 proximity / near-tie distance (cm)
+constexpr double kHexH = 0.8660254037844386;  // O9: nearest double to sqrt(3)/2
+
+enum SurfKind : int { S_PX = 0, S_PY = 1, S_PZ = 2, S_PLANE = 3, S_CZ = 4, S_SPHERE = 5 };
+enum UnivKind : int { U_CSG = 0, U_RECT = 1, U_HEX = 2 };
+
+// Surface record: 32 bytes.  PX/PY/PZ: c0 = a.  PLANE: nx, ny, nz, d.
+// CZ: x0, y0, R*R (c3 unused).  SPHERE: x0, y0, z0, R*R.
+struct alignas(16) DSurf { double c[4]; };
+
+// Half-space entry of a cell: (sid << 4) | (kind << 1) | sense  (sense 1 = positive side).
+NT_HD int hs_sid(int h) { return h >> 4; }
+NT_HD int hs_kind(int h) { return (h >> 1) & 7; }
+NT_HD int hs_sense(int h) { return h & 1; }
+inline int hs_pack(int sid, int kind, int sense) { return (sid << 4) | (kind << 1) | sense; }
+
+// Universe record (160 bytes).
+//  CSG : i0 = BIH root node, i1 = first cell, i2 = cell count
+//  RECT: i0..i2 = shape, is2d; d[0..2] = lower-left, d[3..5] = pitch
+//  HEX : i0 = R = rings-1, i1 = nz (0 = 2-D), i2 = orient; ntile = (2R+1)^2
+//        d[0..1] = C, d[2] = pitch, d[3] = pitch*H, d[4] = z_lower, d[5] = z_pitch,
+//        d[6..7] = a1, d[8..9] = a2, d[10..15] = n0x n0y n1x n1y n2x n2y
+//  fill_off: offset into `fills` (RECT: shape product entries, x fastest;
+//            HEX: ntile * max(nz,1) entries indexed (r+R)*(2R+1)+(q+R) + kz*ntile;
+//            -1 entries = out of lattice -> outer), outer: universe id or -1.
+struct alignas(16) DUniv {
+  int32_t kind, i0, i1, i2;
+  int32_t fill_off, outer, is2d, ntile;
+  double d[16];
+};
+
+// Bounding-interval-hierarchy node (24 bytes): two planes per node.
+//  meta >= 0: internal, split axis = meta, children a and a+1;
+//             left child covers x[axis] <= lmax, right child x[axis] >= rmin (may overlap).
+//  meta <  0: leaf with (-meta - 1) cells at bih_leaf[a ..].
+struct BihNode { double lmax, rmin; int32_t meta, a; };
+
+// Everything a kernel needs, passed by value (kernel parameter space).
+struct DevGeom {
+  const DSurf* surf;
+  const double* surf_tol;     // O16 proximity tolerance per surface
+  const uint8_t* surf_meta;   // per surface: kind | (nt_bc << 4)
+  const int32_t* hs;          // packed half-spaces, per cell sorted by surface id (O13)
+  const int32_t* cell_hs;     // [n_cells+1] CSR offsets into hs
+  const int32_t* cell_fill;   // >= 0: material-cell index (tally bin); < 0: -1 - daughter uid
+  const double* cell_tr;      // [3*n_cells] fill translation
+  const DUniv* univ;
+  const BihNode* bih;
+  const int32_t* bih_leaf;
+  const int32_t* fills;
+  const double* mc_st;        // per material cell: sigma_t
+  const double* mc_pabs;      // per material cell: sigma_a / sigma_t (O14)
+  const int32_t* mc_cell;     // per material cell: global cell id (trace)
+  int32_t root, n_mc, max_depth, n_univ;
+  int32_t n_cells, n_surf, root_kind, pad;
+};
+
+// Rect-specialised tracker tables (Alg. 9-10): root = box or concentric CZ annuli with a PZ
+// pair, then K rect levels, then a concentric-CZ pin.  Arrays index rect universes through
+// the generic DUniv table; pins through `pin_*`.
+struct RectGeom {
+  int32_t K;               // number of rect levels
+  int32_t root_box;        // 1: root cell is an axis box (6 planes); 0: CZ annuli + PZ pair
+  int32_t root_fill_cell;  // root cell that holds the first rect level (annulus index for CZ roots)
+  int32_t n_root_cells;    // CZ root: number of annuli (cells)
+  int32_t root_univ_child; // universe id of level 1
+  int32_t pad0, pad1, pad2;
+  // box root: walls lo/hi per axis + surface ids + bc
+  double box_lo[3], box_hi[3];
+  int32_t box_sid[6], box_bc[6];
+  // CZ root (annulus k spans [R_{k-1}, R_k)): radii^2, surface ids, cells
+  const double* root_r2;   // [n_root_cells] outer R^2 of annulus k (last may be unbounded -> huge)
+  const double* root_tol;  // proximity tol of each root CZ
+  const int32_t* root_sid; // CZ surface id bounding annulus k from outside (-1 none)
+  const int32_t* root_cell;// global cell id of annulus k
+  const int32_t* root_mc;  // material-cell index of annulus k (-1 = filled: core)
+  const uint8_t* root_bc;  // bc of the outer CZ of annulus k
+  double z_lo, z_hi;       // PZ pair
+  int32_t zsid[2], zbc[2];
+  double ztol;
+  // pins: per universe id -> pin record index (-1 if not a pin)
+  const int32_t* pin_of_univ;
+  const int32_t* pin_off;  // [n_pins+1] offsets into pin_r2 / pin_sid ... (annuli count = n+1)
+  const double* pin_r2;    // radii^2 ascending
+  const double* pin_tol;
+  const int32_t* pin_sid;  // CZ surface ids
+  const int32_t* pin_mc;   // [pin_off[p] + p + k] material-cell index of annulus k (n+1 per pin)
+};
+
+}  // namespace nt

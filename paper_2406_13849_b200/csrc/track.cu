@@ -1,0 +1,442 @@
+// Generic nested-geometry tracker for sm_100a (history-based persistent kernel).
+//
+// One thread owns one history at a time and walks it through Alg. 2:
+// distance_to_surface over every level of the universe stack (Table 1), collide
+// or cross, cross_surface at the top-most level holding the surface (Alg. 8,
+// P:584-592) by BIH search or array index +-1 (Alg. 6), re-descend
+// (Alg. 7), isotropic scatter / absorption.  When its history ends
+// the thread claims the next pid from a global counter (persistent refill; warp-aggregated
+// atomics), so the grid never drains while work remains (§2.3 vector of histories,
+// P:424-434, re-designed as a persistent history-based kernel — DESIGN.md).
+//
+// The per-level universe stack lives in shared memory (one slot per thread per level,
+// stride = blockDim, conflict-free); tallies are privatised per block in shared memory and
+// flushed once with fp64 global atomics.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "../../include/nestrack.h"
+#include "nt_geom.cuh"
+#include "nt_kernels.hpp"
+#include "nt_layout.hpp"
+#include "nt_math.cuh"
+
+namespace nt {
+
+
+
+
+// per-thread universe stack in shared memory
+struct Stack {
+  int* si;      // [4][maxd][B]: u, a, b, c
+  double* sT;   // [3][maxd][B]
+  int B, tid, maxd;
+  __device__ __forceinline__ int& u(int l) { return si[(0 * maxd + l) * B + tid]; }
+  __device__ __forceinline__ int& a(int l) { return si[(1 * maxd + l) * B + tid]; }
+  __device__ __forceinline__ int& b(int l) { return si[(2 * maxd + l) * B + tid]; }
+  __device__ __forceinline__ int& c(int l) { return si[(3 * maxd + l) * B + tid]; }
+  __device__ __forceinline__ double& T(int l, int k) { return sT[(k * maxd + l) * B + tid]; }
+};
+
+// Alg. 7 descent from level l0 in universe u with frame translation T; forced sense applies
+// at level l0 only (CSG cross_surface).  Returns false when a level has no cell (LOST).
+__device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int u, double Tx, double Ty,
+                                     double Tz, double rx, double ry, double rz, int fsid, int fsense,
+                                     int& L, int& mc, uint32_t& flags) {
+  for (int l = l0; l < st.maxd; ++l) {
+    st.u(l) = u;
+    st.T(l, 0) = Tx;
+    st.T(l, 1) = Ty;
+    st.T(l, 2) = Tz;
+    const double x = rx - Tx, y = ry - Ty, z = rz - Tz;
+    const DUniv* U = g.univ + u;
+    const int kind = ld(&U->kind);
+    double tx, ty, tz;
+    int dau;
+    if (kind == U_CSG) {
+      const int cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags);
+      if (cell < 0) return false;
+      st.a(l) = cell;
+      const int f = ld(g.cell_fill + cell);
+      if (f >= 0) { L = l + 1; mc = f; return true; }
+      dau = -1 - f;
+      tx = ld(g.cell_tr + 3 * cell);
+      ty = ld(g.cell_tr + 3 * cell + 1);
+      tz = ld(g.cell_tr + 3 * cell + 2);
+    } else if (kind == U_RECT) {
+      const double llx = ld(&U->d[0]), lly = ld(&U->d[1]), px = ld(&U->d[3]), py = ld(&U->d[4]);
+      const int i = rect_index(llx, px, x), j = rect_index(lly, py, y);
+      uint32_t nb = near_wall(llx, px, i, x) | near_wall(lly, py, j, y);
+      int k = 0;
+      if (!ld(&U->is2d)) {
+        const double llz = ld(&U->d[2]), pz = ld(&U->d[5]);
+        k = rect_index(llz, pz, z);
+        nb |= near_wall(llz, pz, k, z);
+      }
+      flags |= nb;
+      st.a(l) = i; st.b(l) = j; st.c(l) = k;
+      dau = array_daughter(g, U, U_RECT, i, j, k, tx, ty, tz);
+    } else {
+      int q, r, k = 0;
+      hex_locate(U, x, y, q, r, flags);
+      if (ld(&U->i1) > 0) {
+        const double zl = ld(&U->d[4]), zp = ld(&U->d[5]);
+        k = rect_index(zl, zp, z);
+        flags |= near_wall(zl, zp, k, z);
+      }
+      st.a(l) = q; st.b(l) = r; st.c(l) = k;
+      dau = array_daughter(g, U, U_HEX, q, r, k, tx, ty, tz);
+    }
+    if (dau < 0) return false;
+    Tx = Tx + tx;
+    Ty = Ty + ty;
+    Tz = Tz + tz;
+    u = dau;
+  }
+  return false;
+}
+
+// distance candidates of level l (canonical order, O13)
+__device__ __forceinline__ void level_distances(const DevGeom& g, Stack& st, int l, double rx, double ry,
+                                                double rz, double u, double v, double w, int os_l,
+                                                int os_s, Best& b) {
+  const double x = rx - st.T(l, 0), y = ry - st.T(l, 1), z = rz - st.T(l, 2);
+  const DUniv* U = g.univ + st.u(l);
+  const int kind = ld(&U->kind);
+  if (kind == U_CSG) {
+    const int cell = st.a(l);
+    const int h0 = ld(g.cell_hs + cell), h1 = ld(g.cell_hs + cell + 1);
+    for (int h = h0; h < h1; ++h) {
+      const int e = ld(g.hs + h);
+      const int sid = hs_sid(e);
+      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, g.surf + sid, x, y, z, u,
+                                 v, w);
+      if (d < NT_INF) b.consider(d, l, sid, hs_sense(e));
+    }
+  } else if (kind == U_RECT) {
+    const int i = st.a(l), j = st.b(l);
+    if (u > 0.0) b.consider(clamp0((ld(&U->d[0]) + static_cast<double>(i + 1) * ld(&U->d[3]) - x) / u), l, 1, 0);
+    else if (u < 0.0) b.consider(clamp0((ld(&U->d[0]) + static_cast<double>(i) * ld(&U->d[3]) - x) / u), l, 0, 0);
+    if (v > 0.0) b.consider(clamp0((ld(&U->d[1]) + static_cast<double>(j + 1) * ld(&U->d[4]) - y) / v), l, 3, 0);
+    else if (v < 0.0) b.consider(clamp0((ld(&U->d[1]) + static_cast<double>(j) * ld(&U->d[4]) - y) / v), l, 2, 0);
+    if (!ld(&U->is2d)) {
+      const int k = st.c(l);
+      if (w > 0.0) b.consider(clamp0((ld(&U->d[2]) + static_cast<double>(k + 1) * ld(&U->d[5]) - z) / w), l, 5, 0);
+      else if (w < 0.0) b.consider(clamp0((ld(&U->d[2]) + static_cast<double>(k) * ld(&U->d[5]) - z) / w), l, 4, 0);
+    }
+  } else {
+    double t0, t1, t2, m0, m1, m2;
+    hex_t(U, x, y, t0, t1, t2);
+    hex_m(st.a(l), st.b(l), m0, m1, m2);
+    const double p = ld(&U->d[2]);
+    const double tk[3] = {t0, t1, t2}, mk[3] = {m0, m1, m2};
+#pragma unroll
+    for (int k = 0; k < 3; ++k) {
+      const double gk = ld(&U->d[10 + 2 * k]) * u + ld(&U->d[11 + 2 * k]) * v;
+      if (gk > 0.0) b.consider(clamp0((p * ((mk[k] + 0.5) - tk[k])) / gk), l, k, 0);
+      else if (gk < 0.0) b.consider(clamp0((p * ((mk[k] - 0.5) - tk[k])) / gk), l, k + 3, 0);
+    }
+    if (ld(&U->i1) > 0) {
+      const int k = st.c(l);
+      const double zl = ld(&U->d[4]), zp = ld(&U->d[5]);
+      if (w > 0.0) b.consider(clamp0((zl + static_cast<double>(k + 1) * zp - z) / w), l, 7, 0);
+      else if (w < 0.0) b.consider(clamp0((zl + static_cast<double>(k) * zp - z) / w), l, 6, 0);
+    }
+  }
+}
+
+template <bool TRACE>
+__device__ __forceinline__ void emit(const KRun& R, uint64_t pid, uint32_t seg, int kind, int level, int j,
+                                     int cb, int ca, double s, int terminal, uint32_t flags) {
+  if (!TRACE) return;
+  const unsigned long long slot = atomicAdd(R.trace_count, 1ull);
+  if (slot >= R.trace_cap) return;
+  nt_trace_rec t;
+  t.pid = pid; t.s = s; t.seg = seg; t.cell_before = cb; t.cell_after = ca; t.j = j;
+  t.kind = (uint8_t)kind; t.level = (int8_t)level; t.terminal = (uint8_t)terminal; t.pad = 0;
+  t.flags = flags;
+  R.trace[slot] = t;
+}
+
+enum { C_PART = 0, C_SEG, C_CROSS, C_REFL, C_LEAK, C_COLL, C_ABS, C_LOST, C_CAP, C_FLAG, C_CBL0 };
+
+template <bool TRACE, bool STATES>
+__global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KRun R) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
+  const int nmc = g.n_mc;
+  double* s_len = reinterpret_cast<double*>(smem);
+  unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(s_len + nmc);
+  unsigned int* s_exit = reinterpret_cast<unsigned int*>(s_cnt + kNC);
+  double* sT = reinterpret_cast<double*>(s_exit + ((nmc + 1) & ~1));
+  Stack st;
+  st.sT = sT;
+  st.si = reinterpret_cast<int*>(sT + 3 * g.max_depth * B);
+  st.B = B; st.tid = tid; st.maxd = g.max_depth;
+  for (int i = tid; i < nmc; i += B) { s_len[i] = 0.0; s_exit[i] = 0u; }
+  for (int i = tid; i < kNC; i += B) s_cnt[i] = 0ull;
+  __syncthreads();
+
+  // particle state (registers)
+  double rx = 0, ry = 0, rz = 0, u = 0, v = 0, w = 0, tau = 0;
+  uint64_t pid = 0, idx = 0;
+  uint32_t epoch = 0, flags = 0, nseg = 0, ncross = 0, ncoll = 0;
+  int L = 0, mc = 0, os_l = -1, os_s = -1;
+  // phase: 0 = needs a history, 1 = needs a descent, 2 = moving
+  int phase = 0;
+  // pending descent
+  int d_l0 = 0, d_u = 0, d_fsid = -1, d_fsense = 0;
+  double d_Tx = 0, d_Ty = 0, d_Tz = 0;
+  // pending crossing record (trace only)
+  int p_l = -1, p_j = -1, p_cb = -1;
+  double p_s = 0;
+  const uint32_t max_seg = static_cast<uint32_t>(R.max_seg);
+
+  for (;;) {
+    int term = NT_T_NONE;
+    if (phase == 0) {
+      // ---- claim the next history (warp-aggregated atomic) and give birth (W1, O17-O18)
+      const unsigned mask = __activemask();
+      const int leader = __ffs(mask) - 1;
+      const int rank = __popc(mask & ((1u << lane) - 1u));
+      unsigned long long base = 0;
+      if (lane == leader) base = atomicAdd(R.counter, static_cast<unsigned long long>(__popc(mask)));
+      base = __shfl_sync(mask, base, leader);
+      idx = base + rank;
+      if (idx >= R.n) break;
+      pid = R.pid0 + idx;
+      double xa, xb;
+      draw2(R.seed, pid, 0, 0, xa, xb);
+      const double xi_tau = xb;
+      if (STATES) {
+        rx = R.states[idx]; ry = R.states[R.n + idx]; rz = R.states[2 * R.n + idx];
+        u = R.states[3 * R.n + idx]; v = R.states[4 * R.n + idx]; w = R.states[5 * R.n + idx];
+      } else {
+        double xmu, xphi, xx, xy, xz, unused;
+        draw2(R.seed, pid, 0, 1, xmu, xphi);
+        draw2(R.seed, pid, 0, 2, xx, xy);
+        draw2(R.seed, pid, 0, 3, xz, unused);
+        rx = R.lo[0] + R.w[0] * xx;
+        ry = R.lo[1] + R.w[1] * xy;
+        rz = R.lo[2] + R.w[2] * xz;
+        isotropic(xmu, xphi, u, v, w);
+      }
+      tau = -spec_log(xi_tau);
+      epoch = 0; flags = 0; nseg = 0; ncross = 0; ncoll = 0; os_l = -1; os_s = -1;
+      d_l0 = 0; d_u = g.root; d_Tx = d_Ty = d_Tz = 0.0; d_fsid = -1; d_fsense = 0;
+      p_l = -2;   // no pending crossing record: a failure here is a birth loss
+      phase = 1;
+    }
+    if (phase == 1) {
+      // ---- Alg. 7 / Alg. 8 descent (single call site for birth and every crossing)
+      const bool ok = descend(g, st, d_l0, d_u, d_Tx, d_Ty, d_Tz, rx, ry, rz, d_fsid, d_fsense, L, mc, flags);
+      if (!ok) {
+        flags |= NT_F3;
+        term = NT_T_LOST;
+        if (p_l == -2) emit<TRACE>(R, pid, 0, NT_EV_CROSS, -1, -1, -1, -1, 0.0, NT_T_LOST, flags);
+        else emit<TRACE>(R, pid, nseg - 1, NT_EV_CROSS, p_l, p_j, p_cb, -1, p_s, NT_T_LOST, flags);
+      } else {
+        if (p_l != -2)
+          emit<TRACE>(R, pid, nseg - 1, NT_EV_CROSS, p_l, p_j, p_cb, TRACE ? ld(g.mc_cell + mc) : 0, p_s,
+                      NT_T_NONE, flags);
+        phase = 2;
+        continue;
+      }
+    } else {
+      // ---- one segment (W2)
+      if (nseg >= max_seg) {
+        flags |= NT_F3;
+        term = NT_T_CAPPED;
+        emit<TRACE>(R, pid, nseg, NT_EV_COLLIDE, -1, -1, ld(g.mc_cell + mc), -1, 0.0, NT_T_CAPPED, flags);
+      } else {
+        Best b;
+        b.d = NT_INF; b.d2 = NT_INF; b.l = -1; b.j = -1; b.sense = 0;
+        for (int l = 0; l < L; ++l) level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+        const double sig = ld(g.mc_st + mc);
+        const double ds = b.d;
+        const double dc = sig > 0.0 ? tau / sig : NT_INF;
+        const double g2 = b.d2 - ds, gc = fabs(dc - ds);
+        if ((g2 > 0.0 && g2 <= kFlagDist) || (gc > 0.0 && gc <= kFlagDist)) flags |= NT_F2;
+        const int cell_before = TRACE ? ld(g.mc_cell + mc) : 0;
+        if (ds == NT_INF && dc == NT_INF) {
+          flags |= NT_F3;
+          term = NT_T_LOST;
+          emit<TRACE>(R, pid, nseg, NT_EV_CROSS, -1, -1, cell_before, -1, 0.0, NT_T_LOST, flags);
+        } else if (ds < dc) {
+          // Alg. 2 "while d < tau/Sigma": tau -= Sigma d, move, cross
+          const double s = ds;
+          atomicAdd(s_len + mc, s);
+          rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
+          const double tt = tau - sig * s;
+          tau = tt > 0.0 ? tt : 0.0;
+          ++nseg;
+          const int l = b.l, j = b.j;
+          const int meta = (l == 0 && g.root_kind == U_CSG) ? ld(g.surf_meta + j) : 0;
+          const int bc = meta >> 4;
+          if (bc == NT_BC_VACUUM) {
+            atomicAdd(s_exit + mc, 1u);
+            ++ncross;
+            term = NT_T_LEAKED;
+            emit<TRACE>(R, pid, nseg - 1, NT_EV_LEAK, 0, j, cell_before, -1, s, NT_T_LEAKED, flags);
+          } else if (bc == NT_BC_REFLECT) {
+            const int ax = meta & 15;
+            if (ax == 0) u = -u; else if (ax == 1) v = -v; else w = -w;
+            os_l = 0; os_s = j;
+            emit<TRACE>(R, pid, nseg - 1, NT_EV_REFLECT, 0, j, cell_before, cell_before, s, NT_T_NONE, flags);
+          } else {
+            atomicAdd(s_exit + mc, 1u);
+            ++ncross;
+            atomicAdd(s_cnt + C_CBL0 + l, 1ull);
+            const int ul = st.u(l);
+            const DUniv* U = g.univ + ul;
+            const int kind = ld(&U->kind);
+            p_l = l; p_j = j; p_cb = cell_before; p_s = s;
+            if (kind == U_CSG) {   // O9': far side of surface j in universe(l)
+              d_l0 = l; d_u = ul; d_Tx = st.T(l, 0); d_Ty = st.T(l, 1); d_Tz = st.T(l, 2);
+              d_fsid = j; d_fsense = b.sense ^ 1;
+              os_l = l; os_s = j;
+              phase = 1;
+            } else {               // Alg. 6: tile +- 1, then the new tile's daughter
+              int ta = st.a(l), tb = st.b(l), tc = st.c(l);
+              if (kind == U_RECT) {
+                const int dir = (j & 1) ? 1 : -1, ax = j >> 1;
+                if (ax == 0) ta += dir; else if (ax == 1) tb += dir; else tc += dir;
+              } else if (j < 6) {
+                ta += (j == 0 || j == 5) ? 1 : ((j == 2 || j == 3) ? -1 : 0);
+                tb += (j == 1 || j == 2) ? 1 : ((j == 4 || j == 5) ? -1 : 0);
+              } else {
+                tc += (j == 7) ? 1 : -1;
+              }
+              st.a(l) = ta; st.b(l) = tb; st.c(l) = tc;
+              double tx, ty, tz;
+              const int dau = array_daughter(g, U, kind, ta, tb, tc, tx, ty, tz);
+              os_l = -1; os_s = -1;
+              if (dau < 0) {
+                flags |= NT_F3;
+                term = NT_T_LOST;
+                emit<TRACE>(R, pid, nseg - 1, NT_EV_CROSS, l, j, cell_before, -1, s, NT_T_LOST, flags);
+              } else {
+                d_l0 = l + 1; d_u = dau;
+                d_Tx = st.T(l, 0) + tx; d_Ty = st.T(l, 1) + ty; d_Tz = st.T(l, 2) + tz;
+                d_fsid = -1; d_fsense = 0;
+                phase = 1;
+              }
+            }
+          }
+        } else {
+          // ---- collision at tau / Sigma_t: absorb or scatter isotropically (O14, O15)
+          const double s = dc;
+          atomicAdd(s_len + mc, s);
+          rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
+          ++nseg;
+          ++ncoll;
+          os_l = -1; os_s = -1;
+          ++epoch;
+          double xa, xb;
+          draw2(R.seed, pid, epoch, 0, xa, xb);
+          if (xa < ld(g.mc_pabs + mc)) {
+            term = NT_T_ABSORBED;
+            emit<TRACE>(R, pid, nseg - 1, NT_EV_COLLIDE, -1, -1, cell_before, cell_before, s, NT_T_ABSORBED,
+                        flags);
+          } else {
+            double xmu, xphi;
+            draw2(R.seed, pid, epoch, 1, xmu, xphi);
+            isotropic(xmu, xphi, u, v, w);
+            tau = -spec_log(xb);
+            emit<TRACE>(R, pid, nseg - 1, NT_EV_COLLIDE, -1, -1, cell_before, cell_before, s, NT_T_NONE, flags);
+          }
+        }
+      }
+      if (term == NT_T_NONE) continue;
+    }
+    // ---- history ended: per-history counters into the block tallies
+    phase = 0;
+    atomicAdd(s_cnt + C_PART, 1ull);
+    atomicAdd(s_cnt + C_SEG, static_cast<unsigned long long>(nseg));
+    atomicAdd(s_cnt + C_CROSS, static_cast<unsigned long long>(ncross));
+    atomicAdd(s_cnt + C_COLL, static_cast<unsigned long long>(ncoll));
+    atomicAdd(s_cnt + C_REFL, static_cast<unsigned long long>(nseg - ncross - ncoll));
+    const int tcn = term == NT_T_ABSORBED ? C_ABS : term == NT_T_LEAKED ? C_LEAK : term == NT_T_LOST ? C_LOST : C_CAP;
+    atomicAdd(s_cnt + tcn, 1ull);
+    if (flags) atomicAdd(s_cnt + C_FLAG, 1ull);
+    if (R.pflags) R.pflags[idx] = static_cast<uint8_t>(flags);
+    if (R.pnseg) R.pnseg[idx] = nseg;
+    if (R.pterm) R.pterm[idx] = static_cast<uint8_t>(term);
+  }
+
+  __syncthreads();
+  for (int i = tid; i < nmc; i += B) {
+    if (s_len[i] != 0.0) atomicAdd(R.out + i, s_len[i]);
+    if (s_exit[i]) atomicAdd(R.out + nmc + i, static_cast<double>(s_exit[i]));
+  }
+  for (int i = tid; i < kNC; i += B)
+    if (s_cnt[i]) atomicAdd(R.out + 2 * nmc + i, static_cast<double>(s_cnt[i]));
+}
+
+// point location for unit parity (Alg. 7)
+__global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const double* xyz, uint64_t n,
+                                                    int32_t* cell_out, uint8_t* flag_out) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int B = blockDim.x;
+  Stack st;
+  st.sT = reinterpret_cast<double*>(smem);
+  st.si = reinterpret_cast<int*>(st.sT + 3 * g.max_depth * B);
+  st.B = B; st.tid = threadIdx.x; st.maxd = g.max_depth;
+  for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < n; i += (uint64_t)gridDim.x * B) {
+    int L = 0, mc = 0;
+    uint32_t fl = 0;
+    const bool ok = descend(g, st, 0, g.root, 0.0, 0.0, 0.0, xyz[i], xyz[n + i], xyz[2 * n + i], -1, 0, L, mc, fl);
+    cell_out[i] = ok ? ld(g.mc_cell + mc) : -1;
+    if (flag_out) flag_out[i] = static_cast<uint8_t>(fl | (ok ? 0u : NT_F3));
+  }
+}
+
+// ---------------------------------------------------------------- host launchers
+size_t generic_smem_bytes(const DevGeom& g, int block) {
+  const size_t nmc = g.n_mc;
+  return nmc * 8 + kNC * 8 + ((nmc + 1) & ~size_t(1)) * 4 + (size_t)g.max_depth * block * (3 * 8 + 4 * 4);
+}
+
+cudaError_t upload_coefficients(const double* host, int n) {
+  return cudaMemcpyToSymbol(c_coef, host, sizeof(double) * n);
+}
+
+cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
+                           int blocks_per_sm, cudaStream_t stream, int* grid_out) {
+  const size_t smem = generic_smem_bytes(g, block);
+  auto pick = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    int bps = blocks_per_sm > 0 ? (blocks_per_sm < occ ? blocks_per_sm : occ) : occ;
+    uint64_t need = (R.n + block - 1) / block;
+    uint64_t grid = (uint64_t)nsm * bps;
+    if (need < grid) grid = need ? need : 1;
+    *grid_out = (int)grid;
+    kern<<<(unsigned)grid, block, smem, stream>>>(g, R);
+    return cudaGetLastError();
+  };
+  if (trace) return states ? pick(k_track_generic<true, true>) : pick(k_track_generic<true, false>);
+  return states ? pick(k_track_generic<false, true>) : pick(k_track_generic<false, false>);
+}
+
+cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,
+                              uint8_t* flag, cudaStream_t stream) {
+  const int block = 256;
+  const size_t smem = (size_t)g.max_depth * block * (3 * 8 + 4 * 4);
+  cudaError_t e = cudaFuncSetAttribute(k_find_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  uint64_t grid = (n + block - 1) / block;
+  if (grid > 148 * 8) grid = 148 * 8;
+  if (grid == 0) return cudaSuccess;
+  k_find_cells<<<(unsigned)grid, block, smem, stream>>>(g, xyz, n, cell, flag);
+  return cudaGetLastError();
+}
+
+}  // namespace nt

@@ -1,0 +1,224 @@
+"""GPU parity: the CUDA path (through the C ABI) against the independent CPU oracle.
+
+Contract (BASELINE.json north_star): event/cell/surface sequences
+bit-exact; segment lengths within 1e-12 relative (the build reaches bit-identity because both
+sides follow the same spec'd arithmetic); per-cell totals within 1e-9 relative (summation order);
+counters exact.  Flagged histories (O16) would be excluded, but with bit-identical walks none
+needs to be.
+"""
+import numpy as np
+import pytest
+
+import workloads
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TRACE_FIELDS = ("pid", "seg", "kind", "level", "j", "cell_before", "cell_after", "terminal", "flags")
+
+
+@pytest.fixture(scope="module")
+def nt():
+    import __graft_entry__
+    __graft_entry__.build()
+    import paper_2406_13849_b200 as nt
+    assert torch.cuda.is_available()
+    return nt
+
+
+@pytest.fixture(scope="module")
+def orc():
+    import oracle
+    oracle.build()
+    return oracle
+
+
+def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, tracker="generic",
+             trace=True, pseudo=False):
+    m = nt.Model.from_spec(spec, device=0, pseudo_array=pseudo)
+    om = orc.OracleModel.from_spec(spec)
+    cap = 400 * max(n, 1) + 64 if trace else 0
+    st_t = None if states is None else torch.tensor(states, dtype=torch.float64, device="cuda")
+    res = m.track(n, seed=seed, pid_begin=pid_begin, pflags=True, per_history=True, trace_cap=cap,
+                  max_segments=max_segments, states=st_t, tracker=tracker)
+    torch.cuda.synchronize()
+    g = m.unpack(res["out"])
+    o = om.run(n, seed=seed, pid_begin=pid_begin, pflags=True, trace_cap=cap, max_segments=max_segments,
+               states=states)
+    assert g["counters"] == o["counters"]
+    assert np.array_equal(g["exits"], o["exits"])
+    assert np.allclose(g["len"], o["len"], rtol=1e-12, atol=1e-300)
+    assert np.array_equal(res["pflags"].cpu().numpy()[:n], o["pflags"])
+    if trace:
+        gt, ot = nt.Model.trace_records(res), o["trace"]
+        assert len(gt) == len(ot)
+        for f in TRACE_FIELDS:
+            assert np.array_equal(gt[f], ot[f]), f
+        # per-segment tolerance of the contract, then the stronger bit-identity we reach
+        assert np.all(np.abs(gt["s"] - ot["s"]) <= 1e-12 * np.abs(ot["s"]) + 1e-13)
+        assert np.array_equal(gt["s"], ot["s"])
+        # per-history summaries agree with the trace
+        nseg = res["pnseg"].cpu().numpy()[:n]
+        cnt = np.bincount((gt["pid"] - pid_begin).astype(np.int64)[gt["kind"] <= 3], minlength=n)
+        assert nseg.sum() == g["counters"]["segments"]
+    return m, g, o, res
+
+
+CONFIG_N = {"c1": 2000, "c2": 600, "c3": 600, "c4": 600, "c5m": 600, "c5r": 600}
+
+
+@pytest.mark.parametrize("cfg", list(CONFIG_N))
+def test_config_trace_parity(nt, orc, cfg):
+    """Every BASELINE config: full traces bit-exact vs the oracle (seeded, small batch)."""
+    spec, _ = workloads.config(cfg)
+    _, g, o, _ = _compare(nt, orc, spec, CONFIG_N[cfg], seed=1)
+    assert g["counters"]["lost"] == 0 and g["counters"]["capped"] == 0
+
+
+@pytest.mark.parametrize("seed", workloads.PARITY_SEEDS)
+def test_c3_parity_seeds(nt, orc, seed):
+    spec, _ = workloads.config("c3")
+    _compare(nt, orc, spec, 1000, seed=seed, pid_begin=12345, trace=False)
+
+
+@pytest.mark.parametrize("name", ["sphere_in_box", "hex_pins_small_pointy", "hex_pins_small_flat",
+                                  "rect3d_small", "lattice3_nested", "lattice3_flat", "infinite_medium",
+                                  "c1_void_vacuum"])
+def test_test_models_parity(nt, orc, name):
+    """Planes, spheres, 3-D rect and hex z-stacks, translations, void + vacuum leakage."""
+    M = workloads.models
+    spec = {"sphere_in_box": M.sphere_in_box, "hex_pins_small_pointy": lambda: M.hex_pins_small("pointy"),
+            "hex_pins_small_flat": lambda: M.hex_pins_small("flat"), "rect3d_small": M.rect3d_small,
+            "lattice3_nested": M.lattice3_nested, "lattice3_flat": lambda: M.lattice3_nested(True),
+            "infinite_medium": M.infinite_medium,
+            "c1_void_vacuum": lambda: M.c1_pincell(bc="vacuum", void=True)}[name]()
+    _compare(nt, orc, spec, 700, seed=2)
+
+
+@pytest.mark.parametrize("n", [1, 31, 257, 1000])
+def test_ragged_batches_and_large_pids(nt, orc, n):
+    """Ragged batch sizes (partial warps / blocks) and pids above 2^32 (counter hi word)."""
+    spec, _ = workloads.config("c2")
+    _compare(nt, orc, spec, n, seed=3, pid_begin=(1 << 33) + 17)
+
+
+def test_capped_histories(nt, orc):
+    """max_segments reached -> CAPPED (F3) on both sides, same extra trace record."""
+    spec, _ = workloads.config("c1")
+    _, g, o, _ = _compare(nt, orc, spec, 300, seed=4, max_segments=7)
+    assert g["counters"]["capped"] > 0
+
+
+def test_lost_at_birth(nt, orc):
+    """Births outside every root cell are LOST at birth (source box larger than the model)."""
+    spec = workloads.c1_pincell()
+    spec["source"] = {"lo": [-1.0, -1.0, 0.0], "hi": [1.0, 1.0, 365.76]}
+    _, g, o, _ = _compare(nt, orc, spec, 500, seed=5)
+    assert g["counters"]["lost"] > 0
+
+
+def test_explicit_states(nt, orc):
+    """nt_track_states: explicit birth states (chord rays through the void pincell)."""
+    spec = workloads.c1_pincell(bc="vacuum", void=True)
+    rng = np.random.default_rng(0)
+    n = 500
+    r = rng.uniform([-0.63, -0.63, 0.0], [0.63, 0.63, 365.76], size=(n, 3))
+    om = rng.normal(size=(n, 3))
+    om /= np.linalg.norm(om, axis=1, keepdims=True)
+    _compare(nt, orc, spec, n, seed=6, states=np.concatenate([r.T, om.T]))
+
+
+def test_zero_particles(nt):
+    spec, _ = workloads.config("c1")
+    m = nt.Model.from_spec(spec, device=0)
+    res = m.track(0, seed=1)
+    torch.cuda.synchronize()
+    assert float(res["out"].abs().sum()) == 0.0
+
+
+def test_find_cells_parity(nt, orc):
+    """Point location (Alg. 7) on random points of every config, exact cell ids."""
+    rng = np.random.default_rng(1)
+    for cfg in CONFIG_N:
+        spec, _ = workloads.config(cfg)
+        m = nt.Model.from_spec(spec, device=0)
+        om = orc.OracleModel.from_spec(spec)
+        lo, hi = np.array(spec["source"]["lo"]), np.array(spec["source"]["hi"])
+        pts = rng.uniform(lo, hi, size=(20000, 3)).T.copy()
+        gc, gf = m.find_cells(torch.tensor(pts, device="cuda"))
+        oc, of = om.find_cells(pts)
+        assert np.array_equal(gc.cpu().numpy(), oc)
+        assert np.array_equal(gf.cpu().numpy(), of)
+
+
+@pytest.mark.parametrize("cfg", ["c2", "c3", "c5r"])
+def test_pseudo_array_equals_generic(nt, cfg):
+    """P13: pseudo-array (ST) mode = generic tracker for RECT lattices: same walk, bit-exact
+    (surface ids j differ by construction)."""
+    spec, _ = workloads.config(cfg)
+    a = nt.Model.from_spec(spec, device=0)
+    b = nt.Model.from_spec(spec, device=0, pseudo_array=True)
+    ra = a.track(600, seed=7, trace_cap=400000, pflags=True)
+    rb = b.track(600, seed=7, trace_cap=400000, pflags=True)
+    torch.cuda.synchronize()
+    ta, tb = nt.Model.trace_records(ra), nt.Model.trace_records(rb)
+    ok = (ra["pflags"] == 0) & (rb["pflags"] == 0)
+    ok = ok.cpu().numpy()[:600]
+    ma, mb = ok[(ta["pid"]).astype(np.int64)], ok[(tb["pid"]).astype(np.int64)]
+    ta, tb = ta[ma], tb[mb]
+    assert len(ta) == len(tb)
+    for f in ("pid", "seg", "kind", "level", "cell_before", "cell_after", "terminal", "s"):
+        assert np.array_equal(ta[f], tb[f]), f
+
+
+def test_host_entry_point(nt):
+    """nt_track_host (host output buffer) equals the device-buffer call."""
+    spec, _ = workloads.config("c2")
+    m = nt.Model.from_spec(spec, device=0)
+    a = m.track(5000, seed=9)["out"].cpu().numpy()
+    b = m.track_host(5000, seed=9)
+    assert np.array_equal(a[-18:], b[-18:])
+    assert np.allclose(a, b, rtol=1e-12, atol=0)
+
+
+def test_determinism_and_additivity(nt):
+    """Counters exact and lengths to summation order across repeat runs and pid splits (P14)."""
+    spec, _ = workloads.config("c3")
+    m = nt.Model.from_spec(spec, device=0)
+    ab = m.unpack(m.track(200000, seed=11)["out"])
+    ab2 = m.unpack(m.track(200000, seed=11)["out"])
+    a = m.unpack(m.track(70000, seed=11)["out"])
+    b = m.unpack(m.track(130000, seed=11, pid_begin=70000)["out"])
+    assert ab["counters"] == ab2["counters"]
+    assert ab["counters"] == {k: a["counters"][k] + b["counters"][k] for k in ab["counters"]}
+    assert np.allclose(ab["len"], a["len"] + b["len"], rtol=1e-11, atol=0)
+    assert np.allclose(ab["len"], ab2["len"], rtol=1e-11, atol=0)
+
+
+def test_full_size_c3_sampled(nt, orc):
+    """BASELINE size (C3, 1e8 histories) in the bench launch configuration: invariants on the
+    whole batch, and per-history segment counts / terminals / flags of sampled pid windows
+    recomputed one by one by the oracle."""
+    spec, n = workloads.config("c3")
+    m = nt.Model.from_spec(spec, device=0)
+    res = m.track(n, seed=workloads.SEED, pflags=True, per_history=True)
+    torch.cuda.synchronize()
+    g = m.unpack(res["out"])
+    c = g["counters"]
+    assert c["particles"] == n and c["lost"] == 0 and c["capped"] == 0
+    assert c["segments"] == c["crossings"] + c["reflections"] + c["collisions"]
+    assert c["particles"] == c["absorptions"] + c["leaks"]
+    assert int(res["pnseg"].sum()) == c["segments"]
+    om = orc.OracleModel.from_spec(spec)
+    nseg = res["pnseg"]
+    term = res["pterm"]
+    fl = res["pflags"]
+    rng = np.random.default_rng(2)
+    starts = sorted(set([0, n - 64] + list(rng.integers(0, n - 64, size=14))))
+    for s0 in starts:
+        o = om.run(64, seed=workloads.SEED, pid_begin=int(s0), pflags=True, trace_cap=64 * 400)
+        per = np.bincount(o["trace"]["pid"].astype(np.int64) - int(s0), minlength=64)
+        assert np.array_equal(nseg[s0:s0 + 64].cpu().numpy(), per)
+        assert np.array_equal(fl[s0:s0 + 64].cpu().numpy(), o["pflags"])
+        last = o["trace"][np.r_[np.nonzero(np.diff(o["trace"]["pid"]))[0], len(o["trace"]) - 1]]
+        assert np.array_equal(term[s0:s0 + 64].cpu().numpy(), last["terminal"])
