@@ -244,14 +244,8 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
                o_ctr = place(blob, F.cell_tr), o_univ = place(blob, F.univ), o_bih = place(blob, F.bih),
                o_leaf = place(blob, F.bih_leaf), o_fills = place(blob, F.fills), o_st = place(blob, F.mc_st),
                o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell);
-  size_t o_rr2 = 0, o_rtol = 0, o_rsid = 0, o_rcell = 0, o_rmc = 0, o_rbc = 0, o_pou = 0, o_poff = 0, o_pr2 = 0,
-         o_ptol = 0, o_psid = 0, o_pmc = 0;
-  if (F.rect_ok) {
-    o_rr2 = place(blob, F.r_root_r2); o_rtol = place(blob, F.r_root_tol); o_rsid = place(blob, F.r_root_sid);
-    o_rcell = place(blob, F.r_root_cell); o_rmc = place(blob, F.r_root_mc); o_rbc = place(blob, F.r_root_bc);
-    o_pou = place(blob, F.r_pin_of_univ); o_poff = place(blob, F.r_pin_off); o_pr2 = place(blob, F.r_pin_r2);
-    o_ptol = place(blob, F.r_pin_tol); o_psid = place(blob, F.r_pin_sid); o_pmc = place(blob, F.r_pin_mc);
-  }
+  const size_t o_pou = place(blob, F.r_pin_of_univ), o_poff = place(blob, F.r_pin_off),
+               o_psid = place(blob, F.r_pin_sid), o_pmc = place(blob, F.r_pin_mc);
   m->blob_bytes = blob.size();
   m->device = o->device;
   if (o->device >= 0) {
@@ -285,21 +279,11 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     g.mc_st = (const double*)(b + o_st);
     g.mc_pabs = (const double*)(b + o_pabs);
     g.mc_cell = (const int32_t*)(b + o_mcc);
-    if (F.rect_ok) {
-      m->rg = F.rg;
-      m->rg.root_r2 = (const double*)(b + o_rr2);
-      m->rg.root_tol = (const double*)(b + o_rtol);
-      m->rg.root_sid = (const int32_t*)(b + o_rsid);
-      m->rg.root_cell = (const int32_t*)(b + o_rcell);
-      m->rg.root_mc = (const int32_t*)(b + o_rmc);
-      m->rg.root_bc = (const uint8_t*)(b + o_rbc);
-      m->rg.pin_of_univ = (const int32_t*)(b + o_pou);
-      m->rg.pin_off = (const int32_t*)(b + o_poff);
-      m->rg.pin_r2 = (const double*)(b + o_pr2);
-      m->rg.pin_tol = (const double*)(b + o_ptol);
-      m->rg.pin_sid = (const int32_t*)(b + o_psid);
-      m->rg.pin_mc = (const int32_t*)(b + o_pmc);
-    }
+    m->rg = F.rg;
+    m->rg.pin_of_univ = (const int32_t*)(b + o_pou);
+    m->rg.pin_off = (const int32_t*)(b + o_poff);
+    m->rg.pin_sid = (const int32_t*)(b + o_psid);
+    m->rg.pin_mc = (const int32_t*)(b + o_pmc);
   }
   DevGeom& g = m->g;
   g.root = F.root;

@@ -232,8 +232,12 @@ struct Best {
   double d, d2;
   int l, j, sense;
   __device__ __forceinline__ void consider(double dd, int ll, int jj, int ss) {
-    if (dd < d) { d2 = d; d = dd; l = ll; j = jj; sense = ss; }
-    else if (dd < d2) d2 = dd;
+    const bool lt = dd < d;                       // branch-free select form
+    d2 = lt ? d : (dd < d2 ? dd : d2);
+    d = lt ? dd : d;
+    l = lt ? ll : l;
+    j = lt ? jj : j;
+    sense = lt ? ss : sense;
   }
 };
 

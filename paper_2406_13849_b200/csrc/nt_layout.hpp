@@ -73,36 +73,24 @@ struct DevGeom {
   int32_t n_cells, n_surf, root_kind, pad;
 };
 
-// Rect-specialised tracker tables (Alg. 9-10): root = box or concentric CZ annuli with a PZ
-// pair, then K rect levels, then a concentric-CZ pin.  Arrays index rect universes through
-// the generic DUniv table; pins through `pin_*`.
+// Rect-specialised tracker tables (Alg. 9-10): root = axis box or concentric CZ annuli between a
+// PZ pair, then K rect levels, then a concentric-CZ pin.  Surfaces are read from the generic
+// DSurf table (same arithmetic); rect universes from the DUniv table.
 struct RectGeom {
-  int32_t K;               // number of rect levels
-  int32_t root_box;        // 1: root cell is an axis box (6 planes); 0: CZ annuli + PZ pair
-  int32_t root_fill_cell;  // root cell that holds the first rect level (annulus index for CZ roots)
-  int32_t n_root_cells;    // CZ root: number of annuli (cells)
-  int32_t root_univ_child; // universe id of level 1
-  int32_t pad0, pad1, pad2;
-  // box root: walls lo/hi per axis + surface ids + bc
-  double box_lo[3], box_hi[3];
-  int32_t box_sid[6], box_bc[6];
-  // CZ root (annulus k spans [R_{k-1}, R_k)): radii^2, surface ids, cells
-  const double* root_r2;   // [n_root_cells] outer R^2 of annulus k (last may be unbounded -> huge)
-  const double* root_tol;  // proximity tol of each root CZ
-  const int32_t* root_sid; // CZ surface id bounding annulus k from outside (-1 none)
-  const int32_t* root_cell;// global cell id of annulus k
-  const int32_t* root_mc;  // material-cell index of annulus k (-1 = filled: core)
-  const uint8_t* root_bc;  // bc of the outer CZ of annulus k
-  double z_lo, z_hi;       // PZ pair
-  int32_t zsid[2], zbc[2];
-  double ztol;
-  // pins: per universe id -> pin record index (-1 if not a pin)
-  const int32_t* pin_of_univ;
-  const int32_t* pin_off;  // [n_pins+1] offsets into pin_r2 / pin_sid ... (annuli count = n+1)
-  const double* pin_r2;    // radii^2 ascending
-  const double* pin_tol;
-  const int32_t* pin_sid;  // CZ surface ids
-  const int32_t* pin_mc;   // [pin_off[p] + p + k] material-cell index of annulus k (n+1 per pin)
+  int32_t K;                 // number of rect levels (0..4)
+  int32_t root_box;          // 1: root cell is an axis box; 0: CZ annuli + PZ pair
+  int32_t root_fill_cell;    // root cell holding level 1 (box cell / innermost annulus)
+  int32_t n_root_cells;      // CZ root: number of annuli
+  int32_t root_univ_child;   // universe id of level 1
+  int32_t box_sid[6];        // box root: PX-, PX+, PY-, PY+, PZ-, PZ+ surface ids
+  int32_t zsid[2];           // CZ root: lower / upper PZ surface ids
+  int32_t root_sid[16];      // annulus k: outer CZ surface id (inner one = root_sid[k-1])
+  int32_t root_cell[16];     // annulus k: global cell id
+  int32_t root_mc[16];       // annulus k: material-cell index (-1 for the core annulus)
+  const int32_t* pin_of_univ;  // per universe: pin index or -1
+  const int32_t* pin_off;      // [n_pins+1] offsets into pin_sid (pin p has off[p+1]-off[p] CZs)
+  const int32_t* pin_sid;      // pin CZ surface ids, ascending radius
+  const int32_t* pin_mc;       // material-cell index of annulus k of pin p at pin_off[p] + p + k
 };
 
 }  // namespace nt

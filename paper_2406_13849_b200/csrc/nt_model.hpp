@@ -63,10 +63,7 @@ struct Flat {
   int rect_K = 0;
   std::string rect_why;
   RectGeom rg{};
-  std::vector<double> r_root_r2, r_root_tol, r_pin_r2, r_pin_tol;
-  std::vector<int32_t> r_root_sid, r_root_cell, r_root_mc, r_pin_of_univ, r_pin_off, r_pin_sid,
-      r_pin_mc;
-  std::vector<uint8_t> r_root_bc;
+  std::vector<int32_t> r_pin_of_univ, r_pin_off, r_pin_sid, r_pin_mc;
 };
 
 struct BuildOpts { int device = 0, max_leaf = 4, pseudo = 0; double ct = 1.0, ci = 1.0; };

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "../../include/nestrack.h"
 #include "nt_geom.cuh"
@@ -27,16 +28,17 @@ namespace nt {
 
 
 
-// per-thread universe stack in shared memory
+// per-thread universe stack in shared memory, level-major: [level][field][B] so that one
+// level's fields sit at fixed offsets from one per-level base (conflict-free across a warp)
 struct Stack {
-  int* si;      // [4][maxd][B]: u, a, b, c
-  double* sT;   // [3][maxd][B]
-  int B, tid, maxd;
-  __device__ __forceinline__ int& u(int l) { return si[(0 * maxd + l) * B + tid]; }
-  __device__ __forceinline__ int& a(int l) { return si[(1 * maxd + l) * B + tid]; }
-  __device__ __forceinline__ int& b(int l) { return si[(2 * maxd + l) * B + tid]; }
-  __device__ __forceinline__ int& c(int l) { return si[(3 * maxd + l) * B + tid]; }
-  __device__ __forceinline__ double& T(int l, int k) { return sT[(k * maxd + l) * B + tid]; }
+  int* si;      // [maxd][4][B]: u, a, b, c   (thread-offset already applied)
+  double* sT;   // [maxd][3][B]               (thread-offset already applied)
+  int B;
+  __device__ __forceinline__ int& u(int l) { return si[(4 * l + 0) * B]; }
+  __device__ __forceinline__ int& a(int l) { return si[(4 * l + 1) * B]; }
+  __device__ __forceinline__ int& b(int l) { return si[(4 * l + 2) * B]; }
+  __device__ __forceinline__ int& c(int l) { return si[(4 * l + 3) * B]; }
+  __device__ __forceinline__ double& T(int l, int k) { return sT[(3 * l + k) * B]; }
 };
 
 // Alg. 7 descent from level l0 in universe u with frame translation T; forced sense applies
@@ -44,7 +46,7 @@ struct Stack {
 __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int u, double Tx, double Ty,
                                      double Tz, double rx, double ry, double rz, int fsid, int fsense,
                                      int& L, int& mc, uint32_t& flags) {
-  for (int l = l0; l < st.maxd; ++l) {
+  for (int l = l0; l < kMaxDepth; ++l) {
     st.u(l) = u;
     st.T(l, 0) = Tx;
     st.T(l, 1) = Ty;
@@ -171,9 +173,9 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
   unsigned int* s_exit = reinterpret_cast<unsigned int*>(s_cnt + kNC);
   double* sT = reinterpret_cast<double*>(s_exit + ((nmc + 1) & ~1));
   Stack st;
-  st.sT = sT;
-  st.si = reinterpret_cast<int*>(sT + 3 * g.max_depth * B);
-  st.B = B; st.tid = tid; st.maxd = g.max_depth;
+  st.sT = sT + tid;
+  st.si = reinterpret_cast<int*>(sT + 3 * g.max_depth * B) + tid;
+  st.B = B;
   for (int i = tid; i < nmc; i += B) { s_len[i] = 0.0; s_exit[i] = 0u; }
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0ull;
   __syncthreads();
@@ -241,9 +243,9 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           emit<TRACE>(R, pid, nseg - 1, NT_EV_CROSS, p_l, p_j, p_cb, TRACE ? ld(g.mc_cell + mc) : 0, p_s,
                       NT_T_NONE, flags);
         phase = 2;
-        continue;
       }
-    } else {
+    }
+    if (phase == 2) {
       // ---- one segment (W2)
       if (nseg >= max_seg) {
         flags |= NT_F3;
@@ -374,15 +376,19 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
     if (s_cnt[i]) atomicAdd(R.out + 2 * nmc + i, static_cast<double>(s_cnt[i]));
 }
 
+}  // namespace nt
+#include "rect_kernel.cuh"
+namespace nt {
+
 // point location for unit parity (Alg. 7)
 __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const double* xyz, uint64_t n,
                                                     int32_t* cell_out, uint8_t* flag_out) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x;
   Stack st;
-  st.sT = reinterpret_cast<double*>(smem);
-  st.si = reinterpret_cast<int*>(st.sT + 3 * g.max_depth * B);
-  st.B = B; st.tid = threadIdx.x; st.maxd = g.max_depth;
+  st.sT = reinterpret_cast<double*>(smem) + threadIdx.x;
+  st.si = reinterpret_cast<int*>(reinterpret_cast<double*>(smem) + 3 * g.max_depth * B) + threadIdx.x;
+  st.B = B;
   for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < n; i += (uint64_t)gridDim.x * B) {
     int L = 0, mc = 0;
     uint32_t fl = 0;
@@ -424,6 +430,47 @@ cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool sta
   };
   if (trace) return states ? pick(k_track_generic<true, true>) : pick(k_track_generic<true, false>);
   return states ? pick(k_track_generic<false, true>) : pick(k_track_generic<false, false>);
+}
+
+cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states,
+                        int block, int blocks_per_sm, cudaStream_t stream, int* grid_out) {
+  const size_t nmc = g.n_mc;
+  const size_t smem = nmc * 8 + kNC * 8 + ((nmc + 1) & ~size_t(1)) * 4;
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    const int bps = blocks_per_sm > 0 ? (blocks_per_sm < occ ? blocks_per_sm : occ) : occ;
+    uint64_t need = (R.n + block - 1) / block, grid = (uint64_t)nsm * bps;
+    if (need < grid) grid = need ? need : 1;
+    *grid_out = (int)grid;
+    kern<<<(unsigned)grid, block, smem, stream>>>(g, rg, R);
+    return cudaGetLastError();
+  };
+  auto pick_k = [&](auto box, auto tr, auto st) -> cudaError_t {
+    constexpr bool BOX = decltype(box)::value, TR = decltype(tr)::value, ST = decltype(st)::value;
+    switch (rg.K) {
+      case 0: return go(k_track_rect<0, BOX, TR, ST>);
+      case 1: return go(k_track_rect<1, BOX, TR, ST>);
+      case 2: return go(k_track_rect<2, BOX, TR, ST>);
+      case 3: return go(k_track_rect<3, BOX, TR, ST>);
+      case 4: return go(k_track_rect<4, BOX, TR, ST>);
+      default: return cudaErrorNotSupported;
+    }
+  };
+  using T = std::true_type;
+  using F = std::false_type;
+  if (rg.root_box) {
+    if (trace) return states ? pick_k(T{}, T{}, T{}) : pick_k(T{}, T{}, F{});
+    return states ? pick_k(T{}, F{}, T{}) : pick_k(T{}, F{}, F{});
+  }
+  if (trace) return states ? pick_k(F{}, T{}, T{}) : pick_k(F{}, T{}, F{});
+  return states ? pick_k(F{}, F{}, T{}) : pick_k(F{}, F{}, F{});
 }
 
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,

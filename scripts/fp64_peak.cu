@@ -1,0 +1,32 @@
+// Microbenchmark: fp64 FMA throughput (DFMA) on the whole chip, to check the derived peak
+// 148 SM x 64 FP64 lanes x 2 flop x clock used as the ALU roofline denominator.
+#include <cstdio>
+#include <cuda_runtime.h>
+__global__ void dfma_loop(double* out, int iters, double a, double b) {
+  double x0 = threadIdx.x, x1 = x0 + 1, x2 = x0 + 2, x3 = x0 + 3, x4 = x0 + 4, x5 = x0 + 5, x6 = x0 + 6, x7 = x0 + 7;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
+    }
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = x0 + x1 + x2 + x3 + x4 + x5 + x6 + x7;
+}
+int main() {
+  int nsm; cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  const int block = 256, grid = nsm * 8, iters = 4096;
+  double* out; cudaMalloc(&out, sizeof(double) * grid * block);
+  dfma_loop<<<grid, block>>>(out, 16, 0.999999, 1e-7);
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  float best = 1e30f;
+  for (int r = 0; r < 5; ++r) {
+    cudaEventRecord(e0);
+    dfma_loop<<<grid, block>>>(out, iters, 0.999999, 1e-7);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
+  }
+  double flops = 2.0 * 8 * 16 * (double)iters * grid * block;
+  printf("{\"fp64_fma_tflops\": %.3f, \"sms\": %d, \"ms\": %.3f}\n", flops / best / 1e9, nsm, best);
+  return 0;
+}

@@ -1,0 +1,7 @@
+#!/bin/bash
+# quick iteration: GPU parity tests (short) + small bench
+cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
+timeout 900 python -m pytest tests -m gpu -x -q --timeout 600 -k "not full_size" > gpurun_out/pytest_gpu.log 2>&1
+echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
+timeout 600 python bench.py --steps 2 --warmup 1 --particles 1e7 --no-cpu-baseline --no-e2e ${BENCH_ARGS} > gpurun_out/bench_small.log 2>&1
+echo "bench exit $?" >> gpurun_out/bench_small.log

@@ -150,3 +150,14 @@ def test_pseudo_array_cell_counts(nt):
     spec4, _ = workloads.config("c4")
     c = _host(nt, spec4, pseudo_array=True)
     assert c.info["n_cells"] > 217 + 19
+
+
+@pytest.mark.parametrize("cfg,ok,K", [("c1", 1, 0), ("c2", 1, 1), ("c3", 1, 2), ("c5r", 1, 3),
+                                      ("c4", 0, 0), ("c5m", 0, 0)])
+def test_rect_specialisable_gate(nt, cfg, ok, K):
+    """NT_TRACKER_RECT accepts exactly the root -> RECT^K -> pin models (Alg. 9-10 shape)."""
+    spec, _ = workloads.config(cfg)
+    m = _host(nt, spec)
+    assert m.info["rect_specialisable"] == ok
+    if ok:
+        assert m.info["rect_levels"] == K

@@ -222,3 +222,30 @@ def test_full_size_c3_sampled(nt, orc):
         assert np.array_equal(fl[s0:s0 + 64].cpu().numpy(), o["pflags"])
         last = o["trace"][np.r_[np.nonzero(np.diff(o["trace"]["pid"]))[0], len(o["trace"]) - 1]]
         assert np.array_equal(term[s0:s0 + 64].cpu().numpy(), last["terminal"])
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c5r"])
+def test_rect_tracker_bit_identical(nt, orc, cfg):
+    """P13: the rect-specialised tracker (Alg. 9-10 analogue) reproduces the generic tracker
+    and the oracle bit for bit on every rect-shaped config."""
+    spec, _ = workloads.config(cfg)
+    _compare(nt, orc, spec, 600, seed=8, tracker="rect")
+
+
+def test_rect_tracker_full_counters_match_generic(nt):
+    spec, _ = workloads.config("c3")
+    m = nt.Model.from_spec(spec, device=0)
+    a = m.unpack(m.track(300000, seed=13)["out"])
+    b = m.unpack(m.track(300000, seed=13, tracker="rect")["out"])
+    assert a["counters"] == b["counters"]
+    assert np.array_equal(a["exits"], b["exits"])
+    assert np.allclose(a["len"], b["len"], rtol=1e-11, atol=0)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5m"])
+def test_rect_tracker_rejects_hex(nt, cfg):
+    spec, _ = workloads.config(cfg)
+    m = nt.Model.from_spec(spec, device=0)
+    with pytest.raises(nt.NtError) as e:
+        m.track(10, seed=1, tracker="rect")
+    assert e.value.status == -5
