@@ -36,6 +36,7 @@ def _args():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--particles", type=float, default=None, help="histories per GPU per step")
     ap.add_argument("--tracker", default="generic", choices=["generic", "rect"])
+    ap.add_argument("--scheduler", default="event", choices=["event", "history"])
     ap.add_argument("--pseudo-array", action="store_true")
     ap.add_argument("--block-dim", type=int, default=0)
     ap.add_argument("--blocks-per-sm", type=int, default=0)
@@ -192,7 +193,8 @@ def main():
     out = torch.zeros(model.out_len, dtype=torch.float64, device="cuda")
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
     seed0 = workloads.SEED
-    kw = dict(tracker=a.tracker, block_dim=a.block_dim, blocks_per_sm=a.blocks_per_sm)
+    kw = dict(tracker=a.tracker, block_dim=a.block_dim, blocks_per_sm=a.blocks_per_sm,
+              scheduler=a.scheduler if a.tracker == "generic" else "history")
 
     outs = [torch.zeros(model.out_len, dtype=torch.float64, device="cuda") for _ in range(a.steps)]
 
@@ -288,6 +290,7 @@ def main():
                 "data": "synthetic (histories born from Philox(seed, pid) on the device)",
                 "config": {"workload": spec["name"], "histories_per_gpu_per_step": n,
                            "tracker": a.tracker, "pseudo_array": bool(a.pseudo_array),
+                           "scheduler": kw["scheduler"],
                            "parallelism": f"pid-sharded x{world}, one fp64 all-reduce per step",
                            "l2": "256 MB buffer written between timed steps (L2 flushed)"},
                 "particles_per_s": particles / t_max,

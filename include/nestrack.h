@@ -72,6 +72,10 @@ typedef enum { NT_TRACKER_GENERIC = 0, NT_TRACKER_RECT = 1 } nt_tracker;
 
 /* nt_run.flags */
 #define NT_TRACE 1u          /* write one nt_trace_rec per segment into outputs.trace */
+#define NT_HISTORY 2u        /* scheduler: history-based persistent kernel (one history per thread)
+                              * instead of the default event-based kernel with block-local event
+                              * queues (§2.3 event-based execution).  Results are
+                              * identical; only speed differs.  NT_TRACKER_RECT is history-based. */
 
 /* Per-particle flag bits written to outputs.pflags (reading O16):
  *   F1: a cell/tile chosen by a descent has another surface within 1e-10 cm
@@ -204,7 +208,7 @@ typedef struct {
     uint64_t max_segments;    /* per history; 0 = 1e6; reaching it -> CAPPED                  */
     int32_t tracker;          /* nt_tracker                                                   */
     uint32_t flags;           /* NT_TRACE                                                     */
-    int32_t block_dim;        /* 0 = auto (tuning knob)                                       */
+    int32_t block_dim;        /* 0 = auto (256); event scheduler: 128 or 256 (tuning knob)    */
     int32_t blocks_per_sm;    /* 0 = auto (tuning knob)                                       */
 } nt_run;
 

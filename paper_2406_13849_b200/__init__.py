@@ -19,6 +19,8 @@ KIND = {"PX": 0, "PY": 1, "PZ": 2, "PLANE": 3, "CZ": 4, "SPHERE": 5}
 BC = {"none": 0, "vacuum": 1, "reflect": 2}
 TRACKER = {"generic": 0, "rect": 1}
 NT_TRACE = 1
+NT_HISTORY = 2
+SCHEDULERS = ("event", "history")
 COUNTERS = ["particles", "segments", "crossings", "reflections", "leaks", "collisions",
             "absorptions", "lost", "capped", "flagged"] + [f"cross_l{i}" for i in range(8)]
 NC = len(COUNTERS)
@@ -239,7 +241,7 @@ class Model:
     # ---------------------------------------------------------------- tracking
     def make_run(self, n: int, seed: int, pid_begin: int = 0, lo=None, hi=None, max_segments: int = 0,
                  tracker: str = "generic", trace: bool = False, block_dim: int = 0,
-                 blocks_per_sm: int = 0) -> Run:
+                 blocks_per_sm: int = 0, scheduler: str = "event") -> Run:
         r = Run()
         r.seed, r.pid_begin, r.n = seed, pid_begin, n
         src = (self.spec or {}).get("source", {"lo": [0, 0, 0], "hi": [0, 0, 0]})
@@ -249,14 +251,15 @@ class Model:
             r.src_lo[a], r.src_hi[a] = lo[a], hi[a]
         r.max_segments = max_segments
         r.tracker = TRACKER[tracker]
-        r.flags = NT_TRACE if trace else 0
+        assert scheduler in SCHEDULERS
+        r.flags = (NT_TRACE if trace else 0) | (NT_HISTORY if scheduler == "history" else 0)
         r.block_dim, r.blocks_per_sm = block_dim, blocks_per_sm
         return r
 
     def track(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
               max_segments: int = 0, tracker: str = "generic", pflags: bool = False,
               trace_cap: int = 0, states=None, out=None, stream=None, block_dim: int = 0,
-              blocks_per_sm: int = 0, per_history: bool = False):
+              blocks_per_sm: int = 0, per_history: bool = False, scheduler: str = "event"):
         """Track histories [pid_begin, pid_begin+n) on this model's GPU (async on `stream`).
         Returns a dict of device tensors: out (accumulated), pflags, trace, trace_count."""
         import torch
@@ -281,7 +284,7 @@ class Model:
             o.trace, o.trace_cap, o.trace_count = tr.data_ptr(), trace_cap, tc.data_ptr()
             res["trace"], res["trace_count"] = tr, tc
         run = self.make_run(n, seed, pid_begin, lo, hi, max_segments, tracker, bool(trace_cap),
-                            block_dim, blocks_per_sm)
+                            block_dim, blocks_per_sm, scheduler)
         sh = _stream_handle(stream)
         if states is not None:
             assert states.dtype == torch.float64 and states.is_cuda and tuple(states.shape) == (6, n)
@@ -295,12 +298,13 @@ class Model:
 
     def track_host(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
                    max_segments: int = 0, tracker: str = "generic", out: np.ndarray | None = None,
-                   stream=None, block_dim: int = 0, blocks_per_sm: int = 0) -> np.ndarray:
+                   stream=None, block_dim: int = 0, blocks_per_sm: int = 0,
+                   scheduler: str = "event") -> np.ndarray:
         """End-to-end call with a HOST output buffer (synchronous)."""
         if out is None:
             out = np.zeros(self.out_len)
         run = self.make_run(n, seed, pid_begin, lo, hi, max_segments, tracker, False, block_dim,
-                            blocks_per_sm)
+                            blocks_per_sm, scheduler)
         _check(self.L.nt_track_host(self.h, C.byref(run), _p(out), _stream_handle(stream)))
         return out
 

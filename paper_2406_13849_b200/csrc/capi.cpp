@@ -367,6 +367,9 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   if (run->max_segments > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": max_segments >= 2^32");
   const int block = run->block_dim > 0 ? run->block_dim : 256;
   if (block % 32 || block > 256) return err(NT_E_ARG, std::string(who) + ": block_dim must be a multiple of 32, <= 256");
+  if (run->tracker == NT_TRACKER_GENERIC && !(run->flags & NT_HISTORY) && block != 128 && block != 256)
+    return err(NT_E_ARG, std::string(who) + ": the event scheduler needs block_dim 128 or 256");
+  if (run->n > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": at most 2^32-1 histories per call");
   m->last_launches = 0;
   if (run->n == 0) return NT_OK;
   int prev = 0;
@@ -394,8 +397,10 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   if (e == cudaSuccess) {
     if (run->tracker == NT_TRACKER_RECT)
       e = launch_rect(m->g, m->rg, R, trace, d_states != nullptr, block, run->blocks_per_sm, s, &grid);
-    else
+    else if (run->flags & NT_HISTORY)
       e = launch_generic(m->g, R, trace, d_states != nullptr, block, run->blocks_per_sm, s, &grid);
+    else
+      e = launch_event(m->g, R, trace, d_states != nullptr, block, run->blocks_per_sm, s, &grid);
   }
   if (prev != m->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_err(e, who);

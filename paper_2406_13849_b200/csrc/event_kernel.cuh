@@ -1,0 +1,405 @@
+// Event-based generic tracker: block-local event queues (§2.3, re-designed
+// for sm_100a).
+//
+// Shift's GPU transport runs every tracking operation as a kernel over a masked vector of
+// histories.  Here one persistent block owns B particle slots (state in shared memory, SoA) and
+// runs three stages per round, each over a COMPACTED queue of the slots that need that event:
+//
+//   DESCEND  : find_cell / cross_surface descents (Alg. 7-8), queue sorted by universe kind of the
+//              crossing level (CSG first, then arrays), plus births into free slots (pid claims
+//              with a warp-aggregated atomic on the global counter);
+//   MOVE     : distance_to_boundary over all levels + collide-or-cross + move_within_cell +
+//              track-length tally (Table 1, Alg. 2); each slot is appended to the queue
+//              of its next event with a ballot / popc / one shared atomic per warp;
+//   COLLIDE  : change_direction: absorption or isotropic scatter.
+//
+// Every warp therefore executes one event type on 32 slots at a time instead of a mix of
+// divergent branches.  The per-level universe stack of each slot stays in shared memory between
+// stages; nothing round-trips through HBM.  Arithmetic is exactly the generic tracker's
+// (nt_geom.cuh, descend(), level_distances()), so results are bit-identical to it and to the oracle.
+#pragma once
+
+namespace nt {
+
+// Queue layout (uint16 slot indices), double-buffered by round parity p:
+//   Q_M[p] move-ready, Q_C[p] collide, Q_DC[p] CSG descents, Q_DA[p] array descents, Q_F[p] free
+enum { Q_M = 0, Q_C = 1, Q_DC = 2, Q_DA = 3, Q_F = 4, NQ = 5 };
+
+__device__ __forceinline__ int warp_append(bool pred, int* counter, int lane) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (m == 0) return -1;
+  const int leader = __ffs(m) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(counter, __popc(m));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  return pred ? base + __popc(m & ((1u << lane) - 1u)) : -1;
+}
+
+__device__ __forceinline__ void warp_count(bool pred, unsigned int* counter, int lane) {
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (lane == 0 && m) atomicAdd(counter, (unsigned)__popc(m));
+}
+
+size_t event_smem_bytes(const DevGeom& g, int B, bool trace) {
+  const size_t nmc = g.n_mc, d = g.max_depth;
+  size_t s = 0;
+  s += (7 + 3 * d + (trace ? 1 : 0)) * 8 * (size_t)B;                 // doubles
+  s += (6 + 4 * d + (trace ? 2 : 0)) * 4 * (size_t)B;                 // ints
+  s += (3 + (trace ? 1 : 0)) * (size_t)B;                             // bytes
+  s = (s + 15) & ~size_t(15);
+  s += 2 * NQ * 2 * (size_t)B;                                         // queues (uint16)
+  s += (nmc + kNC + 2 * NQ + 4) * 4;                                    // exits, counters, queue counts
+  return (s + 15) & ~size_t(15);
+}
+
+template <int B, bool TRACE, bool STATES>
+__global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int nmc = g.n_mc, maxd = g.max_depth;
+  // ---- carve shared memory (see event_smem_bytes)
+  double* sx = reinterpret_cast<double*>(smem);
+  double* sy = sx + B; double* sz = sy + B; double* su = sz + B; double* sv = su + B; double* sw = sv + B;
+  double* stau = sw + B;
+  double* sTb = stau + B;                           // [maxd][3][B]
+  double* sps = sTb + 3 * maxd * B;                 // TRACE: pending segment length
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(sps + (TRACE ? B : 0));
+  uint32_t* sepoch = sidx + B; uint32_t* snseg = sepoch + B;
+  int32_t* smc = reinterpret_cast<int32_t*>(snseg + B);
+  int32_t* sos = smc + B;                           // on-surface sid (-1 none)
+  int32_t* sdesc = sos + B;                         // pending descent: l0 | fsense<<4 | (fsid+1)<<5
+  int32_t* sib = sdesc + B;                         // [maxd][4][B]
+  int32_t* spj = sib + 4 * maxd * B;                // TRACE: pending j, cell_before
+  int32_t* spcb = spj + (TRACE ? B : 0);
+  uint8_t* sflags = reinterpret_cast<uint8_t*>(spcb + (TRACE ? B : 0));
+  uint8_t* sL = sflags + B;
+  int8_t* sosl = reinterpret_cast<int8_t*>(sL + B);
+  int8_t* spl = sosl + B;                           // TRACE: pending level
+  size_t off = (size_t)(reinterpret_cast<unsigned char*>(spl + (TRACE ? B : 0)) - smem);
+  off = (off + 15) & ~size_t(15);
+  uint16_t* sq = reinterpret_cast<uint16_t*>(smem + off);   // [2][NQ][B]
+  unsigned int* s_exit = reinterpret_cast<unsigned int*>(sq + 2 * NQ * B);
+  unsigned int* s_cnt = s_exit + nmc;
+  int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [2][NQ]
+  int* s_flag = s_qn + 2 * NQ;                              // [0] = pids exhausted
+  double* gl = R.slices + (size_t)blockIdx.x * nmc;         // per-block track-length tally (global)
+
+  for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
+  for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
+  if (tid < 2 * NQ) s_qn[tid] = 0;
+  if (tid == 0) { s_flag[0] = 0; s_qn[1 * NQ + Q_F] = B; }
+  for (int i = tid; i < B; i += B) sq[(1 * NQ + Q_F) * B + i] = static_cast<uint16_t>(i);   // all slots free
+  __syncthreads();
+
+  auto Q = [&](int p, int q) { return sq + (p * NQ + q) * B; };
+  auto QN = [&](int p, int q) -> int& { return s_qn[p * NQ + q]; };
+  const uint32_t max_seg = static_cast<uint32_t>(R.max_seg);
+
+  // history ended: per-history counters and per-particle outputs (slot becomes free)
+  auto finalize = [&](int slot, int term) {
+    atomicAdd(s_cnt + C_PART, 1u);
+    atomicAdd(s_cnt + (term == NT_T_ABSORBED ? C_ABS : term == NT_T_LEAKED ? C_LEAK : term == NT_T_LOST ? C_LOST : C_CAP), 1u);
+    const uint32_t fl = sflags[slot];
+    if (fl) atomicAdd(s_cnt + C_FLAG, 1u);
+    const uint32_t id = sidx[slot];
+    if (R.pflags) R.pflags[id] = static_cast<uint8_t>(fl);
+    if (R.pnseg) R.pnseg[id] = snseg[slot];
+    if (R.pterm) R.pterm[id] = static_cast<uint8_t>(term);
+    atomicAdd(s_cnt + C_SEG, snseg[slot]);
+  };
+
+  for (int round = 0;; ++round) {
+    const int p = round & 1, q = p ^ 1;
+    // ================= DESCEND (+ births) =================
+    {
+      // C[p] was consumed by COLLIDE(r-2); M[q] by MOVE(r-1): both are refilled from MOVE(r) on
+      if (tid == 0) { QN(p, Q_C) = 0; QN(q, Q_M) = 0; }
+      const int ndc = QN(q, Q_DC), nda = QN(q, Q_DA), nfr = QN(q, Q_F);
+      const int total = ndc + nda + nfr;
+      for (int base = warp * 32; base < total; base += B) {
+        const int i = base + lane;
+        const bool valid = i < total;
+        int slot = 0, kind = 3;                           // 0 CSG descent, 1 array descent, 2 birth
+        if (valid) {
+          if (i < ndc) { slot = Q(q, Q_DC)[i]; kind = 0; }
+          else if (i < ndc + nda) { slot = Q(q, Q_DA)[i - ndc]; kind = 1; }
+          else { slot = Q(q, Q_F)[i - ndc - nda]; kind = 2; }
+        }
+        // births: claim pids for this warp's birth lanes (warp-aggregated)
+        const unsigned bm = __ballot_sync(0xffffffffu, kind == 2);
+        bool born = false;
+        if (bm) {
+          const int leader = __ffs(bm) - 1;
+          unsigned long long b0 = 0;
+          if (lane == leader) b0 = atomicAdd(R.counter, static_cast<unsigned long long>(__popc(bm)));
+          b0 = __shfl_sync(0xffffffffu, b0, leader);
+          if (kind == 2) {
+            const unsigned long long id = b0 + __popc(bm & ((1u << lane) - 1u));
+            if (id < R.n) { born = true; sidx[slot] = static_cast<uint32_t>(id); }
+            else s_flag[0] = 1;                          // pids exhausted: slot stays unused
+          }
+        }
+        bool ok = false, done = false;
+        Stack st;
+        st.si = sib + slot;
+        st.sT = sTb + slot;
+        st.B = B;
+        double rx = 0, ry = 0, rz = 0;
+        uint32_t flags = 0;
+        int L = 0, mc = 0;
+        if (kind == 0 || kind == 1 || born) {
+          int l0 = 0, du = g.root, fsid = -1, fsense = 0;
+          double Tx = 0.0, Ty = 0.0, Tz = 0.0;
+          if (born) {
+            const uint64_t pid = R.pid0 + sidx[slot];
+            double xa, xb;
+            draw2(R.seed, pid, 0, 0, xa, xb);
+            double u, v, w;
+            if (STATES) {
+              const uint64_t id = sidx[slot];
+              rx = R.states[id]; ry = R.states[R.n + id]; rz = R.states[2 * R.n + id];
+              u = R.states[3 * R.n + id]; v = R.states[4 * R.n + id]; w = R.states[5 * R.n + id];
+            } else {
+              double xmu, xphi, xx, xy, xz, unused;
+              draw2(R.seed, pid, 0, 1, xmu, xphi);
+              draw2(R.seed, pid, 0, 2, xx, xy);
+              draw2(R.seed, pid, 0, 3, xz, unused);
+              rx = R.lo[0] + R.w[0] * xx;
+              ry = R.lo[1] + R.w[1] * xy;
+              rz = R.lo[2] + R.w[2] * xz;
+              isotropic(xmu, xphi, u, v, w);
+            }
+            sx[slot] = rx; sy[slot] = ry; sz[slot] = rz;
+            su[slot] = u; sv[slot] = v; sw[slot] = w;
+            stau[slot] = -spec_log(xb);
+            sepoch[slot] = 0; snseg[slot] = 0; sos[slot] = -1; sosl[slot] = -1;
+            if (TRACE) spl[slot] = -2;
+          } else {
+            rx = sx[slot]; ry = sy[slot]; rz = sz[slot];
+            flags = sflags[slot];
+            const int dsc = sdesc[slot];
+            l0 = dsc & 15;
+            fsense = (dsc >> 4) & 1;
+            fsid = (dsc >> 5) - 1;
+            if (kind == 0) {
+              du = st.u(l0);
+              Tx = st.T(l0, 0); Ty = st.T(l0, 1); Tz = st.T(l0, 2);
+            } else {                                     // Alg. 6: tile +- 1 at level l0, then daughter
+              const int j = fsid;
+              const DUniv* U = g.univ + st.u(l0);
+              const int uk = ld(&U->kind);
+              int ta = st.a(l0), tb = st.b(l0), tc = st.c(l0);
+              if (uk == U_RECT) {
+                const int dir = (j & 1) ? 1 : -1, ax = j >> 1;
+                if (ax == 0) ta += dir; else if (ax == 1) tb += dir; else tc += dir;
+              } else if (j < 6) {
+                ta += (j == 0 || j == 5) ? 1 : ((j == 2 || j == 3) ? -1 : 0);
+                tb += (j == 1 || j == 2) ? 1 : ((j == 4 || j == 5) ? -1 : 0);
+              } else {
+                tc += (j == 7) ? 1 : -1;
+              }
+              st.a(l0) = ta; st.b(l0) = tb; st.c(l0) = tc;
+              double tx, ty, tz;
+              du = array_daughter(g, U, uk, ta, tb, tc, tx, ty, tz);
+              Tx = st.T(l0, 0) + tx; Ty = st.T(l0, 1) + ty; Tz = st.T(l0, 2) + tz;
+              l0 = l0 + 1;
+              fsid = -1;
+              fsense = 0;
+            }
+          }
+          ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
+          done = true;
+        }
+        if (done) {
+          if (!ok) flags |= NT_F3;
+          sflags[slot] = static_cast<uint8_t>(flags);
+          if (ok) { sL[slot] = static_cast<uint8_t>(L); smc[slot] = mc; }
+          if (TRACE) {
+            const uint64_t pid = R.pid0 + sidx[slot];
+            const int pl = spl[slot];
+            if (pl == -2) {
+              if (!ok) emit<TRACE>(R, pid, 0, NT_EV_CROSS, -1, -1, -1, -1, 0.0, NT_T_LOST, flags);
+            } else {
+              emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_CROSS, pl, spj[slot], spcb[slot],
+                          ok ? ld(g.mc_cell + mc) : -1, sps[slot], ok ? NT_T_NONE : NT_T_LOST, flags);
+            }
+          }
+          if (!ok) finalize(slot, NT_T_LOST);
+        }
+        const int pm = warp_append(done && ok, &QN(p, Q_M), lane);
+        if (pm >= 0) Q(p, Q_M)[pm] = static_cast<uint16_t>(slot);
+        const int pf = warp_append(done && !ok, &QN(p, Q_F), lane);
+        if (pf >= 0) Q(p, Q_F)[pf] = static_cast<uint16_t>(slot);
+      }
+    }
+    __syncthreads();
+    // termination: every live history is in M[p] at this point; none left and no more pids
+    if (QN(p, Q_M) == 0 && s_flag[0]) break;
+    // ================= MOVE =================
+    {
+      // DC/DA/F[q] were consumed by DESCEND(r); they are refilled from MOVE(r+1) / round r+1 on
+      if (tid == 0) { QN(q, Q_DC) = 0; QN(q, Q_DA) = 0; QN(q, Q_F) = 0; }
+      const int total = QN(p, Q_M);
+      for (int base = warp * 32; base < total; base += B) {
+        const int i = base + lane;
+        const bool valid = i < total;
+        const int slot = valid ? Q(p, Q_M)[i] : 0;
+        // outcome: 0 none, 1 reflect (-> M), 2 collide, 3 CSG descent, 4 array descent, 5 ended
+        int outc = 0, term = NT_T_NONE, lcross = -1;
+        bool seg = false;
+        if (valid) {
+          Stack st;
+          st.si = sib + slot;
+          st.sT = sTb + slot;
+          st.B = B;
+          double rx = sx[slot], ry = sy[slot], rz = sz[slot];
+          double u = su[slot], v = sv[slot], w = sw[slot];
+          double tau = stau[slot];
+          uint32_t flags = sflags[slot], nseg = snseg[slot];
+          const int L = sL[slot], mc = smc[slot];
+          int os_l = sosl[slot], os_s = sos[slot];
+          if (nseg >= max_seg) {
+            flags |= NT_F3;
+            term = NT_T_CAPPED;
+            outc = 5;
+            emit<TRACE>(R, R.pid0 + sidx[slot], nseg, NT_EV_COLLIDE, -1, -1, ld(g.mc_cell + mc), -1, 0.0,
+                        NT_T_CAPPED, flags);
+          } else {
+            Best b;
+            b.d = NT_INF; b.d2 = NT_INF; b.l = -1; b.j = -1; b.sense = 0;
+            for (int l = 0; l < L; ++l) level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+            const double sig = ld(g.mc_st + mc);
+            const double ds = b.d;
+            const double dc = sig > 0.0 ? tau / sig : NT_INF;
+            const double g2 = b.d2 - ds, gc = fabs(dc - ds);
+            if ((g2 > 0.0 && g2 <= kFlagDist) || (gc > 0.0 && gc <= kFlagDist)) flags |= NT_F2;
+            const int cell_before = TRACE ? ld(g.mc_cell + mc) : 0;
+            if (ds == NT_INF && dc == NT_INF) {
+              flags |= NT_F3;
+              term = NT_T_LOST;
+              outc = 5;
+              emit<TRACE>(R, R.pid0 + sidx[slot], nseg, NT_EV_CROSS, -1, -1, cell_before, -1, 0.0, NT_T_LOST, flags);
+            } else {
+              const bool cross = ds < dc;
+              const double s = cross ? ds : dc;
+              atomicAdd(gl + mc, s);
+              rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
+              ++nseg;
+              seg = true;
+              if (TRACE) { sps[slot] = s; spcb[slot] = cell_before; }
+              if (cross) {
+                const double tt = tau - sig * s;
+                tau = tt > 0.0 ? tt : 0.0;
+                const int l = b.l, j = b.j;
+                const int meta = (l == 0 && g.root_kind == U_CSG) ? ld(g.surf_meta + j) : 0;
+                const int bc = meta >> 4;
+                if (bc == NT_BC_VACUUM) {
+                  atomicAdd(s_exit + mc, 1u);
+                  term = NT_T_LEAKED;
+                  outc = 5;
+                  lcross = -2;
+                  emit<TRACE>(R, R.pid0 + sidx[slot], nseg - 1, NT_EV_LEAK, 0, j, cell_before, -1, s, NT_T_LEAKED, flags);
+                } else if (bc == NT_BC_REFLECT) {
+                  const int ax = meta & 15;
+                  if (ax == 0) u = -u; else if (ax == 1) v = -v; else w = -w;
+                  os_l = 0; os_s = j;
+                  outc = 1;
+                  emit<TRACE>(R, R.pid0 + sidx[slot], nseg - 1, NT_EV_REFLECT, 0, j, cell_before, cell_before, s,
+                              NT_T_NONE, flags);
+                } else {
+                  atomicAdd(s_exit + mc, 1u);
+                  lcross = l;
+                  const int uk = ld(&g.univ[st.u(l)].kind);
+                  if (uk == U_CSG) {
+                    sdesc[slot] = l | ((b.sense ^ 1) << 4) | ((j + 1) << 5);
+                    os_l = l; os_s = j;
+                    outc = 3;
+                  } else {
+                    sdesc[slot] = l | ((j + 1) << 5);
+                    os_l = -1; os_s = -1;
+                    outc = 4;
+                  }
+                  if (TRACE) { spl[slot] = static_cast<int8_t>(l); spj[slot] = j; }
+                }
+              } else {
+                os_l = -1; os_s = -1;
+                outc = 2;
+              }
+            }
+          }
+          sx[slot] = rx; sy[slot] = ry; sz[slot] = rz;
+          su[slot] = u; sv[slot] = v; sw[slot] = w;
+          stau[slot] = tau;
+          sflags[slot] = static_cast<uint8_t>(flags);
+          snseg[slot] = nseg;
+          sosl[slot] = static_cast<int8_t>(os_l);
+          sos[slot] = os_s;
+          if (outc == 5) finalize(slot, term);
+        }
+        // per-event counters (one shared atomic per warp and counter)
+        warp_count(seg && (outc == 3 || outc == 4 || lcross == -2), s_cnt + C_CROSS, lane);
+        warp_count(outc == 1, s_cnt + C_REFL, lane);
+        warp_count(outc == 2, s_cnt + C_COLL, lane);
+        if (__any_sync(0xffffffffu, lcross >= 0))
+          for (int lv = 0; lv < maxd; ++lv) warp_count(lcross == lv, s_cnt + C_CBL0 + lv, lane);
+        // enqueue for the next event
+        int pos;
+        pos = warp_append(outc == 1, &QN(q, Q_M), lane);
+        if (pos >= 0) Q(q, Q_M)[pos] = static_cast<uint16_t>(slot);
+        pos = warp_append(outc == 2, &QN(p, Q_C), lane);
+        if (pos >= 0) Q(p, Q_C)[pos] = static_cast<uint16_t>(slot);
+        pos = warp_append(outc == 3, &QN(p, Q_DC), lane);
+        if (pos >= 0) Q(p, Q_DC)[pos] = static_cast<uint16_t>(slot);
+        pos = warp_append(outc == 4, &QN(p, Q_DA), lane);
+        if (pos >= 0) Q(p, Q_DA)[pos] = static_cast<uint16_t>(slot);
+        pos = warp_append(outc == 5, &QN(p, Q_F), lane);
+        if (pos >= 0) Q(p, Q_F)[pos] = static_cast<uint16_t>(slot);
+      }
+    }
+    __syncthreads();
+    // ================= COLLIDE =================
+    {
+      const int total = QN(p, Q_C);
+      for (int base = warp * 32; base < total; base += B) {
+        const int i = base + lane;
+        const bool valid = i < total;
+        const int slot = valid ? Q(p, Q_C)[i] : 0;
+        bool scat = false, absorbed = false;
+        if (valid) {
+          const uint64_t pid = R.pid0 + sidx[slot];
+          const uint32_t epoch = sepoch[slot] + 1;
+          sepoch[slot] = epoch;
+          const int mc = smc[slot];
+          double xa, xb;
+          draw2(R.seed, pid, epoch, 0, xa, xb);
+          const int cb = TRACE ? ld(g.mc_cell + mc) : 0;
+          if (xa < ld(g.mc_pabs + mc)) {
+            absorbed = true;
+            emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_ABSORBED,
+                        sflags[slot]);
+            finalize(slot, NT_T_ABSORBED);
+          } else {
+            double xmu, xphi, u, v, w;
+            draw2(R.seed, pid, epoch, 1, xmu, xphi);
+            isotropic(xmu, xphi, u, v, w);
+            su[slot] = u; sv[slot] = v; sw[slot] = w;
+            stau[slot] = -spec_log(xb);
+            scat = true;
+            emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_NONE, sflags[slot]);
+          }
+        }
+        int pos = warp_append(scat, &QN(q, Q_M), lane);
+        if (pos >= 0) Q(q, Q_M)[pos] = static_cast<uint16_t>(slot);
+        pos = warp_append(absorbed, &QN(p, Q_F), lane);
+        if (pos >= 0) Q(p, Q_F)[pos] = static_cast<uint16_t>(slot);
+      }
+    }
+    __syncthreads();
+  }
+
+  // ---- flush block tallies: exits / counters from shared memory, lengths from the block slice
+  __syncthreads();
+  flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
+}
+
+}  // namespace nt

@@ -21,6 +21,7 @@ struct KRun {
   uint64_t trace_cap;
   unsigned long long* trace_count;
   unsigned long long* counter;      // work counter (pid claims), zeroed before launch
+  double* slices;                   // [grid][n_mc] zeroed per-block track-length tallies (global)
 };
 
 cudaError_t upload_coefficients(const double* host, int n);
@@ -28,6 +29,8 @@ cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool sta
                            int blocks_per_sm, cudaStream_t stream, int* grid_out);
 cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states,
                         int block, int blocks_per_sm, cudaStream_t stream, int* grid_out);
+cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
+                         int blocks_per_sm, cudaStream_t stream, int* grid_out);
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,
                               uint8_t* flag, cudaStream_t stream);
 

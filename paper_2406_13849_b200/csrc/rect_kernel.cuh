@@ -13,11 +13,11 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
   const int nmc = g.n_mc;
-  double* s_len = reinterpret_cast<double*>(smem);
-  unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(s_len + nmc);
-  unsigned int* s_exit = reinterpret_cast<unsigned int*>(s_cnt + kNC);
-  for (int i = tid; i < nmc; i += B) { s_len[i] = 0.0; s_exit[i] = 0u; }
-  for (int i = tid; i < kNC; i += B) s_cnt[i] = 0ull;
+  unsigned int* s_cnt = reinterpret_cast<unsigned int*>(smem);
+  unsigned int* s_exit = s_cnt + kNC;
+  double* gl = R.slices + (size_t)blockIdx.x * nmc;   // per-block track-length tally (global)
+  for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
+  for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
   __syncthreads();
 
   constexpr int KP = K + 1;          // pin level
@@ -272,7 +272,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
           emit<TRACE>(R, pid, nseg, NT_EV_CROSS, -1, -1, cell_before, -1, 0.0, NT_T_LOST, flags);
         } else if (ds < dc) {
           const double s = ds;
-          atomicAdd(s_len + mc, s);
+          atomicAdd(gl + mc, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
           } else {
             atomicAdd(s_exit + mc, 1u);
             ++ncross;
-            atomicAdd(s_cnt + C_CBL0 + l, 1ull);
+            atomicAdd(s_cnt + C_CBL0 + l, 1u);
             p_l = l; p_j = j; p_cb = cell_before; p_s = s;
             phase = 1;
             if (l == 0 || l == KP) {            // CSG level: far side of surface j (Alg. 10)
@@ -325,7 +325,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
           }
         } else {
           const double s = dc;
-          atomicAdd(s_len + mc, s);
+          atomicAdd(gl + mc, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           ++nseg;
           ++ncoll;
@@ -349,26 +349,21 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
       if (term == NT_T_NONE) continue;
     }
     phase = 0;
-    atomicAdd(s_cnt + C_PART, 1ull);
-    atomicAdd(s_cnt + C_SEG, static_cast<unsigned long long>(nseg));
-    atomicAdd(s_cnt + C_CROSS, static_cast<unsigned long long>(ncross));
-    atomicAdd(s_cnt + C_COLL, static_cast<unsigned long long>(ncoll));
-    atomicAdd(s_cnt + C_REFL, static_cast<unsigned long long>(nseg - ncross - ncoll));
+    atomicAdd(s_cnt + C_PART, 1u);
+    atomicAdd(s_cnt + C_SEG, nseg);
+    atomicAdd(s_cnt + C_CROSS, ncross);
+    atomicAdd(s_cnt + C_COLL, ncoll);
+    atomicAdd(s_cnt + C_REFL, nseg - ncross - ncoll);
     const int tcn = term == NT_T_ABSORBED ? C_ABS : term == NT_T_LEAKED ? C_LEAK : term == NT_T_LOST ? C_LOST : C_CAP;
-    atomicAdd(s_cnt + tcn, 1ull);
-    if (flags) atomicAdd(s_cnt + C_FLAG, 1ull);
+    atomicAdd(s_cnt + tcn, 1u);
+    if (flags) atomicAdd(s_cnt + C_FLAG, 1u);
     if (R.pflags) R.pflags[idx] = static_cast<uint8_t>(flags);
     if (R.pnseg) R.pnseg[idx] = nseg;
     if (R.pterm) R.pterm[idx] = static_cast<uint8_t>(term);
   }
 
   __syncthreads();
-  for (int i = tid; i < nmc; i += B) {
-    if (s_len[i] != 0.0) atomicAdd(R.out + i, s_len[i]);
-    if (s_exit[i]) atomicAdd(R.out + nmc + i, static_cast<double>(s_exit[i]));
-  }
-  for (int i = tid; i < kNC; i += B)
-    if (s_cnt[i]) atomicAdd(R.out + 2 * nmc + i, static_cast<double>(s_cnt[i]));
+  flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
 }
 
 }  // namespace nt

@@ -161,6 +161,18 @@ __device__ __forceinline__ void emit(const KRun& R, uint64_t pid, uint32_t seg, 
   R.trace[slot] = t;
 }
 
+// block tallies -> caller's packed output; the per-block length slice is re-zeroed for reuse
+__device__ __forceinline__ void flush_tallies(const KRun& R, double* gl, const unsigned int* s_exit,
+                                              const unsigned int* s_cnt, int nmc, int tid, int B) {
+  for (int i = tid; i < nmc; i += B) {
+    const double len = gl[i];
+    if (len != 0.0) { atomicAdd(R.out + i, len); gl[i] = 0.0; }
+    if (s_exit[i]) atomicAdd(R.out + nmc + i, static_cast<double>(s_exit[i]));
+  }
+  for (int i = tid; i < kNC; i += B)
+    if (s_cnt[i]) atomicAdd(R.out + 2 * nmc + i, static_cast<double>(s_cnt[i]));
+}
+
 enum { C_PART = 0, C_SEG, C_CROSS, C_REFL, C_LEAK, C_COLL, C_ABS, C_LOST, C_CAP, C_FLAG, C_CBL0 };
 
 template <bool TRACE, bool STATES>
@@ -168,16 +180,16 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
   const int nmc = g.n_mc;
-  double* s_len = reinterpret_cast<double*>(smem);
-  unsigned long long* s_cnt = reinterpret_cast<unsigned long long*>(s_len + nmc);
-  unsigned int* s_exit = reinterpret_cast<unsigned int*>(s_cnt + kNC);
-  double* sT = reinterpret_cast<double*>(s_exit + ((nmc + 1) & ~1));
+  double* sT = reinterpret_cast<double*>(smem);
+  unsigned int* s_cnt = reinterpret_cast<unsigned int*>(sT + 3 * g.max_depth * B + 4 * g.max_depth * B / 2);
+  unsigned int* s_exit = s_cnt + kNC;
+  double* gl = R.slices + (size_t)blockIdx.x * nmc;   // per-block track-length tally (global)
   Stack st;
   st.sT = sT + tid;
   st.si = reinterpret_cast<int*>(sT + 3 * g.max_depth * B) + tid;
   st.B = B;
-  for (int i = tid; i < nmc; i += B) { s_len[i] = 0.0; s_exit[i] = 0u; }
-  for (int i = tid; i < kNC; i += B) s_cnt[i] = 0ull;
+  for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
+  for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
   __syncthreads();
 
   // particle state (registers)
@@ -268,7 +280,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
         } else if (ds < dc) {
           // Alg. 2 "while d < tau/Sigma": tau -= Sigma d, move, cross
           const double s = ds;
-          atomicAdd(s_len + mc, s);
+          atomicAdd(gl + mc, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
@@ -289,7 +301,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           } else {
             atomicAdd(s_exit + mc, 1u);
             ++ncross;
-            atomicAdd(s_cnt + C_CBL0 + l, 1ull);
+            atomicAdd(s_cnt + C_CBL0 + l, 1u);
             const int ul = st.u(l);
             const DUniv* U = g.univ + ul;
             const int kind = ld(&U->kind);
@@ -329,7 +341,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
         } else {
           // ---- collision at tau / Sigma_t: absorb or scatter isotropically (O14, O15)
           const double s = dc;
-          atomicAdd(s_len + mc, s);
+          atomicAdd(gl + mc, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           ++nseg;
           ++ncoll;
@@ -354,29 +366,25 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
     }
     // ---- history ended: per-history counters into the block tallies
     phase = 0;
-    atomicAdd(s_cnt + C_PART, 1ull);
-    atomicAdd(s_cnt + C_SEG, static_cast<unsigned long long>(nseg));
-    atomicAdd(s_cnt + C_CROSS, static_cast<unsigned long long>(ncross));
-    atomicAdd(s_cnt + C_COLL, static_cast<unsigned long long>(ncoll));
-    atomicAdd(s_cnt + C_REFL, static_cast<unsigned long long>(nseg - ncross - ncoll));
+    atomicAdd(s_cnt + C_PART, 1u);
+    atomicAdd(s_cnt + C_SEG, nseg);
+    atomicAdd(s_cnt + C_CROSS, ncross);
+    atomicAdd(s_cnt + C_COLL, ncoll);
+    atomicAdd(s_cnt + C_REFL, nseg - ncross - ncoll);
     const int tcn = term == NT_T_ABSORBED ? C_ABS : term == NT_T_LEAKED ? C_LEAK : term == NT_T_LOST ? C_LOST : C_CAP;
-    atomicAdd(s_cnt + tcn, 1ull);
-    if (flags) atomicAdd(s_cnt + C_FLAG, 1ull);
+    atomicAdd(s_cnt + tcn, 1u);
+    if (flags) atomicAdd(s_cnt + C_FLAG, 1u);
     if (R.pflags) R.pflags[idx] = static_cast<uint8_t>(flags);
     if (R.pnseg) R.pnseg[idx] = nseg;
     if (R.pterm) R.pterm[idx] = static_cast<uint8_t>(term);
   }
 
   __syncthreads();
-  for (int i = tid; i < nmc; i += B) {
-    if (s_len[i] != 0.0) atomicAdd(R.out + i, s_len[i]);
-    if (s_exit[i]) atomicAdd(R.out + nmc + i, static_cast<double>(s_exit[i]));
-  }
-  for (int i = tid; i < kNC; i += B)
-    if (s_cnt[i]) atomicAdd(R.out + 2 * nmc + i, static_cast<double>(s_cnt[i]));
+  flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
 }
 
 }  // namespace nt
+#include "event_kernel.cuh"
 #include "rect_kernel.cuh"
 namespace nt {
 
@@ -400,8 +408,19 @@ __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const doubl
 
 // ---------------------------------------------------------------- host launchers
 size_t generic_smem_bytes(const DevGeom& g, int block) {
-  const size_t nmc = g.n_mc;
-  return nmc * 8 + kNC * 8 + ((nmc + 1) & ~size_t(1)) * 4 + (size_t)g.max_depth * block * (3 * 8 + 4 * 4);
+  return (size_t)g.max_depth * block * (3 * 8 + 4 * 4) + (kNC + (size_t)g.n_mc) * 4;
+}
+
+// per-launch scratch: per-block track-length slices (stream-ordered allocation, zeroed)
+template <class Launch>
+static cudaError_t with_slices(const DevGeom& g, KRun R, uint64_t grid, cudaStream_t stream, Launch launch) {
+  const size_t bytes = (size_t)grid * (size_t)g.n_mc * sizeof(double);
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&R.slices), bytes, stream);
+  if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(R.slices, 0, bytes, stream);
+  if (e == cudaSuccess) e = launch(R);
+  cudaError_t e2 = cudaFreeAsync(R.slices, stream);
+  return e != cudaSuccess ? e : e2;
 }
 
 cudaError_t upload_coefficients(const double* host, int n) {
@@ -425,8 +444,10 @@ cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool sta
     uint64_t grid = (uint64_t)nsm * bps;
     if (need < grid) grid = need ? need : 1;
     *grid_out = (int)grid;
-    kern<<<(unsigned)grid, block, smem, stream>>>(g, R);
-    return cudaGetLastError();
+    return with_slices(g, R, grid, stream, [&](const KRun& Rs) {
+      kern<<<(unsigned)grid, block, smem, stream>>>(g, Rs);
+      return cudaGetLastError();
+    });
   };
   if (trace) return states ? pick(k_track_generic<true, true>) : pick(k_track_generic<true, false>);
   return states ? pick(k_track_generic<false, true>) : pick(k_track_generic<false, false>);
@@ -434,8 +455,7 @@ cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool sta
 
 cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states,
                         int block, int blocks_per_sm, cudaStream_t stream, int* grid_out) {
-  const size_t nmc = g.n_mc;
-  const size_t smem = nmc * 8 + kNC * 8 + ((nmc + 1) & ~size_t(1)) * 4;
+  const size_t smem = (kNC + (size_t)g.n_mc) * 4;
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -449,8 +469,10 @@ cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, boo
     uint64_t need = (R.n + block - 1) / block, grid = (uint64_t)nsm * bps;
     if (need < grid) grid = need ? need : 1;
     *grid_out = (int)grid;
-    kern<<<(unsigned)grid, block, smem, stream>>>(g, rg, R);
-    return cudaGetLastError();
+    return with_slices(g, R, grid, stream, [&](const KRun& Rs) {
+      kern<<<(unsigned)grid, block, smem, stream>>>(g, rg, Rs);
+      return cudaGetLastError();
+    });
   };
   auto pick_k = [&](auto box, auto tr, auto st) -> cudaError_t {
     constexpr bool BOX = decltype(box)::value, TR = decltype(tr)::value, ST = decltype(st)::value;
@@ -471,6 +493,36 @@ cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, boo
   }
   if (trace) return states ? pick_k(F{}, T{}, T{}) : pick_k(F{}, T{}, F{});
   return states ? pick_k(F{}, F{}, T{}) : pick_k(F{}, F{}, F{});
+}
+
+cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
+                         int blocks_per_sm, cudaStream_t stream, int* grid_out) {
+  const size_t smem = event_smem_bytes(g, block, trace);
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    const int bps = blocks_per_sm > 0 ? (blocks_per_sm < occ ? blocks_per_sm : occ) : occ;
+    uint64_t need = (R.n + block - 1) / block, grid = (uint64_t)nsm * bps;
+    if (need < grid) grid = need ? need : 1;
+    *grid_out = (int)grid;
+    return with_slices(g, R, grid, stream, [&](const KRun& Rs) {
+      kern<<<(unsigned)grid, block, smem, stream>>>(g, Rs);
+      return cudaGetLastError();
+    });
+  };
+  if (block == 128) {
+    if (trace) return states ? go(k_track_event<128, true, true>) : go(k_track_event<128, true, false>);
+    return states ? go(k_track_event<128, false, true>) : go(k_track_event<128, false, false>);
+  }
+  if (block != 256) return cudaErrorInvalidValue;
+  if (trace) return states ? go(k_track_event<256, true, true>) : go(k_track_event<256, true, false>);
+  return states ? go(k_track_event<256, false, true>) : go(k_track_event<256, false, false>);
 }
 
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,

@@ -34,13 +34,14 @@ def orc():
 
 
 def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, tracker="generic",
-             trace=True, pseudo=False):
+             trace=True, pseudo=False, scheduler="event", block_dim=0):
     m = nt.Model.from_spec(spec, device=0, pseudo_array=pseudo)
     om = orc.OracleModel.from_spec(spec)
     cap = 400 * max(n, 1) + 64 if trace else 0
     st_t = None if states is None else torch.tensor(states, dtype=torch.float64, device="cuda")
     res = m.track(n, seed=seed, pid_begin=pid_begin, pflags=True, per_history=True, trace_cap=cap,
-                  max_segments=max_segments, states=st_t, tracker=tracker)
+                  max_segments=max_segments, states=st_t, tracker=tracker, scheduler=scheduler,
+                  block_dim=block_dim)
     torch.cuda.synchronize()
     g = m.unpack(res["out"])
     o = om.run(n, seed=seed, pid_begin=pid_begin, pflags=True, trace_cap=cap, max_segments=max_segments,
@@ -67,11 +68,13 @@ def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, t
 CONFIG_N = {"c1": 2000, "c2": 600, "c3": 600, "c4": 600, "c5m": 600, "c5r": 600}
 
 
+@pytest.mark.parametrize("sched", ["event", "history"])
 @pytest.mark.parametrize("cfg", list(CONFIG_N))
-def test_config_trace_parity(nt, orc, cfg):
-    """Every BASELINE config: full traces bit-exact vs the oracle (seeded, small batch)."""
+def test_config_trace_parity(nt, orc, cfg, sched):
+    """Every BASELINE config: full traces bit-exact vs the oracle (seeded, small batch), with
+    both schedulers (event queues / history-based)."""
     spec, _ = workloads.config(cfg)
-    _, g, o, _ = _compare(nt, orc, spec, CONFIG_N[cfg], seed=1)
+    _, g, o, _ = _compare(nt, orc, spec, CONFIG_N[cfg], seed=1, scheduler=sched)
     assert g["counters"]["lost"] == 0 and g["counters"]["capped"] == 0
 
 
@@ -95,29 +98,33 @@ def test_test_models_parity(nt, orc, name):
     _compare(nt, orc, spec, 700, seed=2)
 
 
+@pytest.mark.parametrize("block", [128, 256])
 @pytest.mark.parametrize("n", [1, 31, 257, 1000])
-def test_ragged_batches_and_large_pids(nt, orc, n):
+def test_ragged_batches_and_large_pids(nt, orc, n, block):
     """Ragged batch sizes (partial warps / blocks) and pids above 2^32 (counter hi word)."""
     spec, _ = workloads.config("c2")
-    _compare(nt, orc, spec, n, seed=3, pid_begin=(1 << 33) + 17)
+    _compare(nt, orc, spec, n, seed=3, pid_begin=(1 << 33) + 17, block_dim=block)
 
 
-def test_capped_histories(nt, orc):
+@pytest.mark.parametrize("sched", ["event", "history"])
+def test_capped_histories(nt, orc, sched):
     """max_segments reached -> CAPPED (F3) on both sides, same extra trace record."""
     spec, _ = workloads.config("c1")
-    _, g, o, _ = _compare(nt, orc, spec, 300, seed=4, max_segments=7)
+    _, g, o, _ = _compare(nt, orc, spec, 300, seed=4, max_segments=7, scheduler=sched)
     assert g["counters"]["capped"] > 0
 
 
-def test_lost_at_birth(nt, orc):
+@pytest.mark.parametrize("sched", ["event", "history"])
+def test_lost_at_birth(nt, orc, sched):
     """Births outside every root cell are LOST at birth (source box larger than the model)."""
     spec = workloads.c1_pincell()
     spec["source"] = {"lo": [-1.0, -1.0, 0.0], "hi": [1.0, 1.0, 365.76]}
-    _, g, o, _ = _compare(nt, orc, spec, 500, seed=5)
+    _, g, o, _ = _compare(nt, orc, spec, 500, seed=5, scheduler=sched)
     assert g["counters"]["lost"] > 0
 
 
-def test_explicit_states(nt, orc):
+@pytest.mark.parametrize("sched", ["event", "history"])
+def test_explicit_states(nt, orc, sched):
     """nt_track_states: explicit birth states (chord rays through the void pincell)."""
     spec = workloads.c1_pincell(bc="vacuum", void=True)
     rng = np.random.default_rng(0)
@@ -125,7 +132,7 @@ def test_explicit_states(nt, orc):
     r = rng.uniform([-0.63, -0.63, 0.0], [0.63, 0.63, 365.76], size=(n, 3))
     om = rng.normal(size=(n, 3))
     om /= np.linalg.norm(om, axis=1, keepdims=True)
-    _compare(nt, orc, spec, n, seed=6, states=np.concatenate([r.T, om.T]))
+    _compare(nt, orc, spec, n, seed=6, states=np.concatenate([r.T, om.T]), scheduler=sched)
 
 
 def test_zero_particles(nt):
