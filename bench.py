@@ -36,13 +36,14 @@ def _args():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--particles", type=float, default=None, help="histories per GPU per step")
     ap.add_argument("--tracker", default="generic", choices=["generic", "rect"])
-    ap.add_argument("--scheduler", default="event", choices=["event", "history"])
+    ap.add_argument("--scheduler", default="block", choices=["block", "warp", "history"])
     ap.add_argument("--pseudo-array", action="store_true")
     ap.add_argument("--block-dim", type=int, default=0)
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-ratio", action="store_true", help="skip the rect-tracker comparison run")
     return ap.parse_args()
 
 
@@ -255,6 +256,32 @@ def main():
             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz (DESIGN.md)",
             "falg_flops_per_segment": falg, "kernel_ms_per_launch": 1e3 * kernel_s}
 
+    # the metric's second half: generic tree tracker vs the rect-specialised tracker, same histories
+    ratio = None
+    if not a.no_ratio and a.tracker == "generic" and model.info["rect_specialisable"]:
+        def timed(kk):
+            o2 = torch.zeros_like(out)
+            model.track(n, seed=seed0 + 20_000, pid_begin=rank * n, out=o2, stream=stream, **kk)
+            torch.cuda.synchronize()
+            tt, ss = 0.0, 0
+            for s in range(a.steps):
+                o2.zero_()
+                flush.fill_(s & 0xFF)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                model.track(n, seed=seed0 + s, pid_begin=rank * n, out=o2, stream=stream, **kk)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tt += e0.elapsed_time(e1) / 1e3
+                ss += model.unpack(o2)["counters"]["segments"]
+            return ss / tt, ss
+        rg, sg = timed(kw)
+        rr, sr = timed(dict(kw, tracker="rect", scheduler="history"))
+        ratio = {"generic_over_rect": rg / rr, "generic_segments_per_s": rg, "rect_segments_per_s": rr,
+                 "segments_equal": sg == sr, "generic_scheduler": kw["scheduler"],
+                 "note": "this rank, identical seeds/pids, no all-reduce; rect = Alg. 9-10 specialised "
+                         "tracker (history scheduler); target >= 0.85 (north star)"}
+
     e2e = None
     if not a.no_e2e:
         hout = None
@@ -296,7 +323,7 @@ def main():
                 "particles_per_s": particles / t_max,
                 "segments_per_history": segs / particles,
                 "counters_last_step": res["counters"],
-                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "rect_ratio": ratio,
                 "gpu_launches": launches, "clocks": ck}
         print(json.dumps(line), flush=True)
     if dist is not None:

@@ -72,10 +72,12 @@ typedef enum { NT_TRACKER_GENERIC = 0, NT_TRACKER_RECT = 1 } nt_tracker;
 
 /* nt_run.flags */
 #define NT_TRACE 1u          /* write one nt_trace_rec per segment into outputs.trace */
-#define NT_HISTORY 2u        /* scheduler: history-based persistent kernel (one history per thread)
-                              * instead of the default event-based kernel with block-local event
-                              * queues (§2.3 event-based execution).  Results are
-                              * identical; only speed differs.  NT_TRACKER_RECT is history-based. */
+/* Scheduler of the generic tracker (results are identical; only speed differs).  Default: event
+ * queues per block (§2.3 event-based execution): a block owns block_dim particle slots
+ * and alternates a MOVE stage and an EVENT stage (collide / descend / birth), each over queues
+ * compacted with warp ballots, so every warp runs one event type on 32 slots at a time.         */
+#define NT_HISTORY 2u        /* history-based persistent kernel: one history per thread            */
+#define NT_WARPQ 4u          /* event queues per warp (64 slots per warp, no block barriers)      */
 
 /* Per-particle flag bits written to outputs.pflags (reading O16):
  *   F1: a cell/tile chosen by a descent has another surface within 1e-10 cm
@@ -208,7 +210,7 @@ typedef struct {
     uint64_t max_segments;    /* per history; 0 = 1e6; reaching it -> CAPPED                  */
     int32_t tracker;          /* nt_tracker                                                   */
     uint32_t flags;           /* NT_TRACE                                                     */
-    int32_t block_dim;        /* 0 = auto (256); event scheduler: 128 or 256 (tuning knob)    */
+    int32_t block_dim;        /* 0 = auto (256); block queues: 128 or 256; ignored by NT_WARPQ */
     int32_t blocks_per_sm;    /* 0 = auto (tuning knob)                                       */
 } nt_run;
 

@@ -20,7 +20,8 @@ BC = {"none": 0, "vacuum": 1, "reflect": 2}
 TRACKER = {"generic": 0, "rect": 1}
 NT_TRACE = 1
 NT_HISTORY = 2
-SCHEDULERS = ("event", "history")
+NT_WARPQ = 4
+SCHEDULERS = {"block": 0, "event": 0, "warp": NT_WARPQ, "history": NT_HISTORY}
 COUNTERS = ["particles", "segments", "crossings", "reflections", "leaks", "collisions",
             "absorptions", "lost", "capped", "flagged"] + [f"cross_l{i}" for i in range(8)]
 NC = len(COUNTERS)
@@ -241,7 +242,7 @@ class Model:
     # ---------------------------------------------------------------- tracking
     def make_run(self, n: int, seed: int, pid_begin: int = 0, lo=None, hi=None, max_segments: int = 0,
                  tracker: str = "generic", trace: bool = False, block_dim: int = 0,
-                 blocks_per_sm: int = 0, scheduler: str = "event") -> Run:
+                 blocks_per_sm: int = 0, scheduler: str = "block") -> Run:
         r = Run()
         r.seed, r.pid_begin, r.n = seed, pid_begin, n
         src = (self.spec or {}).get("source", {"lo": [0, 0, 0], "hi": [0, 0, 0]})
@@ -252,14 +253,14 @@ class Model:
         r.max_segments = max_segments
         r.tracker = TRACKER[tracker]
         assert scheduler in SCHEDULERS
-        r.flags = (NT_TRACE if trace else 0) | (NT_HISTORY if scheduler == "history" else 0)
+        r.flags = (NT_TRACE if trace else 0) | SCHEDULERS[scheduler]
         r.block_dim, r.blocks_per_sm = block_dim, blocks_per_sm
         return r
 
     def track(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
               max_segments: int = 0, tracker: str = "generic", pflags: bool = False,
               trace_cap: int = 0, states=None, out=None, stream=None, block_dim: int = 0,
-              blocks_per_sm: int = 0, per_history: bool = False, scheduler: str = "event"):
+              blocks_per_sm: int = 0, per_history: bool = False, scheduler: str = "block"):
         """Track histories [pid_begin, pid_begin+n) on this model's GPU (async on `stream`).
         Returns a dict of device tensors: out (accumulated), pflags, trace, trace_count."""
         import torch
@@ -299,7 +300,7 @@ class Model:
     def track_host(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
                    max_segments: int = 0, tracker: str = "generic", out: np.ndarray | None = None,
                    stream=None, block_dim: int = 0, blocks_per_sm: int = 0,
-                   scheduler: str = "event") -> np.ndarray:
+                   scheduler: str = "block") -> np.ndarray:
         """End-to-end call with a HOST output buffer (synchronous)."""
         if out is None:
             out = np.zeros(self.out_len)

@@ -38,14 +38,22 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objdir = os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
-    objs = []
+    objs, cmds = [], []
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         cmd = [NVCC, *ARCH, *FLAGS, "-c", src, "-o", obj]
         if verbose and src.endswith(".cu"):
             cmd += ["-Xptxas", "-v"]
-        subprocess.check_call(cmd)
+        cmds.append(cmd)
         objs.append(obj)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=min(len(cmds), os.cpu_count() or 4)) as ex:
+        procs = list(ex.map(lambda c: subprocess.run(c, capture_output=True, text=True), cmds))
+    for c, p in zip(cmds, procs):
+        sys.stdout.write(p.stdout)
+        sys.stderr.write(p.stderr)
+        if p.returncode != 0:
+            raise subprocess.CalledProcessError(p.returncode, c)
     tmp = LIB + ".tmp"
     subprocess.check_call([NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart_static", "-lrt", "-ldl",
                            "-lpthread"])

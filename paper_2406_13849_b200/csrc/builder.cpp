@@ -463,6 +463,12 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
   F.root = root;
   F.max_depth = depth;
 
+  // feature set of the (converted) model: selects the compiled kernel variant
+  for (const HSurf& s : S) {
+    if (s.kind == S_PLANE) F.features |= F_PLANE;
+    if (s.kind == S_SPHERE) F.features |= F_SPHERE;
+  }
+  for (const HUniv& u : U) if (u.kind == U_HEX) F.features |= F_HEX;
   // surfaces
   for (const HSurf& s : S) {
     DSurf d{};

@@ -260,7 +260,8 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     if (e == cudaSuccess) e = cudaMemset(m->counters, 0, sizeof(unsigned long long) * kSlots);
     double coef[30];
     coef_table(coef);
-    if (e == cudaSuccess) e = upload_coefficients(coef, 30);
+    if (e == cudaSuccess) e = f0::upload_coefficients(coef, 30);
+    if (e == cudaSuccess) e = f7::upload_coefficients(coef, 30);
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_err(e, "nt_finalize: upload");
     char* b = static_cast<char*>(m->blob);
@@ -293,6 +294,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
   g.n_cells = (int)F.cell_fill.size();
   g.n_surf = (int)F.surf.size();
   g.root_kind = F.univ[F.root].kind;
+  g.features = F.features;
   m->finalized = true;
   return NT_OK;
 }
@@ -367,7 +369,7 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   if (run->max_segments > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": max_segments >= 2^32");
   const int block = run->block_dim > 0 ? run->block_dim : 256;
   if (block % 32 || block > 256) return err(NT_E_ARG, std::string(who) + ": block_dim must be a multiple of 32, <= 256");
-  if (run->tracker == NT_TRACKER_GENERIC && !(run->flags & NT_HISTORY) && block != 128 && block != 256)
+  if (run->tracker == NT_TRACKER_GENERIC && !(run->flags & (NT_WARPQ | NT_HISTORY)) && block != 128 && block != 256)
     return err(NT_E_ARG, std::string(who) + ": the event scheduler needs block_dim 128 or 256");
   if (run->n > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": at most 2^32-1 histories per call");
   m->last_launches = 0;
@@ -395,12 +397,18 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   cudaError_t e = cudaMemsetAsync(R.counter, 0, sizeof(unsigned long long), s);
   int grid = 0;
   if (e == cudaSuccess) {
+    const bool st = d_states != nullptr, f0 = m->g.features == 0;
     if (run->tracker == NT_TRACKER_RECT)
-      e = launch_rect(m->g, m->rg, R, trace, d_states != nullptr, block, run->blocks_per_sm, s, &grid);
+      e = f0::launch_rect(m->g, m->rg, R, trace, st, block, run->blocks_per_sm, s, &grid);
     else if (run->flags & NT_HISTORY)
-      e = launch_generic(m->g, R, trace, d_states != nullptr, block, run->blocks_per_sm, s, &grid);
+      e = f0 ? f0::launch_generic(m->g, R, trace, st, block, run->blocks_per_sm, s, &grid)
+             : f7::launch_generic(m->g, R, trace, st, block, run->blocks_per_sm, s, &grid);
+    else if (run->flags & NT_WARPQ)
+      e = f0 ? f0::launch_wq(m->g, R, trace, st, run->blocks_per_sm, s, &grid)
+             : f7::launch_wq(m->g, R, trace, st, run->blocks_per_sm, s, &grid);
     else
-      e = launch_event(m->g, R, trace, d_states != nullptr, block, run->blocks_per_sm, s, &grid);
+      e = f0 ? f0::launch_event(m->g, R, trace, st, block, run->blocks_per_sm, s, &grid)
+             : f7::launch_event(m->g, R, trace, st, block, run->blocks_per_sm, s, &grid);
   }
   if (prev != m->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_err(e, who);
@@ -457,7 +465,9 @@ nt_status nt_find_cells(nt_model* m, const double* d_xyz, uint64_t n, int32_t* d
   int prev = 0;
   cudaGetDevice(&prev);
   if (prev != m->device) cudaSetDevice(m->device);
-  cudaError_t e = launch_find_cells(m->g, d_xyz, n, d_cell, d_flag, static_cast<cudaStream_t>(stream));
+  cudaError_t e = m->g.features == 0
+                      ? f0::launch_find_cells(m->g, d_xyz, n, d_cell, d_flag, static_cast<cudaStream_t>(stream))
+                      : f7::launch_find_cells(m->g, d_xyz, n, d_cell, d_flag, static_cast<cudaStream_t>(stream));
   if (prev != m->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_err(e, "nt_find_cells");
   return NT_OK;

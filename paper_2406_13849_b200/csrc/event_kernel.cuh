@@ -3,15 +3,16 @@
 //
 // Shift's GPU transport runs every tracking operation as a kernel over a masked vector of
 // histories.  Here one persistent block owns B particle slots (state in shared memory, SoA) and
-// runs three stages per round, each over a COMPACTED queue of the slots that need that event:
+// runs two stages per round, each over COMPACTED queues of the slots that need that event:
 //
-//   DESCEND  : find_cell / cross_surface descents (Alg. 7-8), queue sorted by universe kind of the
-//              crossing level (CSG first, then arrays), plus births into free slots (pid claims
-//              with a warp-aggregated atomic on the global counter);
+//   EVENT    : one queue sorted by event type: change_direction (absorption or isotropic scatter,
+//              P:399-409), then find_cell / cross_surface descents (Alg. 7-8) at CSG levels, then
+//              at array levels, then births into free slots (pid claims with a warp-aggregated
+//              atomic on the global counter).  Warps take consecutive 32-slot chunks, so each
+//              chunk is (almost always) one event type;
 //   MOVE     : distance_to_boundary over all levels + collide-or-cross + move_within_cell +
 //              track-length tally (Table 1, Alg. 2); each slot is appended to the queue
-//              of its next event with a ballot / popc / one shared atomic per warp;
-//   COLLIDE  : change_direction: absorption or isotropic scatter.
+//              of its next event with a ballot / popc / one shared atomic per warp.
 //
 // Every warp therefore executes one event type on 32 slots at a time instead of a mix of
 // divergent branches.  The per-level universe stack of each slot stays in shared memory between
@@ -19,7 +20,7 @@
 // (nt_geom.cuh, descend(), level_distances()), so results are bit-identical to it and to the oracle.
 #pragma once
 
-namespace nt {
+NT_DEV_BEGIN
 
 // Queue layout (uint16 slot indices), double-buffered by round parity p:
 //   Q_M[p] move-ready, Q_C[p] collide, Q_DC[p] CSG descents, Q_DA[p] array descents, Q_F[p] free
@@ -110,20 +111,20 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
 
   for (int round = 0;; ++round) {
     const int p = round & 1, q = p ^ 1;
-    // ================= DESCEND (+ births) =================
+    // ================= EVENT: collisions, descents, births =================
     {
-      // C[p] was consumed by COLLIDE(r-2); M[q] by MOVE(r-1): both are refilled from MOVE(r) on
-      if (tid == 0) { QN(p, Q_C) = 0; QN(q, Q_M) = 0; }
-      const int ndc = QN(q, Q_DC), nda = QN(q, Q_DA), nfr = QN(q, Q_F);
-      const int total = ndc + nda + nfr;
+      if (tid == 0) QN(q, Q_M) = 0;                        // M[q] was consumed by MOVE(r-1)
+      const int nco = QN(q, Q_C), ndc = QN(q, Q_DC), nda = QN(q, Q_DA), nfr = QN(q, Q_F);
+      const int total = nco + ndc + nda + nfr;
       for (int base = warp * 32; base < total; base += B) {
         const int i = base + lane;
         const bool valid = i < total;
-        int slot = 0, kind = 3;                           // 0 CSG descent, 1 array descent, 2 birth
+        int slot = 0, kind = 3;                           // 4 collide, 0 CSG descent, 1 array descent, 2 birth
         if (valid) {
-          if (i < ndc) { slot = Q(q, Q_DC)[i]; kind = 0; }
-          else if (i < ndc + nda) { slot = Q(q, Q_DA)[i - ndc]; kind = 1; }
-          else { slot = Q(q, Q_F)[i - ndc - nda]; kind = 2; }
+          if (i < nco) { slot = Q(q, Q_C)[i]; kind = 4; }
+          else if (i < nco + ndc) { slot = Q(q, Q_DC)[i - nco]; kind = 0; }
+          else if (i < nco + ndc + nda) { slot = Q(q, Q_DA)[i - nco - ndc]; kind = 1; }
+          else { slot = Q(q, Q_F)[i - nco - ndc - nda]; kind = 2; }
         }
         // births: claim pids for this warp's birth lanes (warp-aggregated)
         const unsigned bm = __ballot_sync(0xffffffffu, kind == 2);
@@ -139,15 +140,37 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
             else s_flag[0] = 1;                          // pids exhausted: slot stays unused
           }
         }
-        bool ok = false, done = false;
-        Stack st;
-        st.si = sib + slot;
-        st.sT = sTb + slot;
-        st.B = B;
-        double rx = 0, ry = 0, rz = 0;
-        uint32_t flags = 0;
-        int L = 0, mc = 0;
-        if (kind == 0 || kind == 1 || born) {
+        bool ok = false, done = false, scat = false, absorbed = false;
+        if (kind == 4) {
+          // ---- change_direction (O14, O15)
+          const uint64_t pid = R.pid0 + sidx[slot];
+          const uint32_t epoch = sepoch[slot] + 1;
+          sepoch[slot] = epoch;
+          const int mc = smc[slot];
+          double xa, xb;
+          draw2(R.seed, pid, epoch, 0, xa, xb);
+          const int cb = TRACE ? ld(g.mc_cell + mc) : 0;
+          if (xa < ld(g.mc_pabs + mc)) {
+            absorbed = true;
+            if (TRACE) emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_ABSORBED, sflags[slot]);
+            finalize(slot, NT_T_ABSORBED);
+          } else {
+            double xmu, xphi, u, v, w;
+            draw2(R.seed, pid, epoch, 1, xmu, xphi);
+            isotropic(xmu, xphi, u, v, w);
+            su[slot] = u; sv[slot] = v; sw[slot] = w;
+            stau[slot] = -spec_log(xb);
+            scat = true;
+            if (TRACE) emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_NONE, sflags[slot]);
+          }
+        } else if (kind == 0 || kind == 1 || born) {
+          Stack st;
+          st.si = sib + slot;
+          st.sT = sTb + slot;
+          st.B = B;
+          double rx = 0, ry = 0, rz = 0;
+          uint32_t flags = 0;
+          int L = 0, mc = 0;
           int l0 = 0, du = g.root, fsid = -1, fsense = 0;
           double Tx = 0.0, Ty = 0.0, Tz = 0.0;
           if (born) {
@@ -189,7 +212,7 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
               const DUniv* U = g.univ + st.u(l0);
               const int uk = ld(&U->kind);
               int ta = st.a(l0), tb = st.b(l0), tc = st.c(l0);
-              if (uk == U_RECT) {
+              if (!kHex || uk == U_RECT) {
                 const int dir = (j & 1) ? 1 : -1, ax = j >> 1;
                 if (ax == 0) ta += dir; else if (ax == 1) tb += dir; else tc += dir;
               } else if (j < 6) {
@@ -209,8 +232,6 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
           }
           ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
           done = true;
-        }
-        if (done) {
           if (!ok) flags |= NT_F3;
           sflags[slot] = static_cast<uint8_t>(flags);
           if (ok) { sL[slot] = static_cast<uint8_t>(L); smc[slot] = mc; }
@@ -226,9 +247,9 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
           }
           if (!ok) finalize(slot, NT_T_LOST);
         }
-        const int pm = warp_append(done && ok, &QN(p, Q_M), lane);
+        const int pm = warp_append((done && ok) || scat, &QN(p, Q_M), lane);
         if (pm >= 0) Q(p, Q_M)[pm] = static_cast<uint16_t>(slot);
-        const int pf = warp_append(done && !ok, &QN(p, Q_F), lane);
+        const int pf = warp_append((done && !ok) || absorbed, &QN(p, Q_F), lane);
         if (pf >= 0) Q(p, Q_F)[pf] = static_cast<uint16_t>(slot);
       }
     }
@@ -237,8 +258,8 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
     if (QN(p, Q_M) == 0 && s_flag[0]) break;
     // ================= MOVE =================
     {
-      // DC/DA/F[q] were consumed by DESCEND(r); they are refilled from MOVE(r+1) / round r+1 on
-      if (tid == 0) { QN(q, Q_DC) = 0; QN(q, Q_DA) = 0; QN(q, Q_F) = 0; }
+      // C/DC/DA/F[q] were consumed by EVENT(r); they are refilled from MOVE(r+1) / EVENT(r+1) on
+      if (tid == 0) { QN(q, Q_C) = 0; QN(q, Q_DC) = 0; QN(q, Q_DA) = 0; QN(q, Q_F) = 0; }
       const int total = QN(p, Q_M);
       for (int base = warp * 32; base < total; base += B) {
         const int i = base + lane;
@@ -357,44 +378,6 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
       }
     }
     __syncthreads();
-    // ================= COLLIDE =================
-    {
-      const int total = QN(p, Q_C);
-      for (int base = warp * 32; base < total; base += B) {
-        const int i = base + lane;
-        const bool valid = i < total;
-        const int slot = valid ? Q(p, Q_C)[i] : 0;
-        bool scat = false, absorbed = false;
-        if (valid) {
-          const uint64_t pid = R.pid0 + sidx[slot];
-          const uint32_t epoch = sepoch[slot] + 1;
-          sepoch[slot] = epoch;
-          const int mc = smc[slot];
-          double xa, xb;
-          draw2(R.seed, pid, epoch, 0, xa, xb);
-          const int cb = TRACE ? ld(g.mc_cell + mc) : 0;
-          if (xa < ld(g.mc_pabs + mc)) {
-            absorbed = true;
-            emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_ABSORBED,
-                        sflags[slot]);
-            finalize(slot, NT_T_ABSORBED);
-          } else {
-            double xmu, xphi, u, v, w;
-            draw2(R.seed, pid, epoch, 1, xmu, xphi);
-            isotropic(xmu, xphi, u, v, w);
-            su[slot] = u; sv[slot] = v; sw[slot] = w;
-            stau[slot] = -spec_log(xb);
-            scat = true;
-            emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_NONE, sflags[slot]);
-          }
-        }
-        int pos = warp_append(scat, &QN(q, Q_M), lane);
-        if (pos >= 0) Q(q, Q_M)[pos] = static_cast<uint16_t>(slot);
-        pos = warp_append(absorbed, &QN(p, Q_F), lane);
-        if (pos >= 0) Q(p, Q_F)[pos] = static_cast<uint16_t>(slot);
-      }
-    }
-    __syncthreads();
   }
 
   // ---- flush block tallies: exits / counters from shared memory, lengths from the block slice
@@ -402,4 +385,4 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
   flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
 }
 
-}  // namespace nt
+NT_DEV_END

@@ -7,9 +7,14 @@
 
 #include "nt_layout.hpp"
 
-namespace nt {
+NT_DEV_BEGIN
 
 #define NT_INF __longlong_as_double(0x7ff0000000000000ULL)
+
+// kinds compiled into this feature set (see nt_layout.hpp)
+constexpr bool kHex = (NT_FEAT & F_HEX) != 0;
+constexpr bool kPlane = (NT_FEAT & F_PLANE) != 0;
+constexpr bool kSphere = (NT_FEAT & F_SPHERE) != 0;
 
 template <class T>
 __device__ __forceinline__ T ld(const T* p) { return __ldg(p); }
@@ -24,51 +29,58 @@ __device__ __forceinline__ double sel3(int a, double x, double y, double z) {
 __device__ __forceinline__ double surf_f(int kind, const DSurf* sp, double x, double y, double z) {
   if (kind <= S_PZ) return sel3(kind, x, y, z) - ld(&sp->c[0]);
   const double c0 = ld(&sp->c[0]), c1 = ld(&sp->c[1]), c2 = ld(&sp->c[2]), c3 = ld(&sp->c[3]);
-  if (kind == S_PLANE) return ((c0 * x + c1 * y) + c2 * z) - c3;
+  if (kPlane && kind == S_PLANE) return ((c0 * x + c1 * y) + c2 * z) - c3;
   const double dx = x - c0, dy = y - c1;
-  if (kind == S_CZ) return (dx * dx + dy * dy) - c2;
+  if (!kSphere || kind == S_CZ) return (dx * dx + dy * dy) - c2;
   const double dz = z - c2;
   return ((dx * dx + dy * dy) + dz * dz) - c3;
 }
 
 // forward distance to leave half-space (kind, sense) along (u,v,w) from (x,y,z); O11.
 // os: particle logically on this surface (quadric c := 0).  Returns +inf when no exit.
+// Written with ONE division and ONE square root per call (selected operands) to keep the
+// code small; the selected operands are exactly those of the case formulas in DESIGN.md O11.
 __device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const DSurf* sp, double x,
                                             double y, double z, double u, double v, double w) {
+  double num, den;
+  bool ok;
   if (kind <= S_PZ) {
-    const double uu = sel3(kind, u, v, w);
-    if (sense ? !(uu < 0.0) : !(uu > 0.0)) return NT_INF;   // also uu == 0
-    return clamp0((ld(&sp->c[0]) - sel3(kind, x, y, z)) / uu);
-  }
-  const double c0 = ld(&sp->c[0]), c1 = ld(&sp->c[1]), c2 = ld(&sp->c[2]), c3 = ld(&sp->c[3]);
-  if (kind == S_PLANE) {
-    const double sd = (c0 * u + c1 * v) + c2 * w;
-    if (sense ? !(sd < 0.0) : !(sd > 0.0)) return NT_INF;
-    const double fr = (c0 * x + c1 * y) + c2 * z;
-    return clamp0((c3 - fr) / sd);
-  }
-  double a, k, c, q;
-  if (kind == S_CZ) {
-    const double dx = x - c0, dy = y - c1;
-    a = u * u + v * v;
-    if (a == 0.0) return NT_INF;
-    k = dx * u + dy * v;
-    c = os ? 0.0 : (dx * dx + dy * dy) - c2;
-    q = k * k - a * c;
+    den = sel3(kind, u, v, w);
+    ok = sense ? den < 0.0 : den > 0.0;                      // also excludes den == 0
+    num = ld(&sp->c[0]) - sel3(kind, x, y, z);
   } else {
-    const double dx = x - c0, dy = y - c1, dz = z - c2;
-    a = 1.0;
-    k = (dx * u + dy * v) + dz * w;
-    c = os ? 0.0 : ((dx * dx + dy * dy) + dz * dz) - c3;
-    q = k * k - c;
+    const double c0 = ld(&sp->c[0]), c1 = ld(&sp->c[1]), c2 = ld(&sp->c[2]), c3 = ld(&sp->c[3]);
+    if (kPlane && kind == S_PLANE) {
+      den = (c0 * u + c1 * v) + c2 * w;
+      ok = sense ? den < 0.0 : den > 0.0;
+      num = c3 - ((c0 * x + c1 * y) + c2 * z);
+    } else {
+      double a, k, c, q;
+      if (!kSphere || kind == S_CZ) {
+        const double dx = x - c0, dy = y - c1;
+        a = u * u + v * v;
+        k = dx * u + dy * v;
+        c = os ? 0.0 : (dx * dx + dy * dy) - c2;
+        q = k * k - a * c;
+      } else {
+        const double dx = x - c0, dy = y - c1, dz = z - c2;
+        a = 1.0;
+        k = (dx * u + dy * v) + dz * w;
+        c = os ? 0.0 : ((dx * dx + dy * dy) + dz * dz) - c3;
+        q = k * k - c;
+      }
+      const double sq = sqrt(q > 0.0 ? q : 0.0);                 // q < 0: max(q,0) inside, miss outside
+      if (!sense) {             // inside (negative side): far root
+        ok = a != 0.0;
+        if (k <= 0.0) { num = -k + sq; den = a; } else { num = -c; den = k + sq; }
+      } else {                  // outside: moving away or missing -> no exit
+        ok = a != 0.0 && k < 0.0 && q >= 0.0;
+        num = c;
+        den = -k + sq;
+      }
+    }
   }
-  if (!sense) {   // inside (negative side): far root
-    if (q < 0.0) q = 0.0;
-    const double d = k <= 0.0 ? (-k + sqrt(q)) / a : -c / (k + sqrt(q));
-    return clamp0(d);
-  }
-  if (k >= 0.0 || q < 0.0) return NT_INF;   // outside: moving away or missing
-  return clamp0(c / (-k + sqrt(q)));
+  return ok ? clamp0(num / den) : NT_INF;
 }
 
 // Alg. 3 "cell contains pos" with an optional logically forced sense (O9'); on success the
@@ -132,6 +144,12 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
   }
 }
 
+// forward wall of a rect tile along one axis (O11 RECT walls): (e(i+1) - x)/u or (e(i) - x)/u
+__device__ __forceinline__ double rect_wall(double ll, double p, int i, double x, double u) {
+  const double e = ll + static_cast<double>(u > 0.0 ? i + 1 : i) * p;
+  return clamp0((e - x) / u);
+}
+
 // O8: the unique i with e(i) <= x < e(i+1), e(i) = ll + i p
 __device__ __forceinline__ int rect_index(double ll, double p, double x) {
   int i = static_cast<int>(floor((x - ll) / p));
@@ -145,28 +163,37 @@ __device__ __forceinline__ bool near_wall(double ll, double p, int i, double x) 
          fabs(x - (ll + static_cast<double>(i + 1) * p)) <= kFlagDist;
 }
 
+// tile centre of an array (the daughter translation, readings O8/O9).  rect (i,j,k), hex (q,r,kz).
+__device__ __forceinline__ void array_centre(const DUniv* U, int kind, int a, int b, int c, double& tx,
+                                             double& ty, double& tz) {
+  if (!kHex || kind == U_RECT) {
+    tx = ld(&U->d[0]) + (static_cast<double>(a) + 0.5) * ld(&U->d[3]);
+    ty = ld(&U->d[1]) + (static_cast<double>(b) + 0.5) * ld(&U->d[4]);
+    tz = ld(&U->is2d) ? 0.0 : ld(&U->d[2]) + (static_cast<double>(c) + 0.5) * ld(&U->d[5]);
+  } else {
+    tx = ld(&U->d[0]) + (static_cast<double>(a) * ld(&U->d[6]) + static_cast<double>(b) * ld(&U->d[8]));
+    ty = ld(&U->d[1]) + (static_cast<double>(a) * ld(&U->d[7]) + static_cast<double>(b) * ld(&U->d[9]));
+    tz = ld(&U->i1) > 0 ? ld(&U->d[4]) + (static_cast<double>(c) + 0.5) * ld(&U->d[5]) : 0.0;
+  }
+}
+
 // daughter universe of an array tile (fill inside the lattice, else outer) and the tile
 // centre (daughter translation).  Tile indices: rect (i,j,k), hex (q,r,kz).
 __device__ __forceinline__ int array_daughter(const DevGeom& g, const DUniv* U, int kind, int a, int b,
                                               int c, double& tx, double& ty, double& tz) {
   int idx = -1;
-  if (kind == U_RECT) {
+  if (!kHex || kind == U_RECT) {
     const int n0 = ld(&U->i0), n1 = ld(&U->i1), n2 = ld(&U->i2), is2d = ld(&U->is2d);
     const bool in = a >= 0 && a < n0 && b >= 0 && b < n1 && (is2d || (c >= 0 && c < n2));
     if (in) idx = ld(g.fills + ld(&U->fill_off) + a + n0 * (b + n1 * (is2d ? 0 : c)));
-    tx = ld(&U->d[0]) + (static_cast<double>(a) + 0.5) * ld(&U->d[3]);
-    ty = ld(&U->d[1]) + (static_cast<double>(b) + 0.5) * ld(&U->d[4]);
-    tz = is2d ? 0.0 : ld(&U->d[2]) + (static_cast<double>(c) + 0.5) * ld(&U->d[5]);
   } else {
     const int R = ld(&U->i0), nz = ld(&U->i1);
     const int aq = abs(a), ar = abs(b), as = abs(a + b);
     const int dd = max(aq, max(ar, as));
     const bool in = dd <= R && (nz == 0 || (c >= 0 && c < nz));
     if (in) idx = ld(g.fills + ld(&U->fill_off) + (b + R) * (2 * R + 1) + (a + R) + (nz > 0 ? c * ld(&U->ntile) : 0));
-    tx = ld(&U->d[0]) + (static_cast<double>(a) * ld(&U->d[6]) + static_cast<double>(b) * ld(&U->d[8]));
-    ty = ld(&U->d[1]) + (static_cast<double>(a) * ld(&U->d[7]) + static_cast<double>(b) * ld(&U->d[9]));
-    tz = nz > 0 ? ld(&U->d[4]) + (static_cast<double>(c) + 0.5) * ld(&U->d[5]) : 0.0;
   }
+  array_centre(U, kind, a, b, c, tx, ty, tz);
   return idx >= 0 ? idx : ld(&U->outer);
 }
 
@@ -203,6 +230,7 @@ __device__ __forceinline__ void hex_locate(const DUniv* U, double x, double y, i
   hex_t(U, x, y, t0, t1, t2);
   int q = qc, r = rc;
   bool ok = false;
+#pragma unroll 1
   for (int it = 0; it < 4; ++it) {
     double m0, m1, m2;
     hex_m(q, r, m0, m1, m2);
@@ -241,4 +269,4 @@ struct Best {
   }
 };
 
-}  // namespace nt
+NT_DEV_END

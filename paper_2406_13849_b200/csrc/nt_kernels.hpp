@@ -24,14 +24,21 @@ struct KRun {
   double* slices;                   // [grid][n_mc] zeroed per-block track-length tallies (global)
 };
 
-cudaError_t upload_coefficients(const double* host, int n);
-cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
-                           int blocks_per_sm, cudaStream_t stream, int* grid_out);
-cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states,
-                        int block, int blocks_per_sm, cudaStream_t stream, int* grid_out);
-cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
-                         int blocks_per_sm, cudaStream_t stream, int* grid_out);
-cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,
-                              uint8_t* flag, cudaStream_t stream);
+// one copy of the launchers per compiled feature set (track_f0.cu, track_f7.cu)
+#define NT_LAUNCHERS \
+cudaError_t upload_coefficients(const double* host, int n); \
+cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool states, int block, \
+                           int blocks_per_sm, cudaStream_t stream, int* grid_out); \
+cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states, \
+                        int block, int blocks_per_sm, cudaStream_t stream, int* grid_out); \
+cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block, \
+                         int blocks_per_sm, cudaStream_t stream, int* grid_out); \
+cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, int blocks_per_sm, \
+                      cudaStream_t stream, int* grid_out); \
+cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell, \
+                              uint8_t* flag, cudaStream_t stream); \
+
+namespace f0 { NT_LAUNCHERS }
+namespace f7 { NT_LAUNCHERS }
 
 }  // namespace nt

@@ -12,7 +12,21 @@
 #define NT_HD inline
 #endif
 
+// Device code is compiled once per feature set (track_f0.cu: rect/CSG models with axis planes and
+// cylinders only; track_f7.cu: everything) into namespace nt::NT_NS, so a model that uses no hex
+// arrays, general planes or spheres runs a kernel without that code (smaller i-cache footprint).
+#ifndef NT_NS
+#define NT_NS fall
+#endif
+#ifndef NT_FEAT
+#define NT_FEAT 7
+#endif
+#define NT_DEV_BEGIN namespace nt { namespace NT_NS {
+#define NT_DEV_END } }
+
 namespace nt {
+
+enum Feature : int { F_HEX = 1, F_PLANE = 2, F_SPHERE = 4 };
 
 constexpr int kMaxDepth = 8;          // builder-enforced nesting limit (reading O7)
 constexpr int kNC = 18;               // counters (NT_NC)
@@ -70,7 +84,7 @@ struct DevGeom {
   const double* mc_pabs;      // per material cell: sigma_a / sigma_t (O14)
   const int32_t* mc_cell;     // per material cell: global cell id (trace)
   int32_t root, n_mc, max_depth, n_univ;
-  int32_t n_cells, n_surf, root_kind, pad;
+  int32_t n_cells, n_surf, root_kind, features;   // features: F_* bits present in the model
 };
 
 // Rect-specialised tracker tables (Alg. 9-10): root = axis box or concentric CZ annuli between a

@@ -57,7 +57,7 @@ struct Flat {
   std::vector<double> mc_st, mc_pabs;
   std::vector<int32_t> mc_cell;
   std::vector<int32_t> bih_depth;   // per universe (CSG), host info
-  int root = -1, max_depth = 0, n_mc = 0;
+  int root = -1, max_depth = 0, n_mc = 0, features = 0;
   // rect-specialised tables
   bool rect_ok = false;
   int rect_K = 0;

@@ -6,7 +6,7 @@
 // (SURVEY pin P13) and their rate ratio isolates the cost of generality.
 #pragma once
 
-namespace nt {
+NT_DEV_BEGIN
 
 template <int K, bool BOX, bool TRACE, bool STATES>
 __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectGeom rg, const KRun R) {
@@ -366,4 +366,4 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
   flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
 }
 
-}  // namespace nt
+NT_DEV_END

@@ -23,7 +23,7 @@
 #include "nt_layout.hpp"
 #include "nt_math.cuh"
 
-namespace nt {
+NT_DEV_BEGIN
 
 
 
@@ -43,14 +43,18 @@ struct Stack {
 
 // Alg. 7 descent from level l0 in universe u with frame translation T; forced sense applies
 // at level l0 only (CSG cross_surface).  Returns false when a level has no cell (LOST).
+template <bool STORE_T = true>
 __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int u, double Tx, double Ty,
                                      double Tz, double rx, double ry, double rz, int fsid, int fsense,
                                      int& L, int& mc, uint32_t& flags) {
+#pragma unroll 1
   for (int l = l0; l < kMaxDepth; ++l) {
     st.u(l) = u;
-    st.T(l, 0) = Tx;
-    st.T(l, 1) = Ty;
-    st.T(l, 2) = Tz;
+    if (STORE_T) {
+      st.T(l, 0) = Tx;
+      st.T(l, 1) = Ty;
+      st.T(l, 2) = Tz;
+    }
     const double x = rx - Tx, y = ry - Ty, z = rz - Tz;
     const DUniv* U = g.univ + u;
     const int kind = ld(&U->kind);
@@ -66,7 +70,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
       tx = ld(g.cell_tr + 3 * cell);
       ty = ld(g.cell_tr + 3 * cell + 1);
       tz = ld(g.cell_tr + 3 * cell + 2);
-    } else if (kind == U_RECT) {
+    } else if (!kHex || kind == U_RECT) {
       const double llx = ld(&U->d[0]), lly = ld(&U->d[1]), px = ld(&U->d[3]), py = ld(&U->d[4]);
       const int i = rect_index(llx, px, x), j = rect_index(lly, py, y);
       uint32_t nb = near_wall(llx, px, i, x) | near_wall(lly, py, j, y);
@@ -99,15 +103,12 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
   return false;
 }
 
-// distance candidates of level l (canonical order, O13)
-__device__ __forceinline__ void level_distances(const DevGeom& g, Stack& st, int l, double rx, double ry,
-                                                double rz, double u, double v, double w, int os_l,
-                                                int os_s, Best& b) {
-  const double x = rx - st.T(l, 0), y = ry - st.T(l, 1), z = rz - st.T(l, 2);
-  const DUniv* U = g.univ + st.u(l);
-  const int kind = ld(&U->kind);
+// distance candidates of level l in its local frame (canonical order, O13)
+__device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* U, int kind, int ia, int ib,
+                                                 int ic, int l, double x, double y, double z, double u,
+                                                 double v, double w, int os_l, int os_s, Best& b) {
   if (kind == U_CSG) {
-    const int cell = st.a(l);
+    const int cell = ia;
     const int h0 = ld(g.cell_hs + cell), h1 = ld(g.cell_hs + cell + 1);
     for (int h = h0; h < h1; ++h) {
       const int e = ld(g.hs + h);
@@ -116,35 +117,47 @@ __device__ __forceinline__ void level_distances(const DevGeom& g, Stack& st, int
                                  v, w);
       if (d < NT_INF) b.consider(d, l, sid, hs_sense(e));
     }
-  } else if (kind == U_RECT) {
-    const int i = st.a(l), j = st.b(l);
-    if (u > 0.0) b.consider(clamp0((ld(&U->d[0]) + static_cast<double>(i + 1) * ld(&U->d[3]) - x) / u), l, 1, 0);
-    else if (u < 0.0) b.consider(clamp0((ld(&U->d[0]) + static_cast<double>(i) * ld(&U->d[3]) - x) / u), l, 0, 0);
-    if (v > 0.0) b.consider(clamp0((ld(&U->d[1]) + static_cast<double>(j + 1) * ld(&U->d[4]) - y) / v), l, 3, 0);
-    else if (v < 0.0) b.consider(clamp0((ld(&U->d[1]) + static_cast<double>(j) * ld(&U->d[4]) - y) / v), l, 2, 0);
-    if (!ld(&U->is2d)) {
-      const int k = st.c(l);
-      if (w > 0.0) b.consider(clamp0((ld(&U->d[2]) + static_cast<double>(k + 1) * ld(&U->d[5]) - z) / w), l, 5, 0);
-      else if (w < 0.0) b.consider(clamp0((ld(&U->d[2]) + static_cast<double>(k) * ld(&U->d[5]) - z) / w), l, 4, 0);
-    }
+  } else if (!kHex || kind == U_RECT) {
+    if (u != 0.0) b.consider(rect_wall(ld(&U->d[0]), ld(&U->d[3]), ia, x, u), l, u > 0.0 ? 1 : 0, 0);
+    if (v != 0.0) b.consider(rect_wall(ld(&U->d[1]), ld(&U->d[4]), ib, y, v), l, v > 0.0 ? 3 : 2, 0);
+    if (!ld(&U->is2d) && w != 0.0) b.consider(rect_wall(ld(&U->d[2]), ld(&U->d[5]), ic, z, w), l, w > 0.0 ? 5 : 4, 0);
   } else {
     double t0, t1, t2, m0, m1, m2;
     hex_t(U, x, y, t0, t1, t2);
-    hex_m(st.a(l), st.b(l), m0, m1, m2);
+    hex_m(ia, ib, m0, m1, m2);
     const double p = ld(&U->d[2]);
     const double tk[3] = {t0, t1, t2}, mk[3] = {m0, m1, m2};
-#pragma unroll
+#pragma unroll 1
     for (int k = 0; k < 3; ++k) {
       const double gk = ld(&U->d[10 + 2 * k]) * u + ld(&U->d[11 + 2 * k]) * v;
-      if (gk > 0.0) b.consider(clamp0((p * ((mk[k] + 0.5) - tk[k])) / gk), l, k, 0);
-      else if (gk < 0.0) b.consider(clamp0((p * ((mk[k] - 0.5) - tk[k])) / gk), l, k + 3, 0);
+      if (gk != 0.0) {
+        const double bnd = gk > 0.0 ? mk[k] + 0.5 : mk[k] - 0.5;
+        b.consider(clamp0((p * (bnd - tk[k])) / gk), l, gk > 0.0 ? k : k + 3, 0);
+      }
     }
-    if (ld(&U->i1) > 0) {
-      const int k = st.c(l);
-      const double zl = ld(&U->d[4]), zp = ld(&U->d[5]);
-      if (w > 0.0) b.consider(clamp0((zl + static_cast<double>(k + 1) * zp - z) / w), l, 7, 0);
-      else if (w < 0.0) b.consider(clamp0((zl + static_cast<double>(k) * zp - z) / w), l, 6, 0);
-    }
+    if (ld(&U->i1) > 0 && w != 0.0)
+      b.consider(rect_wall(ld(&U->d[4]), ld(&U->d[5]), ic, z, w), l, w > 0.0 ? 7 : 6, 0);
+  }
+}
+
+// distance candidates of level l using the stored frame T_l
+__device__ __forceinline__ void level_distances(const DevGeom& g, Stack& st, int l, double rx, double ry,
+                                                double rz, double u, double v, double w, int os_l,
+                                                int os_s, Best& b) {
+  const double x = rx - st.T(l, 0), y = ry - st.T(l, 1), z = rz - st.T(l, 2);
+  const DUniv* U = g.univ + st.u(l);
+  level_candidates(g, U, ld(&U->kind), st.a(l), st.b(l), st.c(l), l, x, y, z, u, v, w, os_l, os_s, b);
+}
+
+// translation from the frame of level l to the frame of level l+1 (same arithmetic as descend)
+__device__ __forceinline__ void level_translation(const DevGeom& g, const DUniv* U, int kind, int ia, int ib,
+                                                  int ic, double& tx, double& ty, double& tz) {
+  if (kind == U_CSG) {
+    tx = ld(g.cell_tr + 3 * ia);
+    ty = ld(g.cell_tr + 3 * ia + 1);
+    tz = ld(g.cell_tr + 3 * ia + 2);
+  } else {
+    array_centre(U, kind, ia, ib, ic, tx, ty, tz);
   }
 }
 
@@ -313,7 +326,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
               phase = 1;
             } else {               // Alg. 6: tile +- 1, then the new tile's daughter
               int ta = st.a(l), tb = st.b(l), tc = st.c(l);
-              if (kind == U_RECT) {
+              if (!kHex || kind == U_RECT) {
                 const int dir = (j & 1) ? 1 : -1, ax = j >> 1;
                 if (ax == 0) ta += dir; else if (ax == 1) tb += dir; else tc += dir;
               } else if (j < 6) {
@@ -383,10 +396,13 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
   flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
 }
 
-}  // namespace nt
+NT_DEV_END
 #include "event_kernel.cuh"
+#include "wq_kernel.cuh"
+#if NT_FEAT == 0
 #include "rect_kernel.cuh"
-namespace nt {
+#endif
+NT_DEV_BEGIN
 
 // point location for unit parity (Alg. 7)
 __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const double* xyz, uint64_t n,
@@ -453,6 +469,7 @@ cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool sta
   return states ? pick(k_track_generic<false, true>) : pick(k_track_generic<false, false>);
 }
 
+#if NT_FEAT == 0
 cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states,
                         int block, int blocks_per_sm, cudaStream_t stream, int* grid_out) {
   const size_t smem = (kNC + (size_t)g.n_mc) * 4;
@@ -495,6 +512,12 @@ cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, boo
   return states ? pick_k(F{}, F{}, T{}) : pick_k(F{}, F{}, F{});
 }
 
+#else
+cudaError_t launch_rect(const DevGeom&, const RectGeom&, const KRun&, bool, bool, int, int, cudaStream_t, int*) {
+  return cudaErrorNotSupported;   // rect-specialisable models always use feature set 0
+}
+#endif
+
 cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
                          int blocks_per_sm, cudaStream_t stream, int* grid_out) {
   const size_t smem = event_smem_bytes(g, block, trace);
@@ -525,6 +548,33 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
   return states ? go(k_track_event<256, false, true>) : go(k_track_event<256, false, false>);
 }
 
+cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, int blocks_per_sm,
+                      cudaStream_t stream, int* grid_out) {
+  const size_t smem = wq_smem_bytes(g, trace);
+  const int block = kWqWarps * 32;
+  auto go = [&](auto kern) -> cudaError_t {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int dev = 0, nsm = 0, occ = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
+    if (e != cudaSuccess) return e;
+    if (occ < 1) return cudaErrorInvalidConfiguration;
+    const int bps = blocks_per_sm > 0 ? (blocks_per_sm < occ ? blocks_per_sm : occ) : occ;
+    const uint64_t per_block = (uint64_t)kWqWarps * kWqSlots;
+    uint64_t need = (R.n + per_block - 1) / per_block, grid = (uint64_t)nsm * bps;
+    if (need < grid) grid = need ? need : 1;
+    *grid_out = (int)grid;
+    return with_slices(g, R, grid, stream, [&](const KRun& Rs) {
+      kern<<<(unsigned)grid, block, smem, stream>>>(g, Rs);
+      return cudaGetLastError();
+    });
+  };
+  if (trace) return states ? go(k_track_wq<true, true>) : go(k_track_wq<true, false>);
+  return states ? go(k_track_wq<false, true>) : go(k_track_wq<false, false>);
+}
+
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,
                               uint8_t* flag, cudaStream_t stream) {
   const int block = 256;
@@ -538,4 +588,4 @@ cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, i
   return cudaGetLastError();
 }
 
-}  // namespace nt
+NT_DEV_END

@@ -34,7 +34,7 @@ def orc():
 
 
 def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, tracker="generic",
-             trace=True, pseudo=False, scheduler="event", block_dim=0):
+             trace=True, pseudo=False, scheduler="block", block_dim=0):
     m = nt.Model.from_spec(spec, device=0, pseudo_array=pseudo)
     om = orc.OracleModel.from_spec(spec)
     cap = 400 * max(n, 1) + 64 if trace else 0
@@ -68,7 +68,7 @@ def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, t
 CONFIG_N = {"c1": 2000, "c2": 600, "c3": 600, "c4": 600, "c5m": 600, "c5r": 600}
 
 
-@pytest.mark.parametrize("sched", ["event", "history"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history"])
 @pytest.mark.parametrize("cfg", list(CONFIG_N))
 def test_config_trace_parity(nt, orc, cfg, sched):
     """Every BASELINE config: full traces bit-exact vs the oracle (seeded, small batch), with
@@ -103,10 +103,11 @@ def test_test_models_parity(nt, orc, name):
 def test_ragged_batches_and_large_pids(nt, orc, n, block):
     """Ragged batch sizes (partial warps / blocks) and pids above 2^32 (counter hi word)."""
     spec, _ = workloads.config("c2")
-    _compare(nt, orc, spec, n, seed=3, pid_begin=(1 << 33) + 17, block_dim=block)
+    _compare(nt, orc, spec, n, seed=3, pid_begin=(1 << 33) + 17, block_dim=block, scheduler="block")
+    _compare(nt, orc, spec, n, seed=3, pid_begin=(1 << 33) + 17, scheduler="warp")
 
 
-@pytest.mark.parametrize("sched", ["event", "history"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history"])
 def test_capped_histories(nt, orc, sched):
     """max_segments reached -> CAPPED (F3) on both sides, same extra trace record."""
     spec, _ = workloads.config("c1")
@@ -114,7 +115,7 @@ def test_capped_histories(nt, orc, sched):
     assert g["counters"]["capped"] > 0
 
 
-@pytest.mark.parametrize("sched", ["event", "history"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history"])
 def test_lost_at_birth(nt, orc, sched):
     """Births outside every root cell are LOST at birth (source box larger than the model)."""
     spec = workloads.c1_pincell()
@@ -123,7 +124,7 @@ def test_lost_at_birth(nt, orc, sched):
     assert g["counters"]["lost"] > 0
 
 
-@pytest.mark.parametrize("sched", ["event", "history"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history"])
 def test_explicit_states(nt, orc, sched):
     """nt_track_states: explicit birth states (chord rays through the void pincell)."""
     spec = workloads.c1_pincell(bc="vacuum", void=True)
