@@ -1,0 +1,69 @@
+"""Multi-rank path on CPU (gloo, world size 2): contiguous pid sharding + one all-reduce of the
+packed [len | exits | counters] buffer.  The per-rank tracker here is the oracle
+(no GPU in this container); on a GPU box the same `track_distributed` calls nt_track."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+import workloads
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, cfg, n, seed, outdir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    import paper_2406_13849_b200 as nt
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    spec, _ = workloads.config(cfg)
+    om = oracle.OracleModel.from_spec(spec)
+    seen = []
+
+    def tracker(nn, pid0):
+        seen.append((pid0, nn))
+        return torch.from_numpy(om.run(nn, seed=seed, pid_begin=pid0, threads=1)["out"].copy())
+
+    out = nt.track_distributed(None, n, seed, pid_begin=0, tracker_fn=tracker)
+    np.save(os.path.join(outdir, f"out_{rank}.npy"), out.numpy())
+    np.save(os.path.join(outdir, f"shard_{rank}.npy"), np.array(seen[0]))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("cfg,n", [("c2", 301), ("c3", 257)])
+def test_two_rank_sharding_allreduce(tmp_path, oracle_mod, cfg, n):
+    port = _free_port()
+    mp.spawn(_worker, args=(2, port, cfg, n, 5, str(tmp_path)), nprocs=2, join=True)
+    o0 = np.load(tmp_path / "out_0.npy")
+    o1 = np.load(tmp_path / "out_1.npy")
+    assert np.array_equal(o0, o1)                       # every rank holds the combined tally
+    s0, s1 = np.load(tmp_path / "shard_0.npy"), np.load(tmp_path / "shard_1.npy")
+    assert tuple(s0) == (0, n // 2) and tuple(s1) == (n // 2, n - n // 2)   # contiguous shards
+    spec, _ = workloads.config(cfg)
+    om = oracle_mod.OracleModel.from_spec(spec)
+    full = om.run(n, seed=5, threads=1)
+    got = om.unpack(o0)
+    assert got["counters"] == full["counters"]          # exact for any world size
+    assert np.array_equal(got["exits"], full["exits"])
+    assert np.allclose(got["len"], full["len"], rtol=1e-13, atol=0)
+
+
+def test_shard_function():
+    import paper_2406_13849_b200 as nt
+    for N in (0, 1, 7, 100, 10**8 + 3):
+        for G in (1, 2, 3, 8):
+            shards = [nt.shard(N, g, G) for g in range(G)]
+            assert sum(k for _, k in shards) == N
+            assert all(shards[g][0] + shards[g][1] == (shards[g + 1][0] if g + 1 < G else N) for g in range(G))
