@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libnestrack.so")
+LIB_PATH = os.environ.get("NESTRACK_LIB", os.path.join(HERE, "libnestrack.so"))   # override: tuning builds
 
 KIND = {"PX": 0, "PY": 1, "PZ": 2, "PLANE": 3, "CZ": 4, "SPHERE": 5}
 BC = {"none": 0, "vacuum": 1, "reflect": 2}
