@@ -244,6 +244,12 @@ nt_status nt_find_cells(nt_model* m, const double* d_xyz, uint64_t n, int32_t* d
 /* Number of kernel launches issued by the last tracking call on this model (evidence). */
 int32_t nt_last_launch_count(const nt_model* m);
 
+/* Device self-test of the kernels' fp64 division / square root (nt_math.cuh fdiv, fsqrt) against
+ * the IEEE `/` and sqrt on n random operand pairs spanning the walk's ranges.
+ * mismatches[0] = division mismatches, mismatches[1] = sqrt mismatches (host array of 2).
+ * Synchronous on the current device. */
+nt_status nt_selftest_arith(uint64_t n, uint64_t seed, uint64_t* mismatches);
+
 #ifdef __cplusplus
 }
 #endif

@@ -70,7 +70,8 @@ SYMBOLS = ["nt_last_error", "nt_abi_version", "nt_model_create", "nt_model_destr
            "nt_add_material", "nt_add_csg_universe", "nt_add_cell", "nt_add_rect_array",
            "nt_add_hex_array", "nt_set_root", "nt_build_opts_default", "nt_finalize",
            "nt_model_info_get", "nt_material_cell_ids", "nt_bih_info", "nt_track",
-           "nt_track_states", "nt_track_host", "nt_find_cells", "nt_last_launch_count"]
+           "nt_track_states", "nt_track_host", "nt_find_cells", "nt_last_launch_count",
+           "nt_selftest_arith"]
 
 
 def lib():
@@ -102,6 +103,7 @@ def lib():
         L.nt_track_host.argtypes = [vp, C.POINTER(Run), dp, vp]
         L.nt_find_cells.argtypes = [vp, dp, u64, dp, dp, vp]
         L.nt_last_launch_count.argtypes = [vp]
+        L.nt_selftest_arith.argtypes = [u64, u64, dp]
         _lib = L
     return _lib
 
@@ -337,6 +339,13 @@ class Model:
         assert cnt <= cap, f"trace overflow: {cnt} > {cap}"
         t = buf[:cnt * TRACE_DTYPE.itemsize].view(TRACE_DTYPE)
         return np.sort(t, order=["pid", "seg", "terminal"])
+
+
+def selftest_arith(n: int = 1 << 26, seed: int = 1):
+    """Device check of the kernels' division / sqrt against IEEE: returns (div, sqrt) mismatches."""
+    out = np.zeros(2, dtype=np.uint64)
+    _check(lib().nt_selftest_arith(n, seed, _p(out)))
+    return int(out[0]), int(out[1])
 
 
 def shard(n_total: int, rank: int, world: int) -> tuple[int, int]:

@@ -475,4 +475,16 @@ nt_status nt_find_cells(nt_model* m, const double* d_xyz, uint64_t n, int32_t* d
 
 int32_t nt_last_launch_count(const nt_model* m) { return m ? m->last_launches : 0; }
 
+nt_status nt_selftest_arith(uint64_t n, uint64_t seed, uint64_t* mismatches) {
+  if (!mismatches) return err(NT_E_ARG, "nt_selftest_arith: mismatches is NULL");
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = cudaMemset(d, 0, 2 * sizeof(unsigned long long));
+  if (e == cudaSuccess) e = f0::selftest_arith(n, seed, d);
+  if (e == cudaSuccess) e = cudaMemcpy(mismatches, d, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (d) cudaFree(d);
+  if (e != cudaSuccess) return cuda_err(e, "nt_selftest_arith");
+  return NT_OK;
+}
+
 }  // extern "C"

@@ -6,6 +6,7 @@
 #include <cstdint>
 
 #include "nt_layout.hpp"
+#include "nt_math.cuh"
 
 NT_DEV_BEGIN
 
@@ -69,7 +70,7 @@ __device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const 
         c = os ? 0.0 : ((dx * dx + dy * dy) + dz * dz) - c3;
         q = k * k - c;
       }
-      const double sq = sqrt(q > 0.0 ? q : 0.0);                 // q < 0: max(q,0) inside, miss outside
+      const double sq = fsqrt(q > 0.0 ? q : 0.0);                 // q < 0: max(q,0) inside, miss outside
       if (!sense) {             // inside (negative side): far root
         ok = a != 0.0;
         if (k <= 0.0) { num = -k + sq; den = a; } else { num = -c; den = k + sq; }
@@ -80,7 +81,7 @@ __device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const 
       }
     }
   }
-  return ok ? clamp0(num / den) : NT_INF;
+  return ok ? clamp0(fdiv(num, den)) : NT_INF;
 }
 
 // Alg. 3 "cell contains pos" with an optional logically forced sense (O9'); on success the
@@ -147,12 +148,12 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
 // forward wall of a rect tile along one axis (O11 RECT walls): (e(i+1) - x)/u or (e(i) - x)/u
 __device__ __forceinline__ double rect_wall(double ll, double p, int i, double x, double u) {
   const double e = ll + static_cast<double>(u > 0.0 ? i + 1 : i) * p;
-  return clamp0((e - x) / u);
+  return clamp0(fdiv(e - x, u));
 }
 
 // O8: the unique i with e(i) <= x < e(i+1), e(i) = ll + i p
 __device__ __forceinline__ int rect_index(double ll, double p, double x) {
-  int i = static_cast<int>(floor((x - ll) / p));
+  int i = static_cast<int>(floor(fdiv(x - ll, p)));
   while (!(ll + static_cast<double>(i) * p <= x)) --i;
   while (!(x < ll + static_cast<double>(i + 1) * p)) ++i;
   return i;
@@ -200,9 +201,9 @@ __device__ __forceinline__ int array_daughter(const DevGeom& g, const DUniv* U, 
 // hex t-space coordinates t_k = (n_k . (x - C)) / p  (O9)
 __device__ __forceinline__ void hex_t(const DUniv* U, double x, double y, double& t0, double& t1, double& t2) {
   const double xp = x - ld(&U->d[0]), yp = y - ld(&U->d[1]), p = ld(&U->d[2]);
-  t0 = (ld(&U->d[10]) * xp + ld(&U->d[11]) * yp) / p;
-  t1 = (ld(&U->d[12]) * xp + ld(&U->d[13]) * yp) / p;
-  t2 = (ld(&U->d[14]) * xp + ld(&U->d[15]) * yp) / p;
+  t0 = fdiv(ld(&U->d[10]) * xp + ld(&U->d[11]) * yp, p);
+  t1 = fdiv(ld(&U->d[12]) * xp + ld(&U->d[13]) * yp, p);
+  t2 = fdiv(ld(&U->d[14]) * xp + ld(&U->d[15]) * yp, p);
 }
 
 __device__ __forceinline__ void hex_m(int q, int r, double& m0, double& m1, double& m2) {
@@ -218,8 +219,8 @@ __device__ __forceinline__ void hex_locate(const DUniv* U, double x, double y, i
   const double xp = x - ld(&U->d[0]), yp = y - ld(&U->d[1]);
   const double p = ld(&U->d[2]), pH = ld(&U->d[3]);
   double qf, rf;
-  if (ld(&U->i2) == 0) { rf = yp / pH; qf = (xp - rf * (p * 0.5)) / p; }
-  else { qf = xp / pH; rf = (yp - qf * (p * 0.5)) / p; }
+  if (ld(&U->i2) == 0) { rf = fdiv(yp, pH); qf = fdiv(xp - rf * (p * 0.5), p); }
+  else { qf = fdiv(xp, pH); rf = fdiv(yp - qf * (p * 0.5), p); }
   const double sf = -qf - rf;
   double qr = round(qf), rr = round(rf), sr = round(sf);
   const double dq = fabs(qr - qf), dr = fabs(rr - rf), ds = fabs(sr - sf);

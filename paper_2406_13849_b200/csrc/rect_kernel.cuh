@@ -236,15 +236,10 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
             const DUniv* U = g.univ + lu[q];
             const double x = rx - Tx[q], y = ry - Ty[q], z = rz - Tz[q];
             const int i = li[q], j = lj[q];
-            if (u > 0.0) b.consider(clamp0((ld(&U->d[0]) + static_cast<double>(i + 1) * ld(&U->d[3]) - x) / u), lv, 1, 0);
-            else if (u < 0.0) b.consider(clamp0((ld(&U->d[0]) + static_cast<double>(i) * ld(&U->d[3]) - x) / u), lv, 0, 0);
-            if (v > 0.0) b.consider(clamp0((ld(&U->d[1]) + static_cast<double>(j + 1) * ld(&U->d[4]) - y) / v), lv, 3, 0);
-            else if (v < 0.0) b.consider(clamp0((ld(&U->d[1]) + static_cast<double>(j) * ld(&U->d[4]) - y) / v), lv, 2, 0);
-            if (!ld(&U->is2d)) {
-              const int k = lk[q];
-              if (w > 0.0) b.consider(clamp0((ld(&U->d[2]) + static_cast<double>(k + 1) * ld(&U->d[5]) - z) / w), lv, 5, 0);
-              else if (w < 0.0) b.consider(clamp0((ld(&U->d[2]) + static_cast<double>(k) * ld(&U->d[5]) - z) / w), lv, 4, 0);
-            }
+            if (u != 0.0) b.consider(rect_wall(ld(&U->d[0]), ld(&U->d[3]), i, x, u), lv, u > 0.0 ? 1 : 0, 0);
+            if (v != 0.0) b.consider(rect_wall(ld(&U->d[1]), ld(&U->d[4]), j, y, v), lv, v > 0.0 ? 3 : 2, 0);
+            if (!ld(&U->is2d) && w != 0.0)
+              b.consider(rect_wall(ld(&U->d[2]), ld(&U->d[5]), lk[q], z, w), lv, w > 0.0 ? 5 : 4, 0);
           }
           // pin: inner cylinder (outside of it), then outer cylinder (inside of it)
           const int off = ld(rg.pin_off + pin), ncz = ld(rg.pin_off + pin + 1) - off;
@@ -262,7 +257,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
         }
         const double sig = ld(g.mc_st + mc);
         const double ds = b.d;
-        const double dc = sig > 0.0 ? tau / sig : NT_INF;
+        const double dc = sig > 0.0 ? fdiv(tau, sig) : NT_INF;
         const double g2 = b.d2 - ds, gc = fabs(dc - ds);
         if ((g2 > 0.0 && g2 <= kFlagDist) || (gc > 0.0 && gc <= kFlagDist)) flags |= NT_F2;
         const int cell_before = TRACE ? ld(g.mc_cell + mc) : 0;

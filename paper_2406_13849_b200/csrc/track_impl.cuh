@@ -132,7 +132,7 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
       const double gk = ld(&U->d[10 + 2 * k]) * u + ld(&U->d[11 + 2 * k]) * v;
       if (gk != 0.0) {
         const double bnd = gk > 0.0 ? mk[k] + 0.5 : mk[k] - 0.5;
-        b.consider(clamp0((p * (bnd - tk[k])) / gk), l, gk > 0.0 ? k : k + 3, 0);
+        b.consider(clamp0(fdiv(p * (bnd - tk[k]), gk)), l, gk > 0.0 ? k : k + 3, 0);
       }
     }
     if (ld(&U->i1) > 0 && w != 0.0)
@@ -282,7 +282,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
         for (int l = 0; l < L; ++l) level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
         const double sig = ld(g.mc_st + mc);
         const double ds = b.d;
-        const double dc = sig > 0.0 ? tau / sig : NT_INF;
+        const double dc = sig > 0.0 ? fdiv(tau, sig) : NT_INF;
         const double g2 = b.d2 - ds, gc = fabs(dc - ds);
         if ((g2 > 0.0 && g2 <= kFlagDist) || (gc > 0.0 && gc <= kFlagDist)) flags |= NT_F2;
         const int cell_before = TRACE ? ld(g.mc_cell + mc) : 0;
@@ -573,6 +573,32 @@ cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, 
   };
   if (trace) return states ? go(k_track_wq<true, true>) : go(k_track_wq<true, false>);
   return states ? go(k_track_wq<false, true>) : go(k_track_wq<false, false>);
+}
+
+// device self-test: fdiv / fsqrt against IEEE `/` and sqrt on operands spanning the walk's ranges
+__global__ void k_selftest_arith(uint64_t n, uint64_t seed, unsigned long long* bad) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    double x0, x1, x2, x3;
+    draw2(seed, i, 7, 0, x0, x1);
+    draw2(seed, i, 7, 1, x2, x3);
+    double a = exp10(-20.0 + 26.0 * x0) * (x1 < 0.5 ? -1.0 : 1.0);
+    if (x1 > 0.98) a = 0.0;
+    const double b = exp10(-25.0 + 25.5 * x2) * (x3 < 0.5 ? -1.0 : 1.0);
+    const double xs = x3 > 0.99 ? 0.0 : exp10(-40.0 + 52.0 * x0);
+    const double q1 = fdiv(a, b), q2 = a / b;
+    if (__double_as_longlong(q1) != __double_as_longlong(q2)) atomicAdd(bad, 1ull);
+    const double s1 = fsqrt(xs), s2 = sqrt(xs);
+    if (__double_as_longlong(s1) != __double_as_longlong(s2)) atomicAdd(bad + 1, 1ull);
+    // geometric shapes: differences of nearby coordinates over direction cosines
+    const double e = (x2 - 0.5) * 400.0, xx = e + (x0 - 0.5) * 1e-6;
+    const double q3 = fdiv(e - xx, x1 - 0.5), q4 = (e - xx) / (x1 - 0.5);
+    if (__double_as_longlong(q3) != __double_as_longlong(q4)) atomicAdd(bad, 1ull);
+  }
+}
+
+cudaError_t selftest_arith(uint64_t n, uint64_t seed, unsigned long long* d_bad) {
+  k_selftest_arith<<<148 * 8, 256>>>(n, seed, d_bad);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,

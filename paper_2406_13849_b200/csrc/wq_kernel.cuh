@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
           }
           const double sig = ld(g.mc_st + mc);
           const double ds = b.d;
-          const double dc = sig > 0.0 ? tau / sig : NT_INF;
+          const double dc = sig > 0.0 ? fdiv(tau, sig) : NT_INF;
           const double g2 = b.d2 - ds, gc = fabs(dc - ds);
           if ((g2 > 0.0 && g2 <= kFlagDist) || (gc > 0.0 && gc <= kFlagDist)) flags |= NT_F2;
           const int cell_before = TRACE ? ld(g.mc_cell + mc) : 0;

@@ -257,3 +257,9 @@ def test_rect_tracker_rejects_hex(nt, cfg):
     with pytest.raises(nt.NtError) as e:
         m.track(10, seed=1, tracker="rect")
     assert e.value.status == -5
+
+
+def test_fast_division_sqrt_are_ieee(nt):
+    """The kernels' slow-path-free division / sqrt return the IEEE results bit for bit on 2^26
+    random operands spanning (and exceeding) the walk's ranges."""
+    assert nt.selftest_arith(1 << 26, 3) == (0, 0)
