@@ -2,17 +2,16 @@
 // for sm_100a).
 //
 // Shift's GPU transport runs every tracking operation as a kernel over a masked vector of
-// histories.  Here one persistent block owns B particle slots (state in shared memory, SoA) and
-// runs two stages per round, each over COMPACTED queues of the slots that need that event:
-//
-//   EVENT    : one queue sorted by event type: change_direction (absorption or isotropic scatter,
-//              P:399-409), then find_cell / cross_surface descents (Alg. 7-8) at CSG levels, then
-//              at array levels, then births into free slots (pid claims with a warp-aggregated
-//              atomic on the global counter).  Warps take consecutive 32-slot chunks, so each
-//              chunk is (almost always) one event type;
-//   MOVE     : distance_to_boundary over all levels + collide-or-cross + move_within_cell +
-//              track-length tally (Table 1, Alg. 2); each slot is appended to the queue
-//              of its next event with a ballot / popc / one shared atomic per warp.
+// histories.  Here one persistent block owns B particle slots (state in shared memory, SoA).
+// Each round, every live slot takes one EVENT and one MOVE, taken from ONE queue that is sorted
+// by event type: reflected slots (no event), change_direction (absorption or isotropic scatter,
+// P:399-409), find_cell / cross_surface descents (Alg. 7-8) at CSG levels, then at array levels,
+// then births into free slots (pid claims with a warp-aggregated atomic on the global counter).
+// A warp takes a consecutive 32-slot chunk, so a chunk is (almost always) one event type; the
+// same warp then runs MOVE on those slots: distance_to_boundary over all levels + collide-or-cross
+// + move_within_cell + track-length tally (Table 1, Alg. 2).  Each slot is appended to
+// the next round's queue of its next event with a ballot / popc / one shared atomic per warp.
+// One block barrier per round separates the rounds (queues are triple-buffered).
 //
 // Every warp therefore executes one event type on 32 slots at a time instead of a mix of
 // divergent branches.  The per-level universe stack of each slot stays in shared memory between
@@ -22,9 +21,10 @@
 
 NT_DEV_BEGIN
 
-// Queue layout (uint16 slot indices), double-buffered by round parity p:
+// Queue layout (uint8 slot indices), triple-buffered by round:
 //   Q_M[p] move-ready, Q_C[p] collide, Q_DC[p] CSG descents, Q_DA[p] array descents, Q_F[p] free
 enum { Q_M = 0, Q_C = 1, Q_DC = 2, Q_DA = 3, Q_F = 4, NQ = 5 };
+using QIdx = uint8_t;           // slot index in a queue (blocks own <= 256 slots)
 
 __device__ __forceinline__ int warp_append(bool pred, int* counter, int lane) {
   const unsigned m = __ballot_sync(0xffffffffu, pred);
@@ -48,8 +48,8 @@ size_t event_smem_bytes(const DevGeom& g, int B, bool trace) {
   s += (6 + 4 * d + (trace ? 2 : 0)) * 4 * (size_t)B;                 // ints
   s += (3 + (trace ? 1 : 0)) * (size_t)B;                             // bytes
   s = (s + 15) & ~size_t(15);
-  s += 2 * NQ * 2 * (size_t)B;                                         // queues (uint16)
-  s += (nmc + kNC + 2 * NQ + 4) * 4;                                    // exits, counters, queue counts
+  s += 3 * NQ * sizeof(QIdx) * (size_t)B;                              // queues (triple-buffered)
+  s += (nmc + kNC + 3 * NQ + 4) * 4;                                    // exits, counters, queue counts
   return (s + 15) & ~size_t(15);
 }
 
@@ -78,18 +78,18 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
   int8_t* spl = sosl + B;                           // TRACE: pending level
   size_t off = (size_t)(reinterpret_cast<unsigned char*>(spl + (TRACE ? B : 0)) - smem);
   off = (off + 15) & ~size_t(15);
-  uint16_t* sq = reinterpret_cast<uint16_t*>(smem + off);   // [2][NQ][B]
-  unsigned int* s_exit = reinterpret_cast<unsigned int*>(sq + 2 * NQ * B);
+  QIdx* sq = reinterpret_cast<QIdx*>(smem + off);            // [3][NQ][B]
+  unsigned int* s_exit = reinterpret_cast<unsigned int*>(sq + 3 * NQ * B);
   unsigned int* s_cnt = s_exit + nmc;
-  int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [2][NQ]
-  int* s_flag = s_qn + 2 * NQ;                              // [0] = pids exhausted
+  int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [3][NQ]
+  int* s_flag = s_qn + 3 * NQ;                              // [0] = pids exhausted
   double* gl = R.slices + (size_t)blockIdx.x * nmc;         // per-block track-length tally (global)
 
   for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
-  if (tid < 2 * NQ) s_qn[tid] = 0;
-  if (tid == 0) { s_flag[0] = 0; s_qn[1 * NQ + Q_F] = B; }
-  for (int i = tid; i < B; i += B) sq[(1 * NQ + Q_F) * B + i] = static_cast<uint16_t>(i);   // all slots free
+  if (tid < 3 * NQ) s_qn[tid] = 0;
+  if (tid == 0) { s_flag[0] = 0; s_qn[0 * NQ + Q_F] = B; }
+  for (int i = tid; i < B; i += B) sq[(0 * NQ + Q_F) * B + i] = static_cast<QIdx>(i);   // round 0 reads set 0: all slots free
   __syncthreads();
 
   auto Q = [&](int p, int q) { return sq + (p * NQ + q) * B; };
@@ -110,22 +110,25 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
   };
 
   for (int round = 0;; ++round) {
-    const int p = round & 1, q = p ^ 1;
-    // ================= EVENT: collisions, descents, births =================
-    {
-      if (tid == 0) QN(q, Q_M) = 0;                        // M[q] was consumed by MOVE(r-1)
-      const int nco = QN(q, Q_C), ndc = QN(q, Q_DC), nda = QN(q, Q_DA), nfr = QN(q, Q_F);
-      const int total = nco + ndc + nda + nfr;
-      for (int base = warp * 32; base < total; base += B) {
-        const int i = base + lane;
-        const bool valid = i < total;
-        int slot = 0, kind = 3;                           // 4 collide, 0 CSG descent, 1 array descent, 2 birth
-        if (valid) {
-          if (i < nco) { slot = Q(q, Q_C)[i]; kind = 4; }
-          else if (i < nco + ndc) { slot = Q(q, Q_DC)[i - nco]; kind = 0; }
-          else if (i < nco + ndc + nda) { slot = Q(q, Q_DA)[i - nco - ndc]; kind = 1; }
-          else { slot = Q(q, Q_F)[i - nco - ndc - nda]; kind = 2; }
-        }
+    // queues triple-buffered by round: read rd (filled in round-1), append wr, reset rs
+    const int rd = round % 3, wr = (round + 1) % 3, rs = (round + 2) % 3;
+    if (tid == 0)
+      for (int k = 0; k < NQ; ++k) QN(rs, k) = 0;          // read in round-1, refilled in round+1
+    const int nmv = QN(rd, Q_M), nco = QN(rd, Q_C), ndc = QN(rd, Q_DC), nda = QN(rd, Q_DA), nfr = QN(rd, Q_F);
+    const int total = nmv + nco + ndc + nda + nfr;
+    for (int base = warp * 32; base < total; base += B) {
+      const int i = base + lane;
+      const bool valid = i < total;
+      // kind: 5 move only (reflected), 4 collide, 0 CSG descent, 1 array descent, 2 birth, 3 none
+      int slot = 0, kind = 3;
+      if (valid) {
+        if (i < nmv) { slot = Q(rd, Q_M)[i]; kind = 5; }
+        else if (i < nmv + nco) { slot = Q(rd, Q_C)[i - nmv]; kind = 4; }
+        else if (i < nmv + nco + ndc) { slot = Q(rd, Q_DC)[i - nmv - nco]; kind = 0; }
+        else if (i < nmv + nco + ndc + nda) { slot = Q(rd, Q_DA)[i - nmv - nco - ndc]; kind = 1; }
+        else { slot = Q(rd, Q_F)[i - nmv - nco - ndc - nda]; kind = 2; }
+      }
+      // ---------------- EVENT: change_direction / descent / birth of this chunk's slots
         // births: claim pids for this warp's birth lanes (warp-aggregated)
         const unsigned bm = __ballot_sync(0xffffffffu, kind == 2);
         bool born = false;
@@ -247,28 +250,17 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
           }
           if (!ok) finalize(slot, NT_T_LOST);
         }
-        const int pm = warp_append((done && ok) || scat, &QN(p, Q_M), lane);
-        if (pm >= 0) Q(p, Q_M)[pm] = static_cast<uint16_t>(slot);
-        const int pf = warp_append((done && !ok) || absorbed, &QN(p, Q_F), lane);
-        if (pf >= 0) Q(p, Q_F)[pf] = static_cast<uint16_t>(slot);
+      const bool ready = kind == 5 || (done && ok) || scat;
+      {
+        const int pf = warp_append((done && !ok) || absorbed, &QN(wr, Q_F), lane);
+        if (pf >= 0) Q(wr, Q_F)[pf] = static_cast<QIdx>(slot);
       }
-    }
-    __syncthreads();
-    // termination: every live history is in M[p] at this point; none left and no more pids
-    if (QN(p, Q_M) == 0 && s_flag[0]) break;
-    // ================= MOVE =================
-    {
-      // C/DC/DA/F[q] were consumed by EVENT(r); they are refilled from MOVE(r+1) / EVENT(r+1) on
-      if (tid == 0) { QN(q, Q_C) = 0; QN(q, Q_DC) = 0; QN(q, Q_DA) = 0; QN(q, Q_F) = 0; }
-      const int total = QN(p, Q_M);
-      for (int base = warp * 32; base < total; base += B) {
-        const int i = base + lane;
-        const bool valid = i < total;
-        const int slot = valid ? Q(p, Q_M)[i] : 0;
+      // ---------------- MOVE the same slots (no barrier between a slot's event and its move)
+      {
         // outcome: 0 none, 1 reflect (-> M), 2 collide, 3 CSG descent, 4 array descent, 5 ended
         int outc = 0, term = NT_T_NONE, lcross = -1;
         bool seg = false;
-        if (valid) {
+        if (ready) {
           Stack st;
           st.si = sib + slot;
           st.sT = sTb + slot;
@@ -365,19 +357,21 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
           for (int lv = 0; lv < maxd; ++lv) warp_count(lcross == lv, s_cnt + C_CBL0 + lv, lane);
         // enqueue for the next event
         int pos;
-        pos = warp_append(outc == 1, &QN(q, Q_M), lane);
-        if (pos >= 0) Q(q, Q_M)[pos] = static_cast<uint16_t>(slot);
-        pos = warp_append(outc == 2, &QN(p, Q_C), lane);
-        if (pos >= 0) Q(p, Q_C)[pos] = static_cast<uint16_t>(slot);
-        pos = warp_append(outc == 3, &QN(p, Q_DC), lane);
-        if (pos >= 0) Q(p, Q_DC)[pos] = static_cast<uint16_t>(slot);
-        pos = warp_append(outc == 4, &QN(p, Q_DA), lane);
-        if (pos >= 0) Q(p, Q_DA)[pos] = static_cast<uint16_t>(slot);
-        pos = warp_append(outc == 5, &QN(p, Q_F), lane);
-        if (pos >= 0) Q(p, Q_F)[pos] = static_cast<uint16_t>(slot);
+        pos = warp_append(outc == 1, &QN(wr, Q_M), lane);
+        if (pos >= 0) Q(wr, Q_M)[pos] = static_cast<QIdx>(slot);
+        pos = warp_append(outc == 2, &QN(wr, Q_C), lane);
+        if (pos >= 0) Q(wr, Q_C)[pos] = static_cast<QIdx>(slot);
+        pos = warp_append(outc == 3, &QN(wr, Q_DC), lane);
+        if (pos >= 0) Q(wr, Q_DC)[pos] = static_cast<QIdx>(slot);
+        pos = warp_append(outc == 4, &QN(wr, Q_DA), lane);
+        if (pos >= 0) Q(wr, Q_DA)[pos] = static_cast<QIdx>(slot);
+        pos = warp_append(outc == 5, &QN(wr, Q_F), lane);
+        if (pos >= 0) Q(wr, Q_F)[pos] = static_cast<QIdx>(slot);
       }
     }
     __syncthreads();
+    // termination: no live history queued for the next round and no more pids
+    if (QN(wr, Q_M) + QN(wr, Q_C) + QN(wr, Q_DC) + QN(wr, Q_DA) == 0 && s_flag[0]) break;
   }
 
   // ---- flush block tallies: exits / counters from shared memory, lengths from the block slice
