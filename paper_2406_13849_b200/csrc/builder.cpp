@@ -226,7 +226,9 @@ struct BihBuilder {
 
   void fill(int node, std::vector<int> idx, int d) {
     depth = std::max(depth, d);
-    if ((int)idx.size() <= max_leaf || d >= 40) { make_leaf(node, idx); return; }
+    // depth is bounded by the traversal's register stack (kBihStack); a deeper subtree becomes
+    // one larger leaf (still exact: the leaf is scanned linearly)
+    if ((int)idx.size() <= max_leaf || d >= kBihStack) { make_leaf(node, idx); return; }
     Aabb nb = Aabb::empty(), cen = Aabb::empty();
     for (int c : idx) {
       nb.grow(cb[c]);
@@ -524,6 +526,7 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
       F.bih.push_back({});
       B.fill(node, X.cells, 0);
       F.bih_depth[u] = B.depth;
+      if ((int)F.bih.size() - node >= 65535) fail("BIH of universe %ld has more than 65535 nodes", u);
       d.i0 = node;
       d.i1 = X.cells.empty() ? 0 : X.cells.front();
       d.i2 = (int)X.cells.size();

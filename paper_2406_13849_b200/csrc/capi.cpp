@@ -475,6 +475,14 @@ nt_status nt_find_cells(nt_model* m, const double* d_xyz, uint64_t n, int32_t* d
 
 int32_t nt_last_launch_count(const nt_model* m) { return m ? m->last_launches : 0; }
 
+// debug (tuning builds with -DNT_BIH_STATS): BIH traversal counters of feature set `fset` (0 / 7)
+extern "C" nt_status nt_debug_bih_stats(int32_t fset, uint64_t* out4, int32_t reset) {
+  cudaError_t e = fset == 0 ? f0::bih_stats(reinterpret_cast<unsigned long long*>(out4), reset != 0)
+                            : f7::bih_stats(reinterpret_cast<unsigned long long*>(out4), reset != 0);
+  if (e != cudaSuccess) return cuda_err(e, "nt_debug_bih_stats");
+  return NT_OK;
+}
+
 nt_status nt_selftest_arith(uint64_t n, uint64_t seed, uint64_t* mismatches) {
   if (!mismatches) return err(NT_E_ARG, "nt_selftest_arith: mismatches is NULL");
   unsigned long long* d = nullptr;

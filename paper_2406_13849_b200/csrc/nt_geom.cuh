@@ -107,41 +107,74 @@ __device__ __forceinline__ bool cell_contains(const DevGeom& g, int cell, double
   return true;
 }
 
-// BIH traversal: both children are visited when the point lies in the overlap.
+// BIH traversal for point location: both children are visited when the point lies
+// in their overlap.  Register-resident stack: up to kBihStack pending node indices (relative to the
+// universe's root, 16 bits each) packed in three 64-bit registers -- no local memory.  The builder
+// bounds the tree depth by kBihStack and the node count per universe by 65536, so the stack
+// cannot overflow.  "While-while" form: a lane first walks internal nodes down to a leaf, then
+// tests the leaf's cells, which keeps the lanes of a warp on the same loop body.
+struct BihStack {
+  uint64_t s0 = 0, s1 = 0, s2 = 0;
+  __device__ __forceinline__ void push(uint32_t v) {
+    s2 = (s2 << 16) | (s1 >> 48);
+    s1 = (s1 << 16) | (s0 >> 48);
+    s0 = (s0 << 16) | v;
+  }
+  // returns the popped index, or -1 when empty (entries are stored +1 so that 0 marks empty)
+  __device__ __forceinline__ int pop() {
+    const int v = static_cast<int>(s0 & 0xFFFFull) - 1;
+    s0 = (s0 >> 16) | (s1 << 48);
+    s1 = (s1 >> 16) | (s2 << 48);
+    s2 >>= 16;
+    return v;
+  }
+};
+
+#ifdef NT_BIH_STATS
+__device__ unsigned long long g_bih_stats[4];   // calls, node visits, cell tests, root-leaf calls
+#endif
 __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, double y, double z,
                                         int fsid, int fsense, uint32_t& flags) {
-  int stack[24];
-  int sp = 0, node = root;
+#ifdef NT_BIH_STATS
+  atomicAdd(&g_bih_stats[0], 1ull);
+#endif
+  BihStack stk;
+  int node = 0;                                          // relative to root
   for (;;) {
-    const BihNode* n = g.bih + node;
-    const int meta = ld(&n->meta), a = ld(&n->a);
-    if (meta < 0) {
-      const int cnt = -meta - 1;
-      for (int q = 0; q < cnt; ++q) {
-        const int cell = ld(g.bih_leaf + a + q);
-        uint32_t nb = 0;
-        if (cell_contains(g, cell, x, y, z, fsid, fsense, nb)) {
-          flags |= nb;
-          return cell;
-        }
-      }
-      if (sp == 0) return -1;
-      node = stack[--sp];
-    } else {
+    int meta, a;
+    for (;;) {                                           // internal nodes down to a leaf
+      const BihNode* n = g.bih + root + node;
+      meta = ld(&n->meta);
+      a = ld(&n->a);
+#ifdef NT_BIH_STATS
+      atomicAdd(&g_bih_stats[1], 1ull);
+#endif
+      if (meta < 0) break;
       const double c = sel3(meta, x, y, z);
       const bool gl = c <= ld(&n->lmax), gr = c >= ld(&n->rmin);
-      if (gl && gr) {
-        if (sp < 24) stack[sp++] = a + 1;
-        node = a;
-      } else if (gl) {
-        node = a;
-      } else if (gr) {
-        node = a + 1;
-      } else {
-        if (sp == 0) return -1;
-        node = stack[--sp];
+      const int left = a - root;
+      if (gl && gr) { stk.push(static_cast<uint32_t>(left + 2)); node = left; }
+      else if (gl) node = left;
+      else if (gr) node = left + 1;
+      else {
+        node = stk.pop();
+        if (node < 0) return -1;
       }
     }
+    const int cnt = -meta - 1;                           // leaf: test its cells
+    for (int q = 0; q < cnt; ++q) {
+      const int cell = ld(g.bih_leaf + a + q);
+      uint32_t nb = 0;
+#ifdef NT_BIH_STATS
+      atomicAdd(&g_bih_stats[2], 1ull);
+#endif
+      if (cell_contains(g, cell, x, y, z, fsid, fsense, nb)) {
+        flags |= nb;
+        return cell;
+      }
+    }
+    node = stk.pop();
+    if (node < 0) return -1;
   }
 }
 

@@ -36,6 +36,7 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
 cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, int blocks_per_sm, \
                       cudaStream_t stream, int* grid_out); \
 cudaError_t selftest_arith(uint64_t n, uint64_t seed, unsigned long long* d_bad); \
+cudaError_t bih_stats(unsigned long long* host4, bool reset); \
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell, \
                               uint8_t* flag, cudaStream_t stream); \
 

@@ -29,6 +29,7 @@ namespace nt {
 enum Feature : int { F_HEX = 1, F_PLANE = 2, F_SPHERE = 4 };
 
 constexpr int kMaxDepth = 8;          // builder-enforced nesting limit (reading O7)
+constexpr int kBihStack = 12;         // BIH depth limit = register stack capacity (nt_geom.cuh)
 constexpr int kNC = 18;               // counters (NT_NC)
 constexpr double kFlagDist = 1e-10;   // O16 proximity / near-tie distance (cm)
 constexpr double kHexH = 0.8660254037844386;  // O9: nearest double to sqrt(3)/2

@@ -596,6 +596,16 @@ __global__ void k_selftest_arith(uint64_t n, uint64_t seed, unsigned long long* 
   }
 }
 
+cudaError_t bih_stats(unsigned long long* host4, bool reset) {
+#ifdef NT_BIH_STATS
+  if (reset) { unsigned long long z[4] = {0, 0, 0, 0}; return cudaMemcpyToSymbol(g_bih_stats, z, sizeof z); }
+  return cudaMemcpyFromSymbol(host4, g_bih_stats, 4 * sizeof(unsigned long long));
+#else
+  (void)host4; (void)reset;
+  return cudaErrorNotSupported;
+#endif
+}
+
 cudaError_t selftest_arith(uint64_t n, uint64_t seed, unsigned long long* d_bad) {
   k_selftest_arith<<<148 * 8, 256>>>(n, seed, d_bad);
   return cudaGetLastError();
