@@ -78,6 +78,13 @@ typedef enum { NT_TRACKER_GENERIC = 0, NT_TRACKER_RECT = 1 } nt_tracker;
  * compacted with warp ballots, so every warp runs one event type on 32 slots at a time.         */
 #define NT_HISTORY 2u        /* history-based persistent kernel: one history per thread            */
 #define NT_WARPQ 4u          /* event queues per warp (64 slots per warp, no block barriers)      */
+/* Dispatch of the tracking operations inside the block-queue scheduler (§4 methods):
+ * default SP (switch on the universe kind).  NT_DP: dynamic polymorphism, every
+ * find_cell / distance_to_boundary / array cross_surface is a virtual call on a per-universe
+ * tracker object built on the device; results are identical.  Needs the generic
+ * tracker, block queues (not NT_HISTORY / NT_WARPQ) and block_dim 0 or 256, else NT_E_ARG.
+ * ST (pseudo-array universes) is the build option nt_build_opts.pseudo_array.   */
+#define NT_DP 8u
 
 /* Per-particle flag bits written to outputs.pflags (reading O16):
  *   F1: a cell/tile chosen by a descent has another surface within 1e-10 cm

@@ -21,7 +21,9 @@ TRACKER = {"generic": 0, "rect": 1}
 NT_TRACE = 1
 NT_HISTORY = 2
 NT_WARPQ = 4
-SCHEDULERS = {"block": 0, "event": 0, "warp": NT_WARPQ, "history": NT_HISTORY}
+NT_DP = 8
+# "dp": block queues with dynamic-polymorphism dispatch (virtual tracker calls)
+SCHEDULERS = {"block": 0, "event": 0, "warp": NT_WARPQ, "history": NT_HISTORY, "dp": NT_DP}
 COUNTERS = ["particles", "segments", "crossings", "reflections", "leaks", "collisions",
             "absorptions", "lost", "capped", "flagged"] + [f"cross_l{i}" for i in range(8)]
 NC = len(COUNTERS)

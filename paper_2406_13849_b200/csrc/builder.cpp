@@ -131,6 +131,63 @@ Aabb truncate(const std::vector<HSurf>& S, const HCell& c, const Aabb& start) {
   return b;
 }
 
+// Tighter box for cells bounded by general planes (e.g. the hexagonal prisms of a pseudo-array
+// universe): the box of the polytope {truncated box} ∩ {plane half-spaces}, from its vertices.
+// Quadrics are only used through truncate(), so the result still contains the cell.  Falls
+// back to the truncated box when the enumeration finds nothing (empty or degenerate cell).
+Aabb polytope_box(const std::vector<HSurf>& S, const HCell& c, const Aabb& b) {
+  struct H { double n[3], d; };             // n.x <= d
+  std::vector<H> hs;
+  bool general = false;
+  for (size_t h = 0; h < c.sid.size(); ++h) {
+    const HSurf& s = S[c.sid[h]];
+    if (s.kind != S_PLANE) continue;
+    general = true;
+    const double g = c.sense[h] == 0 ? 1.0 : -1.0;
+    hs.push_back({{g * s.c[0], g * s.c[1], g * s.c[2]}, g * s.c[3]});
+  }
+  if (!general || !b.valid()) return b;
+  for (int a = 0; a < 3; ++a) {
+    H lo{{0, 0, 0}, -b.lo[a]}, hi{{0, 0, 0}, b.hi[a]};
+    lo.n[a] = -1.0;
+    hi.n[a] = 1.0;
+    hs.push_back(lo);
+    hs.push_back(hi);
+  }
+  double scale = 1.0;
+  for (int a = 0; a < 3; ++a) scale = std::max({scale, std::fabs(b.lo[a]), std::fabs(b.hi[a])});
+  Aabb r = Aabb::empty();
+  const size_t m = hs.size();
+  for (size_t i = 0; i < m; ++i)
+    for (size_t j = i + 1; j < m; ++j)
+      for (size_t k = j + 1; k < m; ++k) {
+        const double* A = hs[i].n; const double* B = hs[j].n; const double* C = hs[k].n;
+        const double bc[3] = {B[1] * C[2] - B[2] * C[1], B[2] * C[0] - B[0] * C[2], B[0] * C[1] - B[1] * C[0]};
+        const double ca[3] = {C[1] * A[2] - C[2] * A[1], C[2] * A[0] - C[0] * A[2], C[0] * A[1] - C[1] * A[0]};
+        const double ab[3] = {A[1] * B[2] - A[2] * B[1], A[2] * B[0] - A[0] * B[2], A[0] * B[1] - A[1] * B[0]};
+        const double det = A[0] * bc[0] + A[1] * bc[1] + A[2] * bc[2];
+        const double na = std::sqrt(A[0] * A[0] + A[1] * A[1] + A[2] * A[2]);
+        const double nb = std::sqrt(B[0] * B[0] + B[1] * B[1] + B[2] * B[2]);
+        const double nc = std::sqrt(C[0] * C[0] + C[1] * C[1] + C[2] * C[2]);
+        if (std::fabs(det) <= 1e-9 * na * nb * nc) continue;
+        double p[3];
+        for (int a = 0; a < 3; ++a) p[a] = (hs[i].d * bc[a] + hs[j].d * ca[a] + hs[k].d * ab[a]) / det;
+        bool in = true;
+        for (size_t q = 0; q < m && in; ++q) {
+          const double* n = hs[q].n;
+          const double nn = std::sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
+          in = n[0] * p[0] + n[1] * p[1] + n[2] * p[2] - hs[q].d <= 1e-9 * nn * scale;
+        }
+        if (in) r.grow(Aabb{{p[0], p[1], p[2]}, {p[0], p[1], p[2]}});
+      }
+  if (!r.valid()) return b;
+  for (int a = 0; a < 3; ++a) {          // never looser than the truncated box
+    r.lo[a] = std::max(r.lo[a], b.lo[a]);
+    r.hi[a] = std::min(r.hi[a], b.hi[a]);
+  }
+  return r.valid() ? r : b;
+}
+
 Aabb shift(const Aabb& b, const double t[3]) {
   Aabb r = b;
   for (int a = 0; a < 3; ++a) { r.lo[a] -= t[a]; r.hi[a] -= t[a]; }
@@ -160,7 +217,7 @@ std::vector<Aabb> universe_boxes(const std::vector<HSurf>& S, const std::vector<
   Aabb big{{-kBig, -kBig, -kBig}, {kBig, kBig, kBig}};
   if (U[root].kind == U_CSG) {
     for (int c : U[root].cells) {
-      Aabb a = truncate(S, C[c], big);
+      Aabb a = polytope_box(S, C[c], truncate(S, C[c], big));
       if (a.valid()) box[root].grow(a);
     }
   } else {
@@ -172,7 +229,7 @@ std::vector<Aabb> universe_boxes(const std::vector<HSurf>& S, const std::vector<
     if (X.kind == U_CSG) {
       for (int c : X.cells) {
         if (C[c].fill_kind != 1) continue;
-        Aabb a = truncate(S, C[c], box[u]);
+        Aabb a = polytope_box(S, C[c], truncate(S, C[c], box[u]));
         if (a.valid()) box[C[c].fill].grow(shift(a, C[c].tr));
       }
     } else {
@@ -507,7 +564,7 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
   for (int u = 0; u < (int)U.size(); ++u)
     if (U[u].kind == U_CSG)
       for (int c : U[u].cells) {
-        Aabb a = ubox[u].valid() ? truncate(S, C[c], ubox[u])
+        Aabb a = ubox[u].valid() ? polytope_box(S, C[c], truncate(S, C[c], ubox[u]))
                                  : Aabb{{-kBig, -kBig, -kBig}, {kBig, kBig, kBig}};
         if (!a.valid()) a = ubox[u].valid() ? ubox[u] : Aabb{{0, 0, 0}, {0, 0, 0}};
         cb[c] = pad(a);

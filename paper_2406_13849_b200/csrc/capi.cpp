@@ -50,6 +50,8 @@ struct nt_model {
   size_t host_scratch_len = 0;
   std::mutex host_mu;
   int last_launches = 0;
+  void* dp_objs = nullptr;                  // DP dispatch: tracker objects + pointer table (lazy)
+  std::mutex dp_mu;
 };
 
 // Coefficients of the spec'd transcendentals (reading R-T), computed with IEEE double ops.
@@ -87,13 +89,14 @@ nt_status nt_model_create(nt_model** out) {
 
 void nt_model_destroy(nt_model* m) {
   if (!m) return;
-  if (m->blob || m->counters || m->host_scratch_dev) {
+  if (m->blob || m->counters || m->host_scratch_dev || m->dp_objs) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(m->device);
     if (m->blob) cudaFree(m->blob);
     if (m->counters) cudaFree(m->counters);
     if (m->host_scratch_dev) cudaFree(m->host_scratch_dev);
+    if (m->dp_objs) cudaFree(m->dp_objs);
     cudaSetDevice(prev);
   }
   delete m;
@@ -372,6 +375,9 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   if (run->tracker == NT_TRACKER_GENERIC && !(run->flags & (NT_WARPQ | NT_HISTORY)) && block != 128 && block != 256)
     return err(NT_E_ARG, std::string(who) + ": the event scheduler needs block_dim 128 or 256");
   if (run->n > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": at most 2^32-1 histories per call");
+  const bool dp = (run->flags & NT_DP) != 0;
+  if (dp && (run->tracker != NT_TRACKER_GENERIC || (run->flags & (NT_WARPQ | NT_HISTORY)) || block != 256))
+    return err(NT_E_ARG, std::string(who) + ": NT_DP needs the generic tracker, block queues and block_dim 256");
   m->last_launches = 0;
   if (run->n == 0) return NT_OK;
   int prev = 0;
@@ -395,6 +401,27 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   R.counter = m->counters + slot;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e = cudaMemsetAsync(R.counter, 0, sizeof(unsigned long long), s);
+  DevGeom g = m->g;
+  if (e == cudaSuccess && dp) {
+    // one tracker object per universe, built once per model on its device (vtables of the
+    // feature-set module that runs the kernel)
+    const bool f0 = m->g.features == 0;
+    std::lock_guard<std::mutex> lk(m->dp_mu);
+    const size_t ob = f0 ? f0::dp_object_bytes() : f7::dp_object_bytes();
+    const size_t nu = (size_t)m->g.n_univ, tab_off = (nu * ob + 255) & ~size_t(255);
+    if (!m->dp_objs) {
+      e = cudaMalloc(&m->dp_objs, tab_off + nu * sizeof(void*));
+      if (e == cudaSuccess) {
+        char* base = static_cast<char*>(m->dp_objs);
+        e = f0 ? f0::dp_init(m->g, base, base + tab_off, s) : f7::dp_init(m->g, base, base + tab_off, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) { cudaFree(m->dp_objs); m->dp_objs = nullptr; }
+      } else {
+        m->dp_objs = nullptr;
+      }
+    }
+    if (e == cudaSuccess) g.trk = reinterpret_cast<const void* const*>(static_cast<char*>(m->dp_objs) + tab_off);
+  }
   int grid = 0;
   if (e == cudaSuccess) {
     const bool st = d_states != nullptr, f0 = m->g.features == 0;
@@ -407,8 +434,8 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
       e = f0 ? f0::launch_wq(m->g, R, trace, st, run->blocks_per_sm, s, &grid)
              : f7::launch_wq(m->g, R, trace, st, run->blocks_per_sm, s, &grid);
     else
-      e = f0 ? f0::launch_event(m->g, R, trace, st, block, run->blocks_per_sm, s, &grid)
-             : f7::launch_event(m->g, R, trace, st, block, run->blocks_per_sm, s, &grid);
+      e = f0 ? f0::launch_event(g, R, trace, st, block, run->blocks_per_sm, s, &grid)
+             : f7::launch_event(g, R, trace, st, block, run->blocks_per_sm, s, &grid);
   }
   if (prev != m->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_err(e, who);

@@ -53,7 +53,8 @@ size_t event_smem_bytes(const DevGeom& g, int B, bool trace) {
   return (s + 15) & ~size_t(15);
 }
 
-template <int B, bool TRACE, bool STATES>
+// DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh)
+template <int B, bool TRACE, bool STATES, bool DP = false>
 __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -212,28 +213,33 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
               Tx = st.T(l0, 0); Ty = st.T(l0, 1); Tz = st.T(l0, 2);
             } else {                                     // Alg. 6: tile +- 1 at level l0, then daughter
               const int j = fsid;
-              const DUniv* U = g.univ + st.u(l0);
-              const int uk = ld(&U->kind);
               int ta = st.a(l0), tb = st.b(l0), tc = st.c(l0);
-              if (!kHex || uk == U_RECT) {
-                const int dir = (j & 1) ? 1 : -1, ax = j >> 1;
-                if (ax == 0) ta += dir; else if (ax == 1) tb += dir; else tc += dir;
-              } else if (j < 6) {
-                ta += (j == 0 || j == 5) ? 1 : ((j == 2 || j == 3) ? -1 : 0);
-                tb += (j == 1 || j == 2) ? 1 : ((j == 4 || j == 5) ? -1 : 0);
+              double tx, ty, tz;
+              if constexpr (DP) {
+                du = get_tracker(g, st.u(l0))->next_tile(g, j, ta, tb, tc, tx, ty, tz);
               } else {
-                tc += (j == 7) ? 1 : -1;
+                const DUniv* U = g.univ + st.u(l0);
+                const int uk = ld(&U->kind);
+                if (!kHex || uk == U_RECT) {
+                  const int dir = (j & 1) ? 1 : -1, ax = j >> 1;
+                  if (ax == 0) ta += dir; else if (ax == 1) tb += dir; else tc += dir;
+                } else if (j < 6) {
+                  ta += (j == 0 || j == 5) ? 1 : ((j == 2 || j == 3) ? -1 : 0);
+                  tb += (j == 1 || j == 2) ? 1 : ((j == 4 || j == 5) ? -1 : 0);
+                } else {
+                  tc += (j == 7) ? 1 : -1;
+                }
+                du = array_daughter(g, U, uk, ta, tb, tc, tx, ty, tz);
               }
               st.a(l0) = ta; st.b(l0) = tb; st.c(l0) = tc;
-              double tx, ty, tz;
-              du = array_daughter(g, U, uk, ta, tb, tc, tx, ty, tz);
               Tx = st.T(l0, 0) + tx; Ty = st.T(l0, 1) + ty; Tz = st.T(l0, 2) + tz;
               l0 = l0 + 1;
               fsid = -1;
               fsense = 0;
             }
           }
-          ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
+          if constexpr (DP) ok = du >= 0 && descend_dp(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
+          else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
           done = true;
           if (!ok) flags |= NT_F3;
           sflags[slot] = static_cast<uint8_t>(flags);
@@ -280,7 +286,10 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
           } else {
             Best b;
             b.d = NT_INF; b.d2 = NT_INF; b.l = -1; b.j = -1; b.sense = 0;
-            for (int l = 0; l < L; ++l) level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+            for (int l = 0; l < L; ++l) {
+              if constexpr (DP) level_distances_dp(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+              else level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+            }
             const double sig = ld(g.mc_st + mc);
             const double ds = b.d;
             const double dc = sig > 0.0 ? fdiv(tau, sig) : NT_INF;

@@ -35,6 +35,8 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
                          int blocks_per_sm, cudaStream_t stream, int* grid_out); \
 cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, int blocks_per_sm, \
                       cudaStream_t stream, int* grid_out); \
+cudaError_t dp_init(const DevGeom& g, void* objs, void* tab, cudaStream_t stream); \
+size_t dp_object_bytes(); \
 cudaError_t selftest_arith(uint64_t n, uint64_t seed, unsigned long long* d_bad); \
 cudaError_t bih_stats(unsigned long long* host4, bool reset); \
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell, \

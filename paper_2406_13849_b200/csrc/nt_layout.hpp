@@ -86,6 +86,7 @@ struct DevGeom {
   const int32_t* mc_cell;     // per material cell: global cell id (trace)
   int32_t root, n_mc, max_depth, n_univ;
   int32_t n_cells, n_surf, root_kind, features;   // features: F_* bits present in the model
+  const void* const* trk;     // DP dispatch only: per-universe tracker object pointers (dp_tracker.cuh)
 };
 
 // Rect-specialised tracker tables (Alg. 9-10): root = axis box or concentric CZ annuli between a

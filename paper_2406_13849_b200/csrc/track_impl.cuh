@@ -397,6 +397,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
 }
 
 NT_DEV_END
+#include "dp_tracker.cuh"
 #include "event_kernel.cuh"
 #include "wq_kernel.cuh"
 #if NT_FEAT == 0
@@ -539,6 +540,11 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
       return cudaGetLastError();
     });
   };
+  if (g.trk) {                     // DP dispatch (virtual tracker calls), block 256 only
+    if (block != 256) return cudaErrorInvalidValue;
+    if (trace) return states ? go(k_track_event<256, true, true, true>) : go(k_track_event<256, true, false, true>);
+    return states ? go(k_track_event<256, false, true, true>) : go(k_track_event<256, false, false, true>);
+  }
   if (block == 128) {
     if (trace) return states ? go(k_track_event<128, true, true>) : go(k_track_event<128, true, false>);
     return states ? go(k_track_event<128, false, true>) : go(k_track_event<128, false, false>);
@@ -547,6 +553,14 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
   if (trace) return states ? go(k_track_event<256, true, true>) : go(k_track_event<256, true, false>);
   return states ? go(k_track_event<256, false, true>) : go(k_track_event<256, false, false>);
 }
+
+// DP: construct the per-universe tracker objects (objs: n_univ * kTrkBytes, tab: n_univ pointers)
+cudaError_t dp_init(const DevGeom& g, void* objs, void* tab, cudaStream_t stream) {
+  k_dp_init<<<(g.n_univ + 127) / 128, 128, 0, stream>>>(g, static_cast<unsigned char*>(objs),
+                                                         static_cast<const void**>(tab));
+  return cudaGetLastError();
+}
+size_t dp_object_bytes() { return kTrkBytes; }
 
 cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, int blocks_per_sm,
                       cudaStream_t stream, int* grid_out) {

@@ -68,7 +68,7 @@ def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, t
 CONFIG_N = {"c1": 2000, "c2": 600, "c3": 600, "c4": 600, "c5m": 600, "c5r": 600}
 
 
-@pytest.mark.parametrize("sched", ["warp", "block", "history"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp"])
 @pytest.mark.parametrize("cfg", list(CONFIG_N))
 def test_config_trace_parity(nt, orc, cfg, sched):
     """Every BASELINE config: full traces bit-exact vs the oracle (seeded, small batch), with
@@ -87,7 +87,8 @@ def test_c3_parity_seeds(nt, orc, seed):
 @pytest.mark.parametrize("name", ["sphere_in_box", "hex_pins_small_pointy", "hex_pins_small_flat",
                                   "rect3d_small", "lattice3_nested", "lattice3_flat", "infinite_medium",
                                   "c1_void_vacuum"])
-def test_test_models_parity(nt, orc, name):
+@pytest.mark.parametrize("sched", ["block", "dp"])
+def test_test_models_parity(nt, orc, name, sched):
     """Planes, spheres, 3-D rect and hex z-stacks, translations, void + vacuum leakage."""
     M = workloads.models
     spec = {"sphere_in_box": M.sphere_in_box, "hex_pins_small_pointy": lambda: M.hex_pins_small("pointy"),
@@ -95,7 +96,22 @@ def test_test_models_parity(nt, orc, name):
             "lattice3_nested": M.lattice3_nested, "lattice3_flat": lambda: M.lattice3_nested(True),
             "infinite_medium": M.infinite_medium,
             "c1_void_vacuum": lambda: M.c1_pincell(bc="vacuum", void=True)}[name]()
-    _compare(nt, orc, spec, 700, seed=2)
+    _compare(nt, orc, spec, 700, seed=2, scheduler=sched)
+
+
+def test_dp_dispatch_rejects_other_schedulers(nt):
+    """NT_DP is a dispatch mode of the block-queue scheduler only (nestrack.h)."""
+    spec, _ = workloads.config("c1")
+    m = nt.Model.from_spec(spec, device=0)
+    for kw in ({"block_dim": 128}, {"tracker": "rect"}):
+        with pytest.raises(nt.NtError):
+            m.track(10, seed=1, scheduler="dp", **kw)
+    run = m.make_run(10, 1, scheduler="history")
+    run.flags |= nt.NT_DP
+    out = torch.zeros(m.out_len, dtype=torch.float64, device="cuda")
+    o = nt.Outputs()
+    o.out = out.data_ptr()
+    assert m.L.nt_track(m.h, nt.C.byref(run), nt.C.byref(o), None) == -1
 
 
 @pytest.mark.parametrize("block", [128, 256])
@@ -107,7 +123,7 @@ def test_ragged_batches_and_large_pids(nt, orc, n, block):
     _compare(nt, orc, spec, n, seed=3, pid_begin=(1 << 33) + 17, scheduler="warp")
 
 
-@pytest.mark.parametrize("sched", ["warp", "block", "history"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp"])
 def test_capped_histories(nt, orc, sched):
     """max_segments reached -> CAPPED (F3) on both sides, same extra trace record."""
     spec, _ = workloads.config("c1")
@@ -115,7 +131,7 @@ def test_capped_histories(nt, orc, sched):
     assert g["counters"]["capped"] > 0
 
 
-@pytest.mark.parametrize("sched", ["warp", "block", "history"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp"])
 def test_lost_at_birth(nt, orc, sched):
     """Births outside every root cell are LOST at birth (source box larger than the model)."""
     spec = workloads.c1_pincell()
@@ -124,7 +140,7 @@ def test_lost_at_birth(nt, orc, sched):
     assert g["counters"]["lost"] > 0
 
 
-@pytest.mark.parametrize("sched", ["warp", "block", "history"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp"])
 def test_explicit_states(nt, orc, sched):
     """nt_track_states: explicit birth states (chord rays through the void pincell)."""
     spec = workloads.c1_pincell(bc="vacuum", void=True)
@@ -177,6 +193,23 @@ def test_pseudo_array_equals_generic(nt, cfg):
     assert len(ta) == len(tb)
     for f in ("pid", "seg", "kind", "level", "cell_before", "cell_after", "terminal", "s"):
         assert np.array_equal(ta[f], tb[f]), f
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5m"])
+def test_pseudo_hex_locates_same_cells(nt, cfg):
+    """ST mode on HEX lattices (hexagonal prisms of general planes, polytope AABBs): point
+    location gives the same material cell as the closed-form hex indexing.  Hex tiles are plane
+    cells here, so points within rounding of a tile edge may legitimately differ."""
+    spec, _ = workloads.config(cfg)
+    a = nt.Model.from_spec(spec, device=0)
+    b = nt.Model.from_spec(spec, device=0, pseudo_array=True)
+    rng = np.random.default_rng(3)
+    lo, hi = np.array(spec["source"]["lo"]), np.array(spec["source"]["hi"])
+    pts = torch.tensor(rng.uniform(lo, hi, size=(200000, 3)).T.copy(), device="cuda")
+    ca, fa = a.find_cells(pts)
+    cb, fb = b.find_cells(pts)
+    assert int((fb != 0).sum()) == int((fa != 0).sum())
+    assert int((ca != cb).sum()) <= 2
 
 
 def test_host_entry_point(nt):
