@@ -162,6 +162,18 @@ nt_status nt_add_rect_array(nt_model* m, const double lower_left[3], const doubl
                             const int32_t shape[3], const int32_t* fill, int32_t outer_uid,
                             int32_t* uid);
 
+/* Non-uniform rectilinear array (Alg. 5 find_cell by binary search over the mesh divisions,
+ * P:513-525; non-uniform spacing for inter-assembly gaps; reading N1).
+ * edges: n_edges[0] x divisions, then n_edges[1] y, then n_edges[2] z, each strictly
+ * increasing and finite (copied); n_edges[2] == 0 makes the array 2-D (infinite in z).  Tile
+ * (i, j, k) spans [e_i, e_i+1) per axis; points below the first / at or above the last division
+ * lie in the outer slabs (index -1 / n), which take `outer_uid`.  Daughters are placed at the
+ * tile centre (e_i + e_i+1) * 0.5 (slabs: at the division they touch).  fill: x fastest.
+ * NT_E_GEOMETRY for fewer than 2 edges on an axis or non-increasing edges (at nt_finalize).
+ * Not rect-specialisable (NT_TRACKER_RECT rejects the model). */
+nt_status nt_add_rect_edges(nt_model* m, const double* edges, const int32_t n_edges[3],
+                            const int32_t* fill, int32_t outer_uid, int32_t* uid);
+
 /* Hexagonal array universe (Fig. 3; indexing omitted by the paper, P:444-448 — DESIGN.md
  * reading O9).  Axial (q, r), pitch = flat-to-flat distance, rings >= 1 (1 + 3 rings(rings-1)
  * tiles).  fill order: r ascending, then q ascending over max(|q|,|r|,|q+r|) <= rings-1;

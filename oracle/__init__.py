@@ -58,6 +58,7 @@ def lib():
         L.orc_add_csg_universe.argtypes = [vp]
         L.orc_add_cell.argtypes = [vp, i32, dp, i32, i32, i32, dp]
         L.orc_add_rect.argtypes = [vp, dp, dp, dp, dp, i32]
+        L.orc_add_rect_edges.argtypes = [vp, dp, dp, dp, i32]
         L.orc_add_hex.argtypes = [vp, i32, dp, C.c_double, i32, C.c_double, C.c_double, i32, dp, i32]
         L.orc_set_root.argtypes = [vp, i32]
         L.orc_finalize.argtypes = [vp]
@@ -153,6 +154,12 @@ class OracleModel:
                     r = L.orc_add_cell(m.h, uid, _p(hs), len(hs), fk, f,
                                        _p(tr) if tr is not None else None)
                     assert r >= 0
+            elif u["kind"] == "rect" and "edges" in u:
+                e = np.asarray([v for ax in u["edges"] for v in ax], dtype=np.float64)
+                ne = np.asarray([len(ax) for ax in u["edges"]], dtype=np.int32)
+                fl = np.asarray(u["fill"], dtype=np.int32)
+                if L.orc_add_rect_edges(m.h, _p(e), _p(ne), _p(fl), u["outer"]) < 0:
+                    raise ValueError("oracle: bad rect edges")
             elif u["kind"] == "rect":
                 ll = np.asarray(u["ll"], dtype=np.float64)
                 p = np.asarray(u["pitch"], dtype=np.float64)

@@ -16,6 +16,9 @@
  *     explicit search (Alg. 5; hex reading O9);
  *   - distance to boundary: the minimum over every half-space of every
  *     level's current cell, plus the tile walls (Table 1).
+ *   - non-uniform rect arrays (Alg. 5, P:513-525 and its footnote P:500-505):
+ *     the tile is found by a linear scan over the mesh divisions (reading N1
+ *     in DESIGN.md: index -1 below the first edge, n at or above the last).
  * Everything else follows Alg. 2 step by step: tau bookkeeping
  * (P:391-398), move/cross (Alg. 8; Alg. 6), collision
  * (P:399-409).
@@ -69,9 +72,10 @@ typedef struct {
     int kind;
     /* CSG */
     int ncells, cap, *cells;
-    /* RECT (O8) */
+    /* RECT (O8); non-uniform (N1): e[a] = n[a]+1 increasing edges per axis, else NULL */
     double ll[3], p[3];
     int n[3], is2d;
+    double *e[3];
     /* HEX (O9) */
     int orient, rings, nz;
     double C[2], pitch, pH, zlo, zp;
@@ -96,7 +100,10 @@ void orc_model_free(void *vm) {
     Model *m = vm;
     if (!m) return;
     for (int i = 0; i < m->nc; ++i) { free(m->c[i].sid); free(m->c[i].sense); }
-    for (int i = 0; i < m->nu; ++i) { free(m->u[i].cells); free(m->u[i].fill); free(m->u[i].hexmap); }
+    for (int i = 0; i < m->nu; ++i) {
+        free(m->u[i].cells); free(m->u[i].fill); free(m->u[i].hexmap);
+        for (int a = 0; a < 3; ++a) free(m->u[i].e[a]);
+    }
     free(m->s); free(m->m); free(m->c); free(m->u); free(m->mc_cell); free(m);
 }
 
@@ -170,6 +177,38 @@ int orc_add_rect(void *vm, const double *ll, const double *p, const int *shape, 
     for (int i = 0; i < 3; ++i) { u->ll[i] = ll[i]; u->p[i] = p[i]; u->n[i] = shape[i]; }
     u->is2d = p[2] == 0.0;
     if (u->is2d) u->n[2] = 1;
+    u->nfill = u->n[0] * u->n[1] * u->n[2];
+    u->fill = malloc(sizeof(int) * (size_t)u->nfill);
+    memcpy(u->fill, fill, sizeof(int) * (size_t)u->nfill);
+    u->outer = outer;
+    return id;
+}
+
+/* Non-uniform rect array (Alg. 5 binary-search lattices): ne[a] edges per axis
+ * (ne[2] == 0: 2-D), concatenated x, y, z in `edges`, strictly increasing.  Returns -1 on bad
+ * edges. */
+int orc_add_rect_edges(void *vm, const double *edges, const int *ne, const int *fill, int outer) {
+    Model *m = vm;
+    if (ne[0] < 2 || ne[1] < 2 || (ne[2] != 0 && ne[2] < 2)) return -1;
+    int off = 0;
+    for (int a = 0; a < 3; ++a) {
+        for (int i = 1; i < ne[a]; ++i)
+            if (!(edges[off + i - 1] < edges[off + i]) || !isfinite(edges[off + i])) return -1;
+        off += ne[a];
+    }
+    int id = new_univ(m, U_RECT);
+    Univ *u = &m->u[id];
+    off = 0;
+    for (int a = 0; a < 3; ++a) {
+        u->n[a] = ne[a] > 0 ? ne[a] - 1 : 1;
+        u->ll[a] = 0.0; u->p[a] = 0.0;
+        if (ne[a] > 0) {
+            u->e[a] = malloc(sizeof(double) * (size_t)ne[a]);
+            memcpy(u->e[a], edges + off, sizeof(double) * (size_t)ne[a]);
+        }
+        off += ne[a];
+    }
+    u->is2d = ne[2] == 0;
     u->nfill = u->n[0] * u->n[1] * u->n[2];
     u->fill = malloc(sizeof(int) * (size_t)u->nfill);
     memcpy(u->fill, fill, sizeof(int) * (size_t)u->nfill);
@@ -505,6 +544,37 @@ static int rect_axis_index(double ll, double p, double x) {
     while (!(x < edge(ll, p, i + 1))) i++;
     return i;
 }
+static int rect_axis_index_u(const Univ *U, int a, double x) { return rect_axis_index(U->ll[a], U->p[a], x); }
+
+/* Reading N1, non-uniform axis with edges e[0..n]: tile i spans [E(i), E(i+1)) with
+ * E(i) = e[i] for 0 <= i <= n, E(-1) = -inf, E(n+1) = +inf; so tile -1 is the slab below e[0]
+ * and tile n the slab at or above e[n] (both `outer`).  Tile centre (the daughter translation):
+ * (e[i] + e[i+1]) * 0.5 inside, e[0] for tile -1, e[n] for tile n. */
+static double nu_edge(const Univ *U, int a, int i) {
+    if (i < 0) return -INFINITY;
+    if (i > U->n[a]) return INFINITY;
+    return U->e[a][i];
+}
+static int nu_index(const Univ *U, int a, double x) {
+    for (int i = -1; i <= U->n[a]; ++i)                    /* linear scan: the definition */
+        if (nu_edge(U, a, i) <= x && x < nu_edge(U, a, i + 1)) return i;
+    return U->n[a];                                         /* not reached for finite x */
+}
+static double nu_centre(const Univ *U, int a, int i) {
+    if (i < 0) return U->e[a][0];
+    if (i >= U->n[a]) return U->e[a][U->n[a]];
+    return (U->e[a][i] + U->e[a][i + 1]) * 0.5;
+}
+/* tile edge / centre of rect axis a, uniform or not */
+static double tile_edge(const Univ *U, int a, int i) {
+    return U->e[a] ? nu_edge(U, a, i) : edge(U->ll[a], U->p[a], i);
+}
+static int tile_index(const Univ *U, int a, double x) {
+    return U->e[a] ? nu_index(U, a, x) : rect_axis_index_u(U, a, x);
+}
+static double tile_centre(const Univ *U, int a, int i) {
+    return U->e[a] ? nu_centre(U, a, i) : U->ll[a] + ((double)i + 0.5) * U->p[a];
+}
 
 /* hex t-space (O9) */
 static void hex_t(const Univ *U, const double rl[3], double t[3]) {
@@ -562,16 +632,16 @@ static int locate(const Model *m, int u, const double rl[3], int fsid, int fsens
         int ijk[3] = {0, 0, 0};
         int na = U->is2d ? 2 : 3;
         for (int a = 0; a < na; ++a) {
-            ijk[a] = rect_axis_index(U->ll[a], U->p[a], rl[a]);
-            if (fabs(rl[a] - edge(U->ll[a], U->p[a], ijk[a])) <= FLAG_DIST ||
-                fabs(rl[a] - edge(U->ll[a], U->p[a], ijk[a] + 1)) <= FLAG_DIST) *near |= F1;
+            ijk[a] = tile_index(U, a, rl[a]);
+            if (fabs(rl[a] - tile_edge(U, a, ijk[a])) <= FLAG_DIST ||
+                fabs(rl[a] - tile_edge(U, a, ijk[a] + 1)) <= FLAG_DIST) *near |= F1;
         }
         L->i = ijk[0]; L->j = ijk[1]; L->k = ijk[2];
         int in = 1;
         for (int a = 0; a < na; ++a) if (ijk[a] < 0 || ijk[a] >= U->n[a]) in = 0;
         idx = in ? ijk[0] + U->n[0] * (ijk[1] + U->n[1] * ijk[2]) : -1;
         for (int a = 0; a < 3; ++a)
-            o->t[a] = (a < na) ? U->ll[a] + ((double)ijk[a] + 0.5) * U->p[a] : 0.0;
+            o->t[a] = (a < na) ? tile_centre(U, a, ijk[a]) : 0.0;
     } else {
         double t[3];
         hex_t(U, rl, t);
@@ -656,9 +726,9 @@ static void level_distances(const Model *m, const Level *L, int l, const double 
         int na = U->is2d ? 2 : 3;
         for (int a = 0; a < na; ++a) {
             double u = om[a], d;
-            if (u > 0.0) d = (edge(U->ll[a], U->p[a], ijk[a] + 1) - rl[a]) / u;
-            else if (u < 0.0) d = (edge(U->ll[a], U->p[a], ijk[a]) - rl[a]) / u;
-            else continue;
+            const double e = u > 0.0 ? tile_edge(U, a, ijk[a] + 1) : tile_edge(U, a, ijk[a]);
+            if (u == 0.0 || isinf(e)) continue;              /* no wall that way (N1 slabs) */
+            d = (e - rl[a]) / u;
             if (ev) ev[E_RECT]++;
             consider(b, clamp0(d), l, 2 * a + (u > 0.0));
         }
@@ -820,7 +890,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
                         for (int a = 0; a < na; ++a) if (ijk[a] < 0 || ijk[a] >= U->n[a]) in = 0;
                         idx = in ? ijk[0] + U->n[0] * (ijk[1] + U->n[1] * ijk[2]) : -1;
                         for (int a = 0; a < 3; ++a)
-                            t[a] = (a < na) ? U->ll[a] + ((double)ijk[a] + 0.5) * U->p[a] : 0.0;
+                            t[a] = (a < na) ? tile_centre(U, a, ijk[a]) : 0.0;
                     } else {
                         int q = Lv->i, rr = Lv->j, kz = Lv->k;
                         int R = U->rings - 1, W = 2 * R + 1;

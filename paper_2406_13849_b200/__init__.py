@@ -69,7 +69,7 @@ class Outputs(C.Structure):
 _lib = None
 
 SYMBOLS = ["nt_last_error", "nt_abi_version", "nt_model_create", "nt_model_destroy", "nt_add_surface",
-           "nt_add_material", "nt_add_csg_universe", "nt_add_cell", "nt_add_rect_array",
+           "nt_add_material", "nt_add_csg_universe", "nt_add_cell", "nt_add_rect_array", "nt_add_rect_edges",
            "nt_add_hex_array", "nt_set_root", "nt_build_opts_default", "nt_finalize",
            "nt_model_info_get", "nt_material_cell_ids", "nt_bih_info", "nt_track",
            "nt_track_states", "nt_track_host", "nt_find_cells", "nt_last_launch_count",
@@ -92,6 +92,7 @@ def lib():
         L.nt_add_csg_universe.argtypes = [vp, C.POINTER(i32)]
         L.nt_add_cell.argtypes = [vp, i32, dp, i32, i32, i32, dp, C.POINTER(i32)]
         L.nt_add_rect_array.argtypes = [vp, dp, dp, dp, dp, i32, C.POINTER(i32)]
+        L.nt_add_rect_edges.argtypes = [vp, dp, dp, dp, i32, C.POINTER(i32)]
         L.nt_add_hex_array.argtypes = [vp, i32, dp, C.c_double, i32, C.c_double, C.c_double, i32, dp,
                                        i32, C.POINTER(i32)]
         L.nt_set_root.argtypes = [vp, i32]
@@ -179,6 +180,15 @@ class Model:
         _check(self.L.nt_add_rect_array(self.h, _p(a), _p(p), _p(s), _p(f), outer, C.byref(i)))
         return i.value
 
+    def add_rect_edges(self, edges, fill, outer: int = -1) -> int:
+        """Non-uniform rect array: edges = [ex, ey, ez] (ez empty: 2-D)."""
+        e = np.asarray([v for ax in edges for v in ax], dtype=np.float64)
+        ne = np.asarray([len(ax) for ax in edges], dtype=np.int32)
+        f = np.asarray(fill, dtype=np.int32)
+        i = C.c_int32()
+        _check(self.L.nt_add_rect_edges(self.h, _p(e), _p(ne), _p(f), outer, C.byref(i)))
+        return i.value
+
     def add_hex_array(self, orient: str, center, pitch: float, rings: int, fill, outer: int = -1,
                       z_lower: float = 0.0, z_pitch: float = 0.0, nz: int = 0) -> int:
         c = np.asarray(center, dtype=np.float64)
@@ -227,6 +237,8 @@ class Model:
                         m.add_cell(uid, c["hs"], material=c["material"])
                     else:
                         m.add_cell(uid, c["hs"], fill=c["fill"], translation=c.get("translation"))
+            elif u["kind"] == "rect" and "edges" in u:
+                m.add_rect_edges(u["edges"], u["fill"], u["outer"])
             elif u["kind"] == "rect":
                 m.add_rect_array(u["ll"], u["pitch"], u["shape"], u["fill"], u["outer"])
             else:

@@ -85,7 +85,14 @@ void validate(const std::vector<HSurf>& S, const std::vector<HMat>& M, const std
   }
   for (int i = 0; i < nu; ++i) {
     const HUniv& u = U[i];
-    if (u.kind == U_RECT) {
+    if (u.kind == U_RECT && !u.e[0].empty()) {
+      for (int a = 0; a < (u.is2d ? 2 : 3); ++a) {
+        if ((int)u.e[a].size() != u.n[a] + 1 || u.n[a] < 1) fail("rect array %ld: bad edge count", i);
+        for (size_t k = 0; k < u.e[a].size(); ++k)
+          if (!finite(u.e[a][k]) || (k && !(u.e[a][k - 1] < u.e[a][k])))
+            fail("rect array %ld: edges must be finite and strictly increasing", i);
+      }
+    } else if (u.kind == U_RECT) {
       if (!(u.p[0] > 0) || !(u.p[1] > 0) || u.p[2] < 0) fail("rect array %ld: bad pitch", i);
       for (int a = 0; a < 3; ++a) {
         if (u.n[a] < 1) fail("rect array %ld: bad shape", i);
@@ -234,7 +241,21 @@ std::vector<Aabb> universe_boxes(const std::vector<HSurf>& S, const std::vector<
       }
     } else {
       Aabb t;
-      if (X.kind == U_RECT) {
+      if (X.kind == U_RECT && !X.e[0].empty()) {
+        // N1: in-lattice daughters see at most half the widest tile; the outer universe fills
+        // the half-infinite slabs (handled below)
+        for (int a = 0; a < 3; ++a) {
+          double w = 0.0;
+          if (a < 3 && !X.e[a].empty())
+            for (size_t k = 1; k < X.e[a].size(); ++k) w = std::max(w, X.e[a][k] - X.e[a][k - 1]);
+          t.lo[a] = -0.5 * w * (1.0 + 1e-9);
+          t.hi[a] = 0.5 * w * (1.0 + 1e-9);
+        }
+        if (X.is2d) { t.lo[2] = box[u].lo[2]; t.hi[2] = box[u].hi[2]; }
+        for (int f : X.fill) box[f].grow(t);
+        if (X.outer >= 0) box[X.outer].grow(Aabb{{-kBig, -kBig, -kBig}, {kBig, kBig, kBig}});
+        continue;
+      } else if (X.kind == U_RECT) {
         for (int a = 0; a < 3; ++a) { t.lo[a] = -0.5 * X.p[a]; t.hi[a] = 0.5 * X.p[a]; }
         if (X.is2d) { t.lo[2] = box[u].lo[2]; t.hi[2] = box[u].hi[2]; }
       } else {
@@ -350,7 +371,44 @@ void convert_pseudo_arrays(std::vector<HSurf>& S, std::vector<HCell>& C, std::ve
   for (int u = 0; u < (int)U.size(); ++u) {
     HUniv& X = U[u];
     if (X.kind == U_CSG || !box[u].valid()) continue;
-    if (X.kind == U_RECT) {
+    if (X.kind == U_RECT && !X.e[0].empty()) {
+      // N1: every tile -1..n per axis; the slabs -1 / n are bounded on one side only
+      const int na = X.is2d ? 2 : 3;
+      std::vector<int> plane[3];
+      for (int a = 0; a < na; ++a)
+        for (double v : X.e[a]) {
+          plane[a].push_back((int)S.size());
+          S.push_back(HSurf{a, 0, {v, 0, 0, 0}});
+        }
+      HUniv Y;
+      Y.kind = U_CSG;
+      const int hk = na == 3 ? X.n[2] : 0, lk = na == 3 ? -1 : 0;
+      for (int k = lk; k <= hk; ++k)
+        for (int j = -1; j <= X.n[1]; ++j)
+          for (int i = -1; i <= X.n[0]; ++i) {
+            const int ijk[3] = {i, j, k};
+            bool in = true;
+            for (int a = 0; a < na; ++a) in = in && ijk[a] >= 0 && ijk[a] < X.n[a];
+            const int d = in ? X.fill[i + X.n[0] * (j + X.n[1] * (na == 3 ? k : 0))] : X.outer;
+            if (d < 0) continue;
+            HCell c;
+            c.uid = u;
+            c.fill_kind = 1;
+            c.fill = d;
+            for (int a = 0; a < 3; ++a) {
+              if (a >= na) { c.tr[a] = 0.0; continue; }
+              const int n = X.n[a], t = ijk[a];
+              c.tr[a] = t < 0 ? X.e[a][0] : t >= n ? X.e[a][n] : (X.e[a][t] + X.e[a][t + 1]) * 0.5;
+            }
+            for (int a = 0; a < na; ++a) {
+              if (ijk[a] >= 0) { c.sid.push_back(plane[a][ijk[a]]); c.sense.push_back(1); }
+              if (ijk[a] < X.n[a]) { c.sid.push_back(plane[a][ijk[a] + 1]); c.sense.push_back(0); }
+            }
+            Y.cells.push_back((int)C.size());
+            C.push_back(c);
+          }
+      X = Y;
+    } else if (X.kind == U_RECT) {
       const int na = X.is2d ? 2 : 3;
       int lo[3] = {0, 0, 0}, hi[3] = {0, 0, 0};
       std::vector<int> plane0[3];
@@ -527,7 +585,10 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
     if (s.kind == S_PLANE) F.features |= F_PLANE;
     if (s.kind == S_SPHERE) F.features |= F_SPHERE;
   }
-  for (const HUniv& u : U) if (u.kind == U_HEX) F.features |= F_HEX;
+  for (const HUniv& u : U) {
+    if (u.kind == U_HEX) F.features |= F_HEX;
+    if (u.kind == U_RECT && !u.e[0].empty()) F.features |= F_RECTNU;
+  }
   // surfaces
   for (const HSurf& s : S) {
     DSurf d{};
@@ -591,6 +652,11 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
       d.i0 = X.n[0]; d.i1 = X.n[1]; d.i2 = X.is2d ? 1 : X.n[2];
       d.is2d = X.is2d;
       for (int a = 0; a < 3; ++a) { d.d[a] = X.ll[a]; d.d[3 + a] = X.p[a]; }
+      d.ntile = -1;
+      if (!X.e[0].empty()) {                       // N1 edge table: x, y, z (z only in 3-D)
+        d.ntile = (int32_t)F.edges.size();
+        for (int a = 0; a < (X.is2d ? 2 : 3); ++a) F.edges.insert(F.edges.end(), X.e[a].begin(), X.e[a].end());
+      }
       for (int f : X.fill) F.fills.push_back(f);
     } else {
       const double H = kHexH, p = X.pitch;
@@ -624,6 +690,7 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
   if (F.bih.empty()) F.bih.push_back({});
   if (F.bih_leaf.empty()) F.bih_leaf.push_back(0);
   if (F.fills.empty()) F.fills.push_back(-1);
+  if (F.edges.empty()) F.edges.push_back(0.0);
   if (F.hs.empty()) F.hs.push_back(0);
   if (F.mc_st.empty()) fail("model has no material cells");
 }

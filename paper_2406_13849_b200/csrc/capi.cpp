@@ -179,6 +179,30 @@ nt_status nt_add_rect_array(nt_model* m, const double ll[3], const double p[3], 
   return NT_OK;
 }
 
+nt_status nt_add_rect_edges(nt_model* m, const double* edges, const int32_t n_edges[3], const int32_t* fill,
+                            int32_t outer, int32_t* uid) {
+  CHECK_BUILDER(m);
+  if (!edges || !n_edges || !fill) return err(NT_E_ARG, "nt_add_rect_edges: NULL argument");
+  HUniv u;
+  u.kind = U_RECT;
+  u.is2d = n_edges[2] == 0;
+  long off = 0;
+  for (int a = 0; a < 3; ++a) {
+    if (n_edges[a] < 0 || n_edges[a] > (1 << 20) || (a < 2 && n_edges[a] < 2) || (a == 2 && n_edges[a] == 1))
+      return err(NT_E_GEOMETRY, "nt_add_rect_edges: need >= 2 edges per axis (z: 0 for 2-D)");
+    u.e[a].assign(edges + off, edges + off + n_edges[a]);
+    off += n_edges[a];
+    u.n[a] = n_edges[a] > 0 ? n_edges[a] - 1 : 1;
+    u.ll[a] = n_edges[a] > 0 ? edges[off - n_edges[a]] : 0.0;
+  }
+  const long n = (long)u.n[0] * u.n[1] * u.n[2];
+  u.fill.assign(fill, fill + n);
+  u.outer = outer;
+  m->u.push_back(u);
+  if (uid) *uid = (int32_t)m->u.size() - 1;
+  return NT_OK;
+}
+
 nt_status nt_add_hex_array(nt_model* m, nt_hex_orient orient, const double center[2], double pitch,
                            int32_t rings, double zlo, double zp, int32_t nz, const int32_t* fill,
                            int32_t outer, int32_t* uid) {
@@ -246,7 +270,8 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
                o_hs = place(blob, F.hs), o_chs = place(blob, F.cell_hs), o_cf = place(blob, F.cell_fill),
                o_ctr = place(blob, F.cell_tr), o_univ = place(blob, F.univ), o_bih = place(blob, F.bih),
                o_leaf = place(blob, F.bih_leaf), o_fills = place(blob, F.fills), o_st = place(blob, F.mc_st),
-               o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell);
+               o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell),
+               o_edges = place(blob, F.edges);
   const size_t o_pou = place(blob, F.r_pin_of_univ), o_poff = place(blob, F.r_pin_off),
                o_psid = place(blob, F.r_pin_sid), o_pmc = place(blob, F.r_pin_mc);
   m->blob_bytes = blob.size();
@@ -283,6 +308,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     g.mc_st = (const double*)(b + o_st);
     g.mc_pabs = (const double*)(b + o_pabs);
     g.mc_cell = (const int32_t*)(b + o_mcc);
+    g.edges = (const double*)(b + o_edges);
     m->rg = F.rg;
     m->rg.pin_of_univ = (const int32_t*)(b + o_pou);
     m->rg.pin_off = (const int32_t*)(b + o_poff);

@@ -67,24 +67,14 @@ struct CsgTracker final : UnivTracker {
 struct RectTracker final : UnivTracker {
   __device__ int find_cell(const DevGeom& g, double x, double y, double z, int, int, int& ia, int& ib, int& ic,
                            double& tx, double& ty, double& tz, uint32_t& flags) const override {
-    const double llx = ld(&U->d[0]), lly = ld(&U->d[1]), px = ld(&U->d[3]), py = ld(&U->d[4]);
-    const int i = rect_index(llx, px, x), j = rect_index(lly, py, y);
-    uint32_t nb = near_wall(llx, px, i, x) | near_wall(lly, py, j, y);
-    int k = 0;
-    if (!ld(&U->is2d)) {
-      const double llz = ld(&U->d[2]), pz = ld(&U->d[5]);
-      k = rect_index(llz, pz, z);
-      nb |= near_wall(llz, pz, k, z);
-    }
-    flags |= nb;
+    int i, j, k;
+    rect_locate(g, U, x, y, z, i, j, k, flags);
     ia = i; ib = j; ic = k;
     return array_daughter(g, U, U_RECT, i, j, k, tx, ty, tz);
   }
-  __device__ void distance(const DevGeom&, int ia, int ib, int ic, int l, double x, double y, double z, double u,
-                           double v, double w, int, int, Best& b) const override {
-    if (u != 0.0) b.consider(rect_wall(ld(&U->d[0]), ld(&U->d[3]), ia, x, u), l, u > 0.0 ? 1 : 0, 0);
-    if (v != 0.0) b.consider(rect_wall(ld(&U->d[1]), ld(&U->d[4]), ib, y, v), l, v > 0.0 ? 3 : 2, 0);
-    if (!ld(&U->is2d) && w != 0.0) b.consider(rect_wall(ld(&U->d[2]), ld(&U->d[5]), ic, z, w), l, w > 0.0 ? 5 : 4, 0);
+  __device__ void distance(const DevGeom& g, int ia, int ib, int ic, int l, double x, double y, double z,
+                           double u, double v, double w, int, int, Best& b) const override {
+    rect_candidates(g, U, ia, ib, ic, l, x, y, z, u, v, w, b);
   }
   __device__ int next_tile(const DevGeom& g, int j, int& ta, int& tb, int& tc, double& tx, double& ty,
                            double& tz) const override {

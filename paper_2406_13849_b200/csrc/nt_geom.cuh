@@ -16,6 +16,7 @@ NT_DEV_BEGIN
 constexpr bool kHex = (NT_FEAT & F_HEX) != 0;
 constexpr bool kPlane = (NT_FEAT & F_PLANE) != 0;
 constexpr bool kSphere = (NT_FEAT & F_SPHERE) != 0;
+constexpr bool kRectNU = (NT_FEAT & F_RECTNU) != 0;
 
 template <class T>
 __device__ __forceinline__ T ld(const T* p) { return __ldg(p); }
@@ -197,9 +198,119 @@ __device__ __forceinline__ bool near_wall(double ll, double p, int i, double x) 
          fabs(x - (ll + static_cast<double>(i + 1) * p)) <= kFlagDist;
 }
 
-// tile centre of an array (the daughter translation, readings O8/O9).  rect (i,j,k), hex (q,r,kz).
-__device__ __forceinline__ void array_centre(const DUniv* U, int kind, int a, int b, int c, double& tx,
-                                             double& ty, double& tz) {
+// Distance-to-boundary bookkeeping: strict '<' keeps the top-most level / lowest id on exact
+// ties (O13); d2 = smallest other candidate (O16 F2).
+struct Best {
+  double d, d2;
+  int l, j, sense;
+  __device__ __forceinline__ void consider(double dd, int ll, int jj, int ss) {
+    const bool lt = dd < d;                       // branch-free select form
+    d2 = lt ? d : (dd < d2 ? dd : d2);
+    d = lt ? dd : d;
+    l = lt ? ll : l;
+    j = lt ? jj : j;
+    sense = lt ? ss : sense;
+  }
+};
+
+// ---- non-uniform rect arrays (reading N1; Alg. 5 binary search over the mesh divisions,
+// P:500-525).  Axis divisions e[0..n]; tile -1 is the slab below e[0], tile n the slab at or
+// above e[n] (both `outer`); the slabs have no wall on their open side.
+__device__ __forceinline__ int nu_index(const double* e, int n, double x) {
+  if (x < ld(e)) return -1;
+  if (!(x < ld(e + n))) return n;
+  int lo = 0, hi = n;                                   // e[lo] <= x < e[hi]
+#pragma unroll 1
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (ld(e + mid) <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ bool nu_near(const double* e, int n, int i, double x) {
+  return (i >= 0 && fabs(x - ld(e + i)) <= kFlagDist) || (i + 1 <= n && fabs(x - ld(e + i + 1)) <= kFlagDist);
+}
+__device__ __forceinline__ double nu_wall(const double* e, int n, int i, double x, double u) {
+  const int k = u > 0.0 ? i + 1 : i;
+  if (k < 0 || k > n) return NT_INF;
+  return clamp0(fdiv(ld(e + k) - x, u));
+}
+__device__ __forceinline__ double nu_centre(const double* e, int n, int i) {
+  if (i < 0) return ld(e);
+  if (i >= n) return ld(e + n);
+  return (ld(e + i) + ld(e + i + 1)) * 0.5;
+}
+
+// Alg. 5 find_cell at a rect level: tile (i, j, k) of the local point, F1 proximity flags
+__device__ __forceinline__ void rect_locate(const DevGeom& g, const DUniv* U, double x, double y, double z,
+                                            int& i, int& j, int& k, uint32_t& flags) {
+  const int is2d = ld(&U->is2d);
+  if (kRectNU) {
+    const int eo = ld(&U->ntile);
+    if (eo >= 0) {
+      const int n0 = ld(&U->i0), n1 = ld(&U->i1);
+      const double* ex = g.edges + eo;
+      const double* ey = ex + n0 + 1;
+      i = nu_index(ex, n0, x);
+      j = nu_index(ey, n1, y);
+      k = 0;
+      uint32_t nb = nu_near(ex, n0, i, x) | nu_near(ey, n1, j, y);
+      if (!is2d) {
+        const int n2 = ld(&U->i2);
+        const double* ez = ey + n1 + 1;
+        k = nu_index(ez, n2, z);
+        nb |= nu_near(ez, n2, k, z);
+      }
+      flags |= nb;
+      return;
+    }
+  }
+  const double llx = ld(&U->d[0]), lly = ld(&U->d[1]), px = ld(&U->d[3]), py = ld(&U->d[4]);
+  i = rect_index(llx, px, x);
+  j = rect_index(lly, py, y);
+  uint32_t nb = near_wall(llx, px, i, x) | near_wall(lly, py, j, y);
+  k = 0;
+  if (!is2d) {
+    const double llz = ld(&U->d[2]), pz = ld(&U->d[5]);
+    k = rect_index(llz, pz, z);
+    nb |= near_wall(llz, pz, k, z);
+  }
+  flags |= nb;
+}
+
+// distance_to_boundary candidates of rect tile (ia, ib, ic) at level l (forward walls, O11)
+__device__ __forceinline__ void rect_candidates(const DevGeom& g, const DUniv* U, int ia, int ib, int ic, int l,
+                                                double x, double y, double z, double u, double v, double w,
+                                                Best& b) {
+  if (kRectNU) {
+    const int eo = ld(&U->ntile);
+    if (eo >= 0) {
+      const int n0 = ld(&U->i0), n1 = ld(&U->i1);
+      const double* ex = g.edges + eo;
+      const double* ey = ex + n0 + 1;
+      if (u != 0.0) b.consider(nu_wall(ex, n0, ia, x, u), l, u > 0.0 ? 1 : 0, 0);
+      if (v != 0.0) b.consider(nu_wall(ey, n1, ib, y, v), l, v > 0.0 ? 3 : 2, 0);
+      if (!ld(&U->is2d) && w != 0.0) b.consider(nu_wall(ey + n1 + 1, ld(&U->i2), ic, z, w), l, w > 0.0 ? 5 : 4, 0);
+      return;
+    }
+  }
+  if (u != 0.0) b.consider(rect_wall(ld(&U->d[0]), ld(&U->d[3]), ia, x, u), l, u > 0.0 ? 1 : 0, 0);
+  if (v != 0.0) b.consider(rect_wall(ld(&U->d[1]), ld(&U->d[4]), ib, y, v), l, v > 0.0 ? 3 : 2, 0);
+  if (!ld(&U->is2d) && w != 0.0) b.consider(rect_wall(ld(&U->d[2]), ld(&U->d[5]), ic, z, w), l, w > 0.0 ? 5 : 4, 0);
+}
+
+// tile centre of an array (the daughter translation, readings O8/O9/N1).  rect (i,j,k), hex (q,r,kz).
+__device__ __forceinline__ void array_centre(const DevGeom& g, const DUniv* U, int kind, int a, int b, int c,
+                                             double& tx, double& ty, double& tz) {
+  if (kRectNU && kind == U_RECT && ld(&U->ntile) >= 0) {
+    const int n0 = ld(&U->i0), n1 = ld(&U->i1);
+    const double* ex = g.edges + ld(&U->ntile);
+    const double* ey = ex + n0 + 1;
+    tx = nu_centre(ex, n0, a);
+    ty = nu_centre(ey, n1, b);
+    tz = ld(&U->is2d) ? 0.0 : nu_centre(ey + n1 + 1, ld(&U->i2), c);
+    return;
+  }
   if (!kHex || kind == U_RECT) {
     tx = ld(&U->d[0]) + (static_cast<double>(a) + 0.5) * ld(&U->d[3]);
     ty = ld(&U->d[1]) + (static_cast<double>(b) + 0.5) * ld(&U->d[4]);
@@ -227,7 +338,7 @@ __device__ __forceinline__ int array_daughter(const DevGeom& g, const DUniv* U, 
     const bool in = dd <= R && (nz == 0 || (c >= 0 && c < nz));
     if (in) idx = ld(g.fills + ld(&U->fill_off) + (b + R) * (2 * R + 1) + (a + R) + (nz > 0 ? c * ld(&U->ntile) : 0));
   }
-  array_centre(U, kind, a, b, c, tx, ty, tz);
+  array_centre(g, U, kind, a, b, c, tx, ty, tz);
   return idx >= 0 ? idx : ld(&U->outer);
 }
 
@@ -288,19 +399,5 @@ __device__ __forceinline__ void hex_locate(const DUniv* U, double x, double y, i
   ro = r;
 }
 
-// Distance-to-boundary bookkeeping: strict '<' keeps the top-most level / lowest id on exact
-// ties (O13); d2 = smallest other candidate (O16 F2).
-struct Best {
-  double d, d2;
-  int l, j, sense;
-  __device__ __forceinline__ void consider(double dd, int ll, int jj, int ss) {
-    const bool lt = dd < d;                       // branch-free select form
-    d2 = lt ? d : (dd < d2 ? dd : d2);
-    d = lt ? dd : d;
-    l = lt ? ll : l;
-    j = lt ? jj : j;
-    sense = lt ? ss : sense;
-  }
-};
 
 NT_DEV_END

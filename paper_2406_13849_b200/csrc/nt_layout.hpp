@@ -26,7 +26,7 @@
 
 namespace nt {
 
-enum Feature : int { F_HEX = 1, F_PLANE = 2, F_SPHERE = 4 };
+enum Feature : int { F_HEX = 1, F_PLANE = 2, F_SPHERE = 4, F_RECTNU = 8 };   // F_RECTNU: non-uniform rect
 
 constexpr int kMaxDepth = 8;          // builder-enforced nesting limit (reading O7)
 constexpr int kBihStack = 12;         // BIH depth limit = register stack capacity (nt_geom.cuh)
@@ -58,7 +58,7 @@ inline int hs_pack(int sid, int kind, int sense) { return (sid << 4) | (kind << 
 //            -1 entries = out of lattice -> outer), outer: universe id or -1.
 struct alignas(16) DUniv {
   int32_t kind, i0, i1, i2;
-  int32_t fill_off, outer, is2d, ntile;
+  int32_t fill_off, outer, is2d, ntile;   // rect: ntile = offset of the edge table (N1), -1 uniform
   double d[16];
 };
 
@@ -84,6 +84,7 @@ struct DevGeom {
   const double* mc_st;        // per material cell: sigma_t
   const double* mc_pabs;      // per material cell: sigma_a / sigma_t (O14)
   const int32_t* mc_cell;     // per material cell: global cell id (trace)
+  const double* edges;        // non-uniform rect edges (N1): per array x[n0+1] y[n1+1] z[n2+1]
   int32_t root, n_mc, max_depth, n_univ;
   int32_t n_cells, n_surf, root_kind, features;   // features: F_* bits present in the model
   const void* const* trk;     // DP dispatch only: per-universe tracker object pointers (dp_tracker.cuh)

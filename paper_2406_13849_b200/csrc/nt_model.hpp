@@ -26,6 +26,7 @@ struct HUniv {
   bool is2d = false;
   int orient = 0, rings = 1, nz = 0;
   double C[2] = {0, 0}, pitch = 0, zlo = 0, zp = 0;
+  std::vector<double> e[3];      // non-uniform rect (N1): increasing edges per axis (empty: uniform)
   std::vector<int> fill;         // rect: x fastest; hex: O9 order (x nz layers)
   int outer = -1;
 };
@@ -56,6 +57,7 @@ struct Flat {
   std::vector<int32_t> bih_leaf, fills;
   std::vector<double> mc_st, mc_pabs;
   std::vector<int32_t> mc_cell;
+  std::vector<double> edges;        // non-uniform rect edges (N1)
   std::vector<int32_t> bih_depth;   // per universe (CSG), host info
   int root = -1, max_depth = 0, n_mc = 0, features = 0;
   // rect-specialised tables

@@ -113,6 +113,8 @@ void build_rect_tables(const std::vector<HSurf>& S, const std::vector<HMat>& M, 
       for (int u : level) { all_rect &= U[u].kind == U_RECT; all_csg &= U[u].kind == U_CSG; }
       if (all_csg) break;
       if (!all_rect) throw Reject{"a level mixes universe kinds (or holds a hex array)"};
+      for (int u : level)
+        if (!U[u].e[0].empty()) throw Reject{"non-uniform rect array (binary-search lattice)"};
       if (++K > 4) throw Reject{"more than 4 rect levels"};
       std::set<int> next;
       for (int u : level) {

@@ -1,4 +1,4 @@
 // Kernels for models with any surface kind and hex arrays.
-#define NT_FEAT 7
+#define NT_FEAT 15
 #define NT_NS f7
 #include "track_impl.cuh"

@@ -71,16 +71,8 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
       ty = ld(g.cell_tr + 3 * cell + 1);
       tz = ld(g.cell_tr + 3 * cell + 2);
     } else if (!kHex || kind == U_RECT) {
-      const double llx = ld(&U->d[0]), lly = ld(&U->d[1]), px = ld(&U->d[3]), py = ld(&U->d[4]);
-      const int i = rect_index(llx, px, x), j = rect_index(lly, py, y);
-      uint32_t nb = near_wall(llx, px, i, x) | near_wall(lly, py, j, y);
-      int k = 0;
-      if (!ld(&U->is2d)) {
-        const double llz = ld(&U->d[2]), pz = ld(&U->d[5]);
-        k = rect_index(llz, pz, z);
-        nb |= near_wall(llz, pz, k, z);
-      }
-      flags |= nb;
+      int i, j, k;
+      rect_locate(g, U, x, y, z, i, j, k, flags);
       st.a(l) = i; st.b(l) = j; st.c(l) = k;
       dau = array_daughter(g, U, U_RECT, i, j, k, tx, ty, tz);
     } else {
@@ -118,9 +110,7 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
       if (d < NT_INF) b.consider(d, l, sid, hs_sense(e));
     }
   } else if (!kHex || kind == U_RECT) {
-    if (u != 0.0) b.consider(rect_wall(ld(&U->d[0]), ld(&U->d[3]), ia, x, u), l, u > 0.0 ? 1 : 0, 0);
-    if (v != 0.0) b.consider(rect_wall(ld(&U->d[1]), ld(&U->d[4]), ib, y, v), l, v > 0.0 ? 3 : 2, 0);
-    if (!ld(&U->is2d) && w != 0.0) b.consider(rect_wall(ld(&U->d[2]), ld(&U->d[5]), ic, z, w), l, w > 0.0 ? 5 : 4, 0);
+    rect_candidates(g, U, ia, ib, ic, l, x, y, z, u, v, w, b);
   } else {
     double t0, t1, t2, m0, m1, m2;
     hex_t(U, x, y, t0, t1, t2);
@@ -157,7 +147,7 @@ __device__ __forceinline__ void level_translation(const DevGeom& g, const DUniv*
     ty = ld(g.cell_tr + 3 * ia + 1);
     tz = ld(g.cell_tr + 3 * ia + 2);
   } else {
-    array_centre(U, kind, ia, ib, ic, tx, ty, tz);
+    array_centre(g, U, kind, ia, ib, ic, tx, ty, tz);
   }
 }
 

@@ -161,3 +161,21 @@ def test_rect_specialisable_gate(nt, cfg, ok, K):
     assert m.info["rect_specialisable"] == ok
     if ok:
         assert m.info["rect_levels"] == K
+
+
+def test_nonuniform_rect_host_build(nt):
+    """Non-uniform rect arrays (Alg. 5, reading N1): build, feature bit, rect-tracker gate,
+    pseudo-array conversion (every tile -1..n per axis), edge validation."""
+    spec = workloads.models.nonuniform_slabs()
+    m = _host(nt, spec)
+    assert m.info["rect_specialisable"] == 0
+    assert m.info["max_depth"] == 3
+    p = _host(nt, spec, pseudo_array=True)
+    assert p.info["n_cells"] == 1 + 12 + 12            # root box + tiles (+ their all-space cells)
+    g = _host(nt, workloads.models.gap_lattice(True), pseudo_array=True)
+    assert g.info["n_cells"] > 7 * 7
+    bad = workloads.models.nonuniform_slabs()
+    lat = next(u for u in bad["universes"] if u["kind"] == "rect")
+    lat["edges"][0] = [0.0, 3.0, 1.0, 6.0]
+    with pytest.raises(nt.NtError, match="strictly increasing"):
+        _host(nt, bad)

@@ -99,6 +99,35 @@ def test_test_models_parity(nt, orc, name, sched):
     _compare(nt, orc, spec, 700, seed=2, scheduler=sched)
 
 
+NONUNIFORM = {"gap_lattice": lambda: workloads.models.gap_lattice(True),
+              "c2_gap_assembly": lambda: workloads.models.c2_gap_assembly(),
+              "nonuniform_slabs": lambda: workloads.models.nonuniform_slabs()}
+
+
+@pytest.mark.parametrize("sched", ["block", "warp", "history", "dp"])
+@pytest.mark.parametrize("name", list(NONUNIFORM))
+def test_nonuniform_rect_parity(nt, orc, name, sched):
+    """Non-uniform rect arrays (Alg. 5 binary search, reading N1): traces bit-exact vs the oracle
+    under every scheduler / dispatch."""
+    _compare(nt, orc, NONUNIFORM[name](), 600, seed=8, scheduler=sched)
+
+
+@pytest.mark.parametrize("name", ["gap_lattice", "c2_gap_assembly"])
+def test_nonuniform_pseudo_array_equals_generic(nt, name):
+    """ST conversion of a non-uniform array (planes at the divisions, slabs -1 / n bounded on one
+    side): same walk as the binary-search lattice (surface ids j differ by construction)."""
+    spec = NONUNIFORM[name]()
+    a = nt.Model.from_spec(spec, device=0)
+    b = nt.Model.from_spec(spec, device=0, pseudo_array=True)
+    ra = a.track(600, seed=7, trace_cap=400000, pflags=True)
+    rb = b.track(600, seed=7, trace_cap=400000, pflags=True)
+    torch.cuda.synchronize()
+    ta, tb = nt.Model.trace_records(ra), nt.Model.trace_records(rb)
+    assert len(ta) == len(tb)
+    for f in ("pid", "seg", "kind", "level", "cell_before", "cell_after", "terminal", "s"):
+        assert np.array_equal(ta[f], tb[f]), f
+
+
 def test_dp_dispatch_rejects_other_schedulers(nt):
     """NT_DP is a dispatch mode of the block-queue scheduler only (nestrack.h)."""
     spec, _ = workloads.config("c1")

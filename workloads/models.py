@@ -79,6 +79,17 @@ class Spec:
                                "outer": -1 if outer is None else int(outer)})
         return len(self.universes) - 1
 
+    def rect_edges(self, name: str, edges, fill, outer: int | None) -> int:
+        """Non-uniform rect array (Alg. 5 binary-search lattice): edges = [ex, ey, ez]
+        strictly increasing mesh divisions per axis; ez = [] -> 2-D.  fill: x fastest."""
+        ex, ey, ez = ([float(v) for v in e] for e in edges)
+        shape = (len(ex) - 1, len(ey) - 1, max(len(ez) - 1, 1))
+        assert len(fill) == shape[0] * shape[1] * shape[2]
+        self.universes.append({"kind": "rect", "name": name, "edges": [ex, ey, ez],
+                               "shape": list(shape), "fill": [int(v) for v in fill],
+                               "outer": -1 if outer is None else int(outer)})
+        return len(self.universes) - 1
+
     def hex(self, name: str, orient: str, center, pitch: float, rings: int, fill,
             outer: int | None, z_lower: float = 0.0, z_pitch: float = 0.0, nz: int = 0) -> int:
         """Hex array (axial q,r).  fill in O9 order: r ascending then q ascending over
@@ -208,6 +219,84 @@ def c2_assembly() -> dict:
     sp.cell(root, box, fill=assy)
     sp.root = root
     sp.source = {"lo": [-ha, -ha, 0.0], "hi": [ha, ha, HEIGHT]}
+    return sp.to_dict()
+
+
+def c2_gap_assembly() -> dict:
+    """C2 as a NON-UNIFORM 19x19 lattice (the paper's motivation for Alg. 5's binary search,
+    P:500-505): a 0.04 cm water-gap column / row on each side of the 17 pin pitches, filled by
+    the water pin, instead of the uniform lattice's `outer`.  The material layout is exactly
+    C2's, and the 17x17 edges are computed like the uniform edges (ll + i*p)."""
+    sp = Spec("c2_gap_assembly")
+    root = sp.csg("root")
+    ha = ASSY_PITCH / 2
+    box = _box(sp, (-ha, -ha, 0.0), (ha, ha, HEIGHT), "reflect")
+    mats = _pwr_materials(sp)
+    fuel = _pin(sp, "fuel_pin", PIN_R, [mats["uo2"], mats["gap"], mats["zr"], mats["water"]])
+    gt = _pin(sp, "guide_tube", GT_R, [mats["water"], mats["zr"], mats["water"]])
+    water = _pin(sp, "water_pin", (), [mats["water"]])
+    ll = -ASSY_N * PIN_PITCH / 2
+    e = [-ha] + [ll + i * PIN_PITCH for i in range(ASSY_N + 1)] + [ha]
+    gts = set(C2_GT)
+    fill = []
+    for j in range(ASSY_N + 2):
+        for i in range(ASSY_N + 2):
+            inner = 1 <= i <= ASSY_N and 1 <= j <= ASSY_N
+            fill.append((gt if (j - 1, i - 1) in gts else fuel) if inner else water)
+    assy = sp.rect_edges("gap_assembly", [e, e, []], fill, water)
+    sp.cell(root, box, fill=assy)
+    sp.root = root
+    sp.source = {"lo": [-ha, -ha, 0.0], "hi": [ha, ha, HEIGHT]}
+    return sp.to_dict()
+
+
+def gap_lattice(nonuniform: bool) -> dict:
+    """5x5 pin lattice, pitch 1.25, with a 0.0625 cm water gap to a reflective box: either a
+    uniform lattice whose `outer` (water pin) fills the gap, or a NON-UNIFORM 7x7 lattice with
+    explicit gap columns.  All divisions and tile centres are dyadic, hence exact in both forms,
+    so the two walks must be bit-identical (pin for reading N1)."""
+    sp = Spec("gap_lattice_" + ("nonuniform" if nonuniform else "uniform"))
+    root = sp.csg("root")
+    n, p, g = 5, 1.25, 0.0625
+    ll = -n * p / 2
+    h = -ll + g
+    box = _box(sp, (-h, -h, 0.0), (h, h, 10.0), "reflect")
+    mats = _pwr_materials(sp)
+    fuel = _pin(sp, "fuel_pin", PIN_R, [mats["uo2"], mats["gap"], mats["zr"], mats["water"]])
+    gt = _pin(sp, "guide_tube", GT_R, [mats["water"], mats["zr"], mats["water"]])
+    water = _pin(sp, "water_pin", (), [mats["water"]])
+    pin = lambda i, j: gt if (i + j) % 3 == 0 else fuel          # noqa: E731
+    if nonuniform:
+        e = [-h] + [ll + i * p for i in range(n + 1)] + [h]
+        fill = [pin(i - 1, j - 1) if 1 <= i <= n and 1 <= j <= n else water
+                for j in range(n + 2) for i in range(n + 2)]
+        lat = sp.rect_edges("lattice", [e, e, []], fill, water)
+    else:
+        lat = sp.rect("lattice", (ll, ll, 0.0), (p, p, 0.0), (n, n, 1),
+                      [pin(i, j) for j in range(n) for i in range(n)], water)
+    sp.cell(root, box, fill=lat)
+    sp.root = root
+    sp.source = {"lo": [-h, -h, 0.0], "hi": [h, h, 10.0]}
+    return sp.to_dict()
+
+
+def nonuniform_slabs(sigma_t=1.0, sigma_a=0.1) -> dict:
+    """Reflective box [0,6]x[0,3]x[0,2] tiled by a non-uniform 3x2x2 lattice (x edges 0,1,3,6;
+    y 0,0.5,3; z 0,0.7,2), one all-space cell of the same material per tile: track-length
+    fractions must equal the tile volumes (P9 applied to Alg. 5 lattices)."""
+    sp = Spec("nonuniform_slabs")
+    root = sp.csg("root")
+    box = _box(sp, (0.0, 0.0, 0.0), (6.0, 3.0, 2.0), "reflect")
+    m = sp.mat("medium", sigma_t, sigma_a)
+    tiles = []
+    for t in range(12):
+        u = sp.csg(f"tile{t}")
+        sp.cell(u, [], material=m)
+        tiles.append(u)
+    lat = sp.rect_edges("slabs", [[0.0, 1.0, 3.0, 6.0], [0.0, 0.5, 3.0], [0.0, 0.7, 2.0]], tiles, None)
+    sp.cell(root, box, fill=lat)
+    sp.root = root
+    sp.source = {"lo": [0.0, 0.0, 0.0], "hi": [6.0, 3.0, 2.0]}
     return sp.to_dict()
 
 
