@@ -44,6 +44,8 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-ratio", action="store_true", help="skip the rect-tracker comparison run")
+    ap.add_argument("--mesh", default=None, help="superimposed mesh tally NXxNYxNZ over the config's "
+                    "source box (NEXT-2; the paper's active-cycle mesh is 119x119x30)")
     return ap.parse_args()
 
 
@@ -189,10 +191,18 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     n = int(a.particles) if a.particles else n_cfg
+    mesh_shape = None
+    if a.mesh:
+        mesh_shape = [int(v) for v in a.mesh.lower().split("x")]
+        spec["mesh"] = {"lo": spec["source"]["lo"], "hi": spec["source"]["hi"], "shape": mesh_shape}
     model = nt.Model.from_spec(spec, device=local, pseudo_array=a.pseudo_array)
+    mbuf = (torch.zeros(model.info["mesh_bins"], dtype=torch.float64, device="cuda")
+            if mesh_shape else None)
     stream = torch.cuda.current_stream()
     out = torch.zeros(model.out_len, dtype=torch.float64, device="cuda")
-    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")   # > 126 MB L2
+    # L2 flush between timed steps: READ a 256 MB buffer (> 126 MB L2).  Reading leaves clean
+    # lines, so no write-back of flush data is charged to the next tracking launch.
+    flush = torch.ones(256 * 1024 * 1024, dtype=torch.uint8, device="cuda")
     seed0 = workloads.SEED
     kw = dict(tracker=a.tracker, block_dim=a.block_dim, blocks_per_sm=a.blocks_per_sm,
               scheduler=a.scheduler if a.tracker == "generic" else "history")
@@ -201,7 +211,9 @@ def main():
 
     def step(s, o):
         o.zero_()
-        model.track(n, seed=seed0 + s, pid_begin=rank * n, out=o, stream=stream, **kw)
+        if mbuf is not None:
+            mbuf.zero_()
+        model.track(n, seed=seed0 + s, pid_begin=rank * n, out=o, stream=stream, mesh=mbuf, **kw)
         if dist is not None:
             dist.all_reduce(o)      # the one collective: packed [len | exits | counters]
 
@@ -217,7 +229,7 @@ def main():
     if dist is not None:
         dist.barrier()
     for s in range(a.steps):
-        flush.fill_(s & 0xFF)                       # evict L2 between timed steps (untimed)
+        flush.max()                                 # evict L2 between timed steps (untimed)
         ev[s][0].record(stream)
         step(s, outs[s])
         ev[s][1].record(stream)
@@ -261,15 +273,15 @@ def main():
     if not a.no_ratio and a.tracker == "generic" and model.info["rect_specialisable"]:
         def timed(kk):
             o2 = torch.zeros_like(out)
-            model.track(n, seed=seed0 + 20_000, pid_begin=rank * n, out=o2, stream=stream, **kk)
+            model.track(n, seed=seed0 + 20_000, pid_begin=rank * n, out=o2, stream=stream, mesh=mbuf, **kk)
             torch.cuda.synchronize()
             tt, ss = 0.0, 0
             for s in range(a.steps):
                 o2.zero_()
-                flush.fill_(s & 0xFF)
+                flush.max()
                 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
                 e0.record(stream)
-                model.track(n, seed=seed0 + s, pid_begin=rank * n, out=o2, stream=stream, **kk)
+                model.track(n, seed=seed0 + s, pid_begin=rank * n, out=o2, stream=stream, mesh=mbuf, **kk)
                 e1.record(stream)
                 torch.cuda.synchronize()
                 tt += e0.elapsed_time(e1) / 1e3
@@ -283,7 +295,29 @@ def main():
                          "tracker (history scheduler); target >= 0.85 (north star)"}
 
     e2e = None
-    if not a.no_e2e:
+    if not a.no_e2e and mbuf is not None:
+        # mesh runs: the public Python call + D2H of the packed tallies and the mesh (pinned host)
+        hout = torch.empty(model.out_len, dtype=torch.float64).pin_memory()
+        hmesh = torch.empty(mbuf.numel(), dtype=torch.float64).pin_memory()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        esegs = 0
+        t0 = time.perf_counter()
+        e0.record(stream)
+        for s in range(a.steps):
+            out.zero_()
+            mbuf.zero_()
+            model.track(n, seed=seed0 + 500 + s, pid_begin=rank * n, out=out, stream=stream, mesh=mbuf, **kw)
+            hout.copy_(out, non_blocking=True)
+            hmesh.copy_(mbuf, non_blocking=True)
+            torch.cuda.synchronize()
+            esegs += int(hout[2 * model.n_mc + 1])
+        e1.record(stream)
+        torch.cuda.synchronize()
+        te = max(e0.elapsed_time(e1) / 1e3, time.perf_counter() - t0)
+        e2e = {"value": esegs / te, "unit": UNIT, "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": int(model.out_len * 8 + mbuf.numel() * 8),
+               "api": "Model.track with a mesh buffer + D2H of tallies and mesh into pinned host memory"}
+    elif not a.no_e2e:
         hout = None
         import numpy as np
         hout = np.zeros(model.out_len)
@@ -319,7 +353,8 @@ def main():
                            "tracker": a.tracker, "pseudo_array": bool(a.pseudo_array),
                            "scheduler": kw["scheduler"],
                            "parallelism": f"pid-sharded x{world}, one fp64 all-reduce per step",
-                           "l2": "256 MB buffer written between timed steps (L2 flushed)"},
+                           "l2": "256 MB buffer read between timed steps (L2 flushed)",
+                           "mesh_tally": mesh_shape},
                 "particles_per_s": particles / t_max,
                 "segments_per_history": segs / particles,
                 "counters_last_step": res["counters"],

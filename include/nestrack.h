@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define NT_ABI_VERSION 1
+#define NT_ABI_VERSION 2
 
 typedef enum {
     NT_OK = 0,
@@ -184,6 +184,14 @@ nt_status nt_add_hex_array(nt_model* m, nt_hex_orient orient, const double cente
 
 nt_status nt_set_root(nt_model* m, int32_t uid);
 
+/* Superimposed Cartesian mesh track-length tally (the paper's active-cycle
+ * 119x119x30 mesh tally; reading M1).  Voxel (i, j, k) spans
+ * [lo_a + i d_a, lo_a + (i+1) d_a) per axis with d_a = (hi_a - lo_a) / shape_a (global frame).
+ * When a run passes nt_outputs.mesh, every segment adds to each voxel the length of its part
+ * inside that voxel (parts outside the mesh are not scored).  1 <= shape_a <= 4096, hi > lo,
+ * else NT_E_GEOMETRY.  Call before nt_finalize; a later call replaces the mesh. */
+nt_status nt_set_mesh(nt_model* m, const double lo[3], const double hi[3], const int32_t shape[3]);
+
 /* ---- finalize: validate, BIH (SAH), optional pseudo-arrays, flatten, upload -------- */
 typedef struct {
     int32_t device;         /* CUDA device for the geometry copy; -1 = host-only build (no upload) */
@@ -209,6 +217,7 @@ typedef struct {
     int32_t n_bih_nodes;
     int64_t out_len;              /* 2*n_material_cells + NT_NC */
     size_t device_bytes;          /* size of the device geometry blob */
+    int64_t mesh_bins;            /* voxels of the mesh set by nt_set_mesh (0: none) */
 } nt_model_info;
 
 nt_status nt_model_info_get(const nt_model* m, nt_model_info* info);
@@ -241,6 +250,9 @@ typedef struct {
     nt_trace_rec* trace;      /* device, optional: records in arbitrary order                  */
     uint64_t trace_cap;       /* capacity of trace in records                                  */
     uint64_t* trace_count;    /* device, required with NT_TRACE: records attempted (may exceed cap) */
+    double* mesh;             /* device, optional (NULL = no mesh tally): per-voxel track length of the
+                                 model's mesh (nt_set_mesh), x fastest, accumulated; ignored when the
+                                 model has no mesh */
 } nt_outputs;
 
 /* Track run->n histories born from (seed, pid) in the source box. Asynchronous on cuda_stream. */

@@ -66,8 +66,9 @@ def lib():
             getattr(L, f).argtypes = [vp]
         L.orc_material_cell_ids.argtypes = [vp, dp]
         L.orc_cell_material.argtypes = [vp, i32]
-        L.orc_run.argtypes = [vp, u64, u64, u64, dp, dp, u64, i32, dp, dp, dp, u64, dp, dp]
-        L.orc_run_states.argtypes = [vp, u64, u64, u64, dp, u64, i32, dp, dp, dp, u64, dp, dp]
+        L.orc_run.argtypes = [vp, u64, u64, u64, dp, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp]
+        L.orc_run_states.argtypes = [vp, u64, u64, u64, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp]
+        L.orc_set_mesh.argtypes = [vp, dp, dp, dp]
         L.orc_find_cells.argtypes = [vp, dp, u64, dp, dp]
         L.orc_count_containing.argtypes = [vp, i32, dp]
         L.orc_surface_distance.argtypes = [vp, i32, i32, i32, dp, dp]
@@ -172,6 +173,14 @@ class OracleModel:
                 L.orc_add_hex(m.h, 0 if u["orient"] == "pointy" else 1, _p(cen), u["pitch"],
                               u["rings"], u["z_lower"], u["z_pitch"], u["nz"], _p(fl), u["outer"])
         L.orc_set_root(m.h, spec["root"])
+        m.mesh_shape = None
+        if spec.get("mesh"):
+            me = spec["mesh"]
+            lo, hi = np.asarray(me["lo"], dtype=np.float64), np.asarray(me["hi"], dtype=np.float64)
+            sh = np.asarray(me["shape"], dtype=np.int32)
+            if L.orc_set_mesh(m.h, _p(lo), _p(hi), _p(sh)) != 0:
+                raise ValueError("oracle: bad mesh")
+            m.mesh_shape = tuple(int(v) for v in sh)
         rc = L.orc_finalize(m.h)
         if rc != 0:
             raise ValueError(f"oracle finalize failed: {rc}")
@@ -186,8 +195,9 @@ class OracleModel:
     # ------------------------------------------------------------------ runs
     def run(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
             max_segments: int = 1_000_000, threads: int | None = None, pflags: bool = False,
-            trace_cap: int = 0, states: np.ndarray | None = None):
-        """Track particles [pid_begin, pid_begin+n).  Returns dict with out, counters, ..."""
+            trace_cap: int = 0, states: np.ndarray | None = None, mesh: bool = False):
+        """Track particles [pid_begin, pid_begin+n).  Returns dict with out, counters, ...
+        mesh=True (model spec with a "mesh"): res["mesh"] = per-voxel track length, x fastest."""
         if threads is None:
             threads = len(os.sched_getaffinity(0))
         out = np.zeros(self.out_len)
@@ -195,23 +205,30 @@ class OracleModel:
         tr = np.zeros(max(trace_cap, 1), dtype=TRACE_DTYPE) if trace_cap else None
         tcount = np.zeros(1, dtype=np.uint64)
         ev = np.zeros(8, dtype=np.uint64)
+        mo = None
+        if mesh:
+            assert self.mesh_shape is not None, "model has no mesh"
+            mo = np.zeros(int(np.prod(self.mesh_shape)))
         if states is None:
             src = self.spec["source"]
             lo = np.asarray(src["lo"] if lo is None else lo, dtype=np.float64)
             hi = np.asarray(src["hi"] if hi is None else hi, dtype=np.float64)
             rc = self.L.orc_run(self.h, seed, pid_begin, n, _p(lo), _p(hi), max_segments, threads,
                                 _p(out), _p(pf) if pf is not None else None,
-                                _p(tr) if tr is not None else None, trace_cap, _p(tcount), _p(ev))
+                                _p(tr) if tr is not None else None, trace_cap, _p(tcount), _p(ev),
+                                _p(mo) if mo is not None else None)
         else:
             st = np.ascontiguousarray(states, dtype=np.float64)
             assert st.shape == (6, n)
             rc = self.L.orc_run_states(self.h, seed, pid_begin, n, _p(st), max_segments, threads,
                                        _p(out), _p(pf) if pf is not None else None,
                                        _p(tr) if tr is not None else None, trace_cap, _p(tcount),
-                                       _p(ev))
+                                       _p(ev), _p(mo) if mo is not None else None)
         assert rc == 0
         res = self.unpack(out)
         res["evals"] = {k: int(ev[i]) for i, k in enumerate(EVAL_KINDS)}
+        if mo is not None:
+            res["mesh"] = mo
         if pf is not None:
             res["pflags"] = pf[:n]
         if tr is not None:

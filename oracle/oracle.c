@@ -16,6 +16,10 @@
  *     explicit search (Alg. 5; hex reading O9);
  *   - distance to boundary: the minimum over every half-space of every
  *     level's current cell, plus the tile walls (Table 1).
+ *   - mesh track-length tally (NEXT-2; reading M1 in DESIGN.md):
+ *     every segment's [0, s] is cut at every mesh-plane crossing, the cut
+ *     parameters are sorted, and each piece goes to the voxel that holds its
+ *     midpoint (found by the same explicit search as a rect index).
  *   - non-uniform rect arrays (Alg. 5, P:513-525 and its footnote P:500-505):
  *     the tile is found by a linear scan over the mesh divisions (reading N1
  *     in DESIGN.md: index -1 below the first edge, n at or above the last).
@@ -88,6 +92,9 @@ typedef struct {
     int ns, nm, nc, nu, cs, cm, cc, cu;
     Surf *s; Mat *m; Cell *c; Univ *u;
     int root, finalized, n_mc, max_depth;
+    /* superimposed Cartesian mesh (M1): voxel edges lo + i * d per axis, n[a] voxels */
+    int mesh_on, mesh_n[3];
+    double mesh_lo[3], mesh_d[3];
     int *mc_cell;                /* mc index -> global cell id */
 } Model;
 
@@ -768,6 +775,7 @@ static void neu_add(Neu *a, double x) {        /* Neumaier compensated summation
 
 typedef struct {
     Neu *len; uint64_t *exits; uint64_t cnt[NCOUNT]; uint64_t ev[NEVAL];
+    Neu *mesh;                   /* per-voxel track length (M1), NULL when not tallied */
 } Acc;
 
 typedef struct {
@@ -775,6 +783,7 @@ typedef struct {
     double lo[3], w[3];
     const double *states;    /* optional explicit births: SoA 6 x n */
     uint8_t *pflags; TraceRec *trace; uint64_t trace_cap; uint64_t *trace_count;
+    double *mesh_out;        /* optional per-voxel track length (M1), accumulated */
 } RunCtx;
 
 static void emit(const RunCtx *R, uint64_t pid, uint32_t seg, int kind, int level, int j, int cb,
@@ -788,6 +797,64 @@ static void emit(const RunCtx *R, uint64_t pid, uint32_t seg, int kind, int leve
     memset(t, 0, sizeof(*t));
     t->pid = pid; t->s = s; t->seg = seg; t->cell_before = cb; t->cell_after = ca; t->j = j;
     t->kind = (uint8_t)kind; t->level = (int8_t)level; t->terminal = (uint8_t)terminal; t->flags = flags;
+}
+
+/* M1: mesh plane i of axis a */
+static double mesh_edge(const Model *m, int a, int i) { return m->mesh_lo[a] + (double)i * m->mesh_d[a]; }
+
+/* M1: score the segment r + t om, t in [0, s], into the mesh: cut at every plane crossing,
+ * sort the cuts, give each piece to the voxel holding its midpoint (plain definition). */
+static void mesh_score(const Model *m, Acc *A, const double r[3], const double om[3], double s) {
+    if (!A->mesh || !(s > 0.0)) return;
+    int cap = 2 + m->mesh_n[0] + m->mesh_n[1] + m->mesh_n[2] + 3;
+    double tl[2 + 4096];
+    if (cap > 2 + 4096) return;                                  /* meshes here are <= 1024 / axis */
+    int nt = 0;
+    tl[nt++] = 0.0;
+    tl[nt++] = s;
+    for (int a = 0; a < 3; ++a) {
+        if (om[a] == 0.0) continue;
+        for (int i = 0; i <= m->mesh_n[a]; ++i) {
+            double t = (mesh_edge(m, a, i) - r[a]) / om[a];
+            if (t > 0.0 && t < s) tl[nt++] = t;
+        }
+    }
+    /* insertion sort: the lists are short */
+    for (int i = 1; i < nt; ++i) {
+        double v = tl[i];
+        int j = i - 1;
+        while (j >= 0 && tl[j] > v) { tl[j + 1] = tl[j]; --j; }
+        tl[j + 1] = v;
+    }
+    for (int k = 0; k + 1 < nt; ++k) {
+        double t0 = tl[k], t1 = tl[k + 1];
+        if (!(t1 > t0)) continue;
+        double tm = (t0 + t1) * 0.5;
+        int ijk[3], in = 1;
+        for (int a = 0; a < 3 && in; ++a) {
+            double x = r[a] + tm * om[a];
+            int i = -1;
+            for (int q = 0; q < m->mesh_n[a]; ++q)               /* explicit search: the definition */
+                if (mesh_edge(m, a, q) <= x && x < mesh_edge(m, a, q + 1)) { i = q; break; }
+            if (i < 0) in = 0;
+            ijk[a] = i;
+        }
+        if (!in) continue;
+        neu_add(&A->mesh[ijk[0] + m->mesh_n[0] * (ijk[1] + m->mesh_n[1] * ijk[2])], t1 - t0);
+    }
+}
+
+int orc_set_mesh(void *vm, const double *lo, const double *hi, const int *n) {
+    Model *m = vm;
+    for (int a = 0; a < 3; ++a)
+        if (n[a] < 1 || n[a] > 1024 || !(hi[a] > lo[a])) return -1;
+    for (int a = 0; a < 3; ++a) {
+        m->mesh_n[a] = n[a];
+        m->mesh_lo[a] = lo[a];
+        m->mesh_d[a] = (hi[a] - lo[a]) / (double)n[a];
+    }
+    m->mesh_on = 1;
+    return 0;
 }
 
 static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
@@ -846,6 +913,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
         if (ds < dc) {                                            /* Alg. 2 "while d < tau/Sigma" */
             double s = ds;
             neu_add(&A->len[mc], s);
+            mesh_score(m, A, r, om, s);
             for (int a = 0; a < 3; ++a) r[a] = r[a] + s * om[a];
             double tt = tau - M->st * s;
             tau = tt > 0.0 ? tt : 0.0;                            /* O12 */
@@ -921,6 +989,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
         } else {                                                  /* collision at tau/Sigma */
             double s = dc;
             neu_add(&A->len[mc], s);
+            mesh_score(m, A, r, om, s);
             for (int a = 0; a < 3; ++a) r[a] = r[a] + s * om[a];
             nseg++;
             A->cnt[C_COLLISIONS]++;
@@ -954,7 +1023,7 @@ done:
 static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *lo,
                       const double *hi, const double *states, uint64_t max_seg, int nthreads,
                       double *out, uint8_t *pflags, void *trace, uint64_t trace_cap,
-                      uint64_t *trace_count, uint64_t *evals) {
+                      uint64_t *trace_count, uint64_t *evals, double *mesh_out) {
     Model *m = vm;
     if (!m->finalized) return -1;
     RunCtx R;
@@ -962,6 +1031,8 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
     R.m = m; R.seed = seed; R.pid0 = pid0; R.n = n; R.max_seg = max_seg ? max_seg : 1000000;
     R.states = states; R.pflags = pflags; R.trace = trace; R.trace_cap = trace_cap;
     R.trace_count = trace_count;
+    R.mesh_out = m->mesh_on ? mesh_out : NULL;
+    const size_t nbins = m->mesh_on ? (size_t)m->mesh_n[0] * m->mesh_n[1] * m->mesh_n[2] : 0;
     for (int a = 0; a < 3; ++a) { R.lo[a] = lo ? lo[a] : 0.0; R.w[a] = lo ? hi[a] - lo[a] : 0.0; }
     int nmc = m->n_mc;
     int T = nthreads > 0 ? nthreads : 1;
@@ -972,6 +1043,7 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
     for (int t = 0; t < T; ++t) {
         acc[t].len = calloc((size_t)nmc + 1, sizeof(Neu));
         acc[t].exits = calloc((size_t)nmc + 1, sizeof(uint64_t));
+        acc[t].mesh = R.mesh_out ? calloc(nbins, sizeof(Neu)) : NULL;
     }
 #pragma omp parallel num_threads(T)
     {
@@ -997,23 +1069,29 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
     }
     if (evals)
         for (int k = 0; k < NEVAL; ++k) for (int t = 0; t < T; ++t) evals[k] += acc[t].ev[k];
-    for (int t = 0; t < T; ++t) { free(acc[t].len); free(acc[t].exits); }
+    if (R.mesh_out)
+        for (size_t v = 0; v < nbins; ++v) {
+            Neu tot = {0.0, 0.0};
+            for (int t = 0; t < T; ++t) { neu_add(&tot, acc[t].mesh[v].sum); neu_add(&tot, acc[t].mesh[v].comp); }
+            R.mesh_out[v] += tot.sum + tot.comp;
+        }
+    for (int t = 0; t < T; ++t) { free(acc[t].len); free(acc[t].exits); free(acc[t].mesh); }
     free(acc);
     return 0;
 }
 
 int orc_run(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *lo, const double *hi,
             uint64_t max_seg, int nthreads, double *out, uint8_t *pflags, void *trace,
-            uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals) {
+            uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out) {
     return run_common(vm, seed, pid0, n, lo, hi, NULL, max_seg, nthreads, out, pflags, trace,
-                      trace_cap, trace_count, evals);
+                      trace_cap, trace_count, evals, mesh_out);
 }
 
 int orc_run_states(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *states,
                    uint64_t max_seg, int nthreads, double *out, uint8_t *pflags, void *trace,
-                   uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals) {
+                   uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out) {
     return run_common(vm, seed, pid0, n, NULL, NULL, states, max_seg, nthreads, out, pflags, trace,
-                      trace_cap, trace_count, evals);
+                      trace_cap, trace_count, evals, mesh_out);
 }
 
 /* ---------------------------------------------------------------- unit queries */

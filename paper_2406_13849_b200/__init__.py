@@ -50,7 +50,8 @@ class ModelInfo(C.Structure):
     _fields_ = [("n_surfaces", C.c_int32), ("n_cells", C.c_int32), ("n_material_cells", C.c_int32),
                 ("n_universes", C.c_int32), ("max_depth", C.c_int32),
                 ("rect_specialisable", C.c_int32), ("rect_levels", C.c_int32),
-                ("n_bih_nodes", C.c_int32), ("out_len", C.c_int64), ("device_bytes", C.c_size_t)]
+                ("n_bih_nodes", C.c_int32), ("out_len", C.c_int64), ("device_bytes", C.c_size_t),
+                ("mesh_bins", C.c_int64)]
 
 
 class Run(C.Structure):
@@ -63,14 +64,14 @@ class Run(C.Structure):
 class Outputs(C.Structure):
     _fields_ = [("out", C.c_void_p), ("pflags", C.c_void_p), ("pnseg", C.c_void_p),
                 ("pterm", C.c_void_p), ("trace", C.c_void_p),
-                ("trace_cap", C.c_uint64), ("trace_count", C.c_void_p)]
+                ("trace_cap", C.c_uint64), ("trace_count", C.c_void_p), ("mesh", C.c_void_p)]
 
 
 _lib = None
 
 SYMBOLS = ["nt_last_error", "nt_abi_version", "nt_model_create", "nt_model_destroy", "nt_add_surface",
            "nt_add_material", "nt_add_csg_universe", "nt_add_cell", "nt_add_rect_array", "nt_add_rect_edges",
-           "nt_add_hex_array", "nt_set_root", "nt_build_opts_default", "nt_finalize",
+           "nt_add_hex_array", "nt_set_root", "nt_set_mesh", "nt_build_opts_default", "nt_finalize",
            "nt_model_info_get", "nt_material_cell_ids", "nt_bih_info", "nt_track",
            "nt_track_states", "nt_track_host", "nt_find_cells", "nt_last_launch_count",
            "nt_selftest_arith"]
@@ -96,6 +97,7 @@ def lib():
         L.nt_add_hex_array.argtypes = [vp, i32, dp, C.c_double, i32, C.c_double, C.c_double, i32, dp,
                                        i32, C.POINTER(i32)]
         L.nt_set_root.argtypes = [vp, i32]
+        L.nt_set_mesh.argtypes = [vp, dp, dp, dp]
         L.nt_build_opts_default.argtypes = [C.POINTER(BuildOpts)]
         L.nt_finalize.argtypes = [vp, C.POINTER(BuildOpts)]
         L.nt_model_info_get.argtypes = [vp, C.POINTER(ModelInfo)]
@@ -201,6 +203,12 @@ class Model:
     def set_root(self, uid: int):
         _check(self.L.nt_set_root(self.h, uid))
 
+    def set_mesh(self, lo, hi, shape):
+        """Superimposed Cartesian mesh for the track-length mesh tally (reading M1)."""
+        lo_, hi_ = np.asarray(lo, dtype=np.float64), np.asarray(hi, dtype=np.float64)
+        sh = np.asarray(shape, dtype=np.int32)
+        _check(self.L.nt_set_mesh(self.h, _p(lo_), _p(hi_), _p(sh)))
+
     def finalize(self, device: int = 0, pseudo_array: bool = False, bih_max_leaf: int = 4):
         o = BuildOpts()
         self.L.nt_build_opts_default(C.byref(o))
@@ -245,6 +253,8 @@ class Model:
                 m.add_hex_array(u["orient"], u["center"], u["pitch"], u["rings"], u["fill"], u["outer"],
                                 u["z_lower"], u["z_pitch"], u["nz"])
         m.set_root(spec["root"])
+        if spec.get("mesh"):
+            m.set_mesh(spec["mesh"]["lo"], spec["mesh"]["hi"], spec["mesh"]["shape"])
         return m.finalize(device=device, pseudo_array=pseudo_array, bih_max_leaf=bih_max_leaf)
 
     def bih_info(self, uid: int):
@@ -276,7 +286,7 @@ class Model:
     def track(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
               max_segments: int = 0, tracker: str = "generic", pflags: bool = False,
               trace_cap: int = 0, states=None, out=None, stream=None, block_dim: int = 0,
-              blocks_per_sm: int = 0, per_history: bool = False, scheduler: str = "block"):
+              blocks_per_sm: int = 0, per_history: bool = False, scheduler: str = "block", mesh=None):
         """Track histories [pid_begin, pid_begin+n) on this model's GPU (async on `stream`).
         Returns a dict of device tensors: out (accumulated), pflags, trace, trace_count."""
         import torch
@@ -300,6 +310,12 @@ class Model:
             tc = torch.zeros(1, dtype=torch.int64, device=dev)
             o.trace, o.trace_cap, o.trace_count = tr.data_ptr(), trace_cap, tc.data_ptr()
             res["trace"], res["trace_count"] = tr, tc
+        if mesh is not None:                       # True: fresh zeroed tensor; or a caller tensor
+            if mesh is True:
+                mesh = torch.zeros(max(self.info["mesh_bins"], 1), dtype=torch.float64, device=dev)
+            assert mesh.dtype == torch.float64 and mesh.is_cuda and mesh.numel() >= self.info["mesh_bins"] > 0
+            o.mesh = mesh.data_ptr()
+            res["mesh"] = mesh
         run = self.make_run(n, seed, pid_begin, lo, hi, max_segments, tracker, bool(trace_cap),
                             block_dim, blocks_per_sm, scheduler)
         sh = _stream_handle(stream)

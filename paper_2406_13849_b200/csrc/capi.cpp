@@ -51,6 +51,9 @@ struct nt_model {
   std::mutex host_mu;
   int last_launches = 0;
   void* dp_objs = nullptr;                  // DP dispatch: tracker objects + pointer table (lazy)
+  bool mesh_on = false;                     // superimposed mesh (M1)
+  double mesh_lo[3] = {0, 0, 0}, mesh_d[3] = {0, 0, 0};
+  int32_t mesh_n[3] = {0, 0, 0};
   std::mutex dp_mu;
 };
 
@@ -236,6 +239,21 @@ nt_status nt_set_root(nt_model* m, int32_t uid) {
   return NT_OK;
 }
 
+nt_status nt_set_mesh(nt_model* m, const double lo[3], const double hi[3], const int32_t shape[3]) {
+  CHECK_BUILDER(m);
+  if (!lo || !hi || !shape) return err(NT_E_ARG, "nt_set_mesh: NULL argument");
+  for (int a = 0; a < 3; ++a)
+    if (shape[a] < 1 || shape[a] > 4096 || !(hi[a] > lo[a]) || !std::isfinite(lo[a]) || !std::isfinite(hi[a]))
+      return err(NT_E_GEOMETRY, "nt_set_mesh: need 1 <= shape <= 4096 and finite lo < hi on every axis");
+  for (int a = 0; a < 3; ++a) {
+    m->mesh_lo[a] = lo[a];
+    m->mesh_d[a] = (hi[a] - lo[a]) / (double)shape[a];
+    m->mesh_n[a] = shape[a];
+  }
+  m->mesh_on = true;
+  return NT_OK;
+}
+
 void nt_build_opts_default(nt_build_opts* o) {
   if (!o) return;
   o->device = 0;
@@ -324,6 +342,8 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
   g.n_surf = (int)F.surf.size();
   g.root_kind = F.univ[F.root].kind;
   g.features = F.features;
+  g.mesh_on = m->mesh_on ? 1 : 0;
+  for (int a = 0; a < 3; ++a) { g.mesh_lo[a] = m->mesh_lo[a]; g.mesh_d[a] = m->mesh_d[a]; g.mesh_n[a] = m->mesh_n[a]; }
   m->finalized = true;
   return NT_OK;
 }
@@ -342,6 +362,7 @@ nt_status nt_model_info_get(const nt_model* m, nt_model_info* info) {
   info->n_bih_nodes = (int)F.bih.size();
   info->out_len = 2 * (int64_t)F.n_mc + NT_NC;
   info->device_bytes = m->blob_bytes;
+  info->mesh_bins = m->mesh_on ? (int64_t)m->mesh_n[0] * m->mesh_n[1] * m->mesh_n[2] : 0;
   return NT_OK;
 }
 
@@ -423,6 +444,7 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   R.trace = o->trace;
   R.trace_cap = trace ? o->trace_cap : 0;
   R.trace_count = reinterpret_cast<unsigned long long*>(o->trace_count);
+  R.mesh = m->g.mesh_on ? o->mesh : nullptr;
   const unsigned slot = m->slot.fetch_add(1) % kSlots;
   R.counter = m->counters + slot;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

@@ -238,8 +238,9 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
               fsense = 0;
             }
           }
-          if constexpr (DP) ok = du >= 0 && descend_dp(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
-          else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
+          const uint32_t dir = dir_bits(su[slot], sv[slot], sw[slot]);
+          if constexpr (DP) ok = du >= 0 && descend_dp(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags, dir);
+          else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags, dir);
           done = true;
           if (!ok) flags |= NT_F3;
           sflags[slot] = static_cast<uint8_t>(flags);
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
               const bool cross = ds < dc;
               const double s = cross ? ds : dc;
               atomicAdd(gl + mc, s);
+              if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
               rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
               ++nseg;
               seg = true;

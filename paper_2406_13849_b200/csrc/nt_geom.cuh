@@ -134,8 +134,16 @@ struct BihStack {
 #ifdef NT_BIH_STATS
 __device__ unsigned long long g_bih_stats[4];   // calls, node visits, cell tests, root-leaf calls
 #endif
+// dir: bit a set when the particle moves towards +a.  Where both children of a node hold the
+// point (it lies in their overlap, typically on a crossed split plane), the child on the side the
+// particle is heading to is searched first.  Only the search order changes: the containing cell
+// is unique (POS iff f >= 0, forced sense on the crossed surface), so the result does not.
+__device__ __forceinline__ uint32_t dir_bits(double u, double v, double w) {
+  return (u > 0.0 ? 1u : 0u) | (v > 0.0 ? 2u : 0u) | (w > 0.0 ? 4u : 0u);
+}
+
 __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, double y, double z,
-                                        int fsid, int fsense, uint32_t& flags) {
+                                        int fsid, int fsense, uint32_t& flags, uint32_t dir = 0) {
 #ifdef NT_BIH_STATS
   atomicAdd(&g_bih_stats[0], 1ull);
 #endif
@@ -154,7 +162,10 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
       const double c = sel3(meta, x, y, z);
       const bool gl = c <= ld(&n->lmax), gr = c >= ld(&n->rmin);
       const int left = a - root;
-      if (gl && gr) { stk.push(static_cast<uint32_t>(left + 2)); node = left; }
+      if (gl && gr) {
+        if ((dir >> meta) & 1u) { stk.push(static_cast<uint32_t>(left + 1)); node = left + 1; }
+        else { stk.push(static_cast<uint32_t>(left + 2)); node = left; }
+      }
       else if (gl) node = left;
       else if (gr) node = left + 1;
       else {
@@ -212,6 +223,63 @@ struct Best {
     sense = lt ? ss : sense;
   }
 };
+
+// ---- superimposed mesh track-length tally (NEXT-2; reading M1).  3-D DDA along the
+// segment r + t om, t in [0, s].  The cut parameters are (E_a(i) - r_a) / om_a with
+// E_a(i) = lo_a + i d_a -- the oracle's -- so every scored piece is the oracle's piece.  Pieces
+// outside the mesh are skipped; the walk stops once the ray leaves the mesh on some axis.
+// Out of line: the branch that calls it is taken only by runs that pass a mesh buffer.
+struct MeshGeom { double lo[3], d[3]; int n[3]; };
+
+__device__ __noinline__ void mesh_score_impl(const MeshGeom M, double* out, double x, double y, double z,
+                                             double u, double v, double w, double s) {
+  if (!(s > 0.0)) return;
+  const double r[3] = {x, y, z}, om[3] = {u, v, w};
+  int idx[3];
+  double tn[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const double lo = M.lo[a], d = M.d[a];
+    int i = rect_index(lo, d, r[a]);                             // E(i) <= r < E(i+1)
+    if (om[a] < 0.0 && r[a] == lo + static_cast<double>(i) * d) --i;   // on a plane, moving down
+    idx[a] = i;
+    tn[a] = om[a] > 0.0 ? fdiv(lo + static_cast<double>(i + 1) * d - r[a], om[a])
+          : om[a] < 0.0 ? fdiv(lo + static_cast<double>(i) * d - r[a], om[a]) : NT_INF;
+  }
+  const int n0 = M.n[0], n1 = M.n[1], n2 = M.n[2];
+  double t = 0.0;
+#pragma unroll 1
+  for (;;) {
+    if ((idx[0] < 0 && !(u > 0.0)) || (idx[0] >= n0 && !(u < 0.0)) || (idx[1] < 0 && !(v > 0.0)) ||
+        (idx[1] >= n1 && !(v < 0.0)) || (idx[2] < 0 && !(w > 0.0)) || (idx[2] >= n2 && !(w < 0.0)))
+      return;                                                    // left the mesh for good
+    const double te = fmin(fmin(tn[0], tn[1]), fmin(tn[2], s));
+    const bool in = idx[0] >= 0 && idx[0] < n0 && idx[1] >= 0 && idx[1] < n1 && idx[2] >= 0 && idx[2] < n2;
+    if (in && te > t) atomicAdd(out + idx[0] + n0 * (idx[1] + n1 * idx[2]), te - t);
+    if (te >= s) return;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      if (tn[a] == te) {
+        const double lo = M.lo[a], d = M.d[a];
+        if (om[a] > 0.0) {
+          ++idx[a];
+          tn[a] = fdiv(lo + static_cast<double>(idx[a] + 1) * d - r[a], om[a]);
+        } else {
+          --idx[a];
+          tn[a] = fdiv(lo + static_cast<double>(idx[a]) * d - r[a], om[a]);
+        }
+      }
+    }
+    t = te;
+  }
+}
+
+__device__ __forceinline__ void mesh_score(const DevGeom& g, double* out, double x, double y, double z, double u,
+                                           double v, double w, double s) {
+  MeshGeom M;
+  for (int a = 0; a < 3; ++a) { M.lo[a] = g.mesh_lo[a]; M.d[a] = g.mesh_d[a]; M.n[a] = g.mesh_n[a]; }
+  mesh_score_impl(M, out, x, y, z, u, v, w, s);
+}
 
 // ---- non-uniform rect arrays (reading N1; Alg. 5 binary search over the mesh divisions,
 // P:500-525).  Axis divisions e[0..n]; tile -1 is the slab below e[0], tile n the slab at or

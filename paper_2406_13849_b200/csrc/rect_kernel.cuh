@@ -268,6 +268,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
         } else if (ds < dc) {
           const double s = ds;
           atomicAdd(gl + mc, s);
+          if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
@@ -321,6 +322,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
         } else {
           const double s = dc;
           atomicAdd(gl + mc, s);
+          if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           ++nseg;
           ++ncoll;

@@ -46,7 +46,7 @@ struct Stack {
 template <bool STORE_T = true>
 __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int u, double Tx, double Ty,
                                      double Tz, double rx, double ry, double rz, int fsid, int fsense,
-                                     int& L, int& mc, uint32_t& flags) {
+                                     int& L, int& mc, uint32_t& flags, uint32_t dir = 0) {
 #pragma unroll 1
   for (int l = l0; l < kMaxDepth; ++l) {
     st.u(l) = u;
@@ -61,7 +61,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
     double tx, ty, tz;
     int dau;
     if (kind == U_CSG) {
-      const int cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags);
+      const int cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags, dir);
       if (cell < 0) return false;
       st.a(l) = cell;
       const int f = ld(g.cell_fill + cell);
@@ -247,7 +247,8 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
     }
     if (phase == 1) {
       // ---- Alg. 7 / Alg. 8 descent (single call site for birth and every crossing)
-      const bool ok = descend(g, st, d_l0, d_u, d_Tx, d_Ty, d_Tz, rx, ry, rz, d_fsid, d_fsense, L, mc, flags);
+      const bool ok = descend(g, st, d_l0, d_u, d_Tx, d_Ty, d_Tz, rx, ry, rz, d_fsid, d_fsense, L, mc, flags,
+                              dir_bits(u, v, w));
       if (!ok) {
         flags |= NT_F3;
         term = NT_T_LOST;
@@ -284,6 +285,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           // Alg. 2 "while d < tau/Sigma": tau -= Sigma d, move, cross
           const double s = ds;
           atomicAdd(gl + mc, s);
+          if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
@@ -345,6 +347,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           // ---- collision at tau / Sigma_t: absorb or scatter isotropically (O14, O15)
           const double s = dc;
           atomicAdd(gl + mc, s);
+          if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           ++nseg;
           ++ncoll;

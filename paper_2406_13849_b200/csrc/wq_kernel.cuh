@@ -223,7 +223,8 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
             fsense = 0;
           }
         }
-        ok = du >= 0 && descend<false>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
+        ok = du >= 0 && descend<false>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags,
+                                       dir_bits(su[slot], sv[slot], sw[slot]));
         done = true;
         if (!ok) flags |= NT_F3;
         sflags[slot] = static_cast<uint8_t>(flags);
@@ -300,6 +301,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
             const bool cross = ds < dc;
             const double s = cross ? ds : dc;
             atomicAdd(gl + mc, s);
+            if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
             rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
             ++nseg;
             seg = true;

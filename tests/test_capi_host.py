@@ -29,7 +29,7 @@ def test_exports_every_header_symbol(nt):
     missing = [s for s in declared if not hasattr(L, s)]
     assert not missing, missing
     assert set(declared) == set(nt.SYMBOLS)
-    assert L.nt_abi_version() == 1
+    assert L.nt_abi_version() == 2
 
 
 def _host(nt, spec, **kw):
@@ -179,3 +179,17 @@ def test_nonuniform_rect_host_build(nt):
     lat["edges"][0] = [0.0, 3.0, 1.0, 6.0]
     with pytest.raises(nt.NtError, match="strictly increasing"):
         _host(nt, bad)
+
+
+def test_mesh_host_validation(nt):
+    """nt_set_mesh (NEXT-2): voxel count reported by nt_model_info; bad shapes / boxes rejected."""
+    spec, _ = workloads.config("c3")
+    spec["mesh"] = {"lo": [-161.25, -161.25, 0.0], "hi": [161.25, 161.25, 365.76], "shape": [119, 119, 30]}
+    m = _host(nt, spec)
+    assert m.info["mesh_bins"] == 119 * 119 * 30
+    assert _host(nt, workloads.config("c1")[0]).info["mesh_bins"] == 0
+    for bad in ({"shape": [0, 1, 1]}, {"hi": [-161.25, 161.25, 365.76]}):
+        s2 = dict(spec)
+        s2["mesh"] = dict(spec["mesh"], **bad)
+        with pytest.raises(nt.NtError, match="nt_set_mesh"):
+            _host(nt, s2)

@@ -128,6 +128,56 @@ def test_nonuniform_pseudo_array_equals_generic(nt, name):
         assert np.array_equal(ta[f], tb[f]), f
 
 
+def _with_mesh(spec, lo, hi, shape):
+    spec = dict(spec)
+    spec["mesh"] = {"lo": list(lo), "hi": list(hi), "shape": list(shape)}
+    return spec
+
+
+MESHED = {
+    # C1 pincell, mesh over the whole box (every segment scored)
+    "c1": lambda: _with_mesh(workloads.config("c1")[0], (-0.63, -0.63, 0.0), (0.63, 0.63, 365.76), (7, 5, 9)),
+    # C3 core with a coarse mesh over part of the core (segments cross in and out of it)
+    "c3": lambda: _with_mesh(workloads.config("c3")[0], (-120.0, -161.25, 20.0), (161.25, 100.0, 300.0), (23, 19, 7)),
+    # C4 hex core, mesh larger than the model
+    "c4": lambda: _with_mesh(workloads.config("c4")[0], (-120.0, -120.0, -10.0), (120.0, 120.0, 160.0), (16, 16, 4)),
+}
+
+
+@pytest.mark.parametrize("sched", ["block", "warp", "history", "dp", "rect"])
+@pytest.mark.parametrize("name", list(MESHED))
+def test_mesh_tally_parity(nt, orc, name, sched):
+    """Superimposed mesh track-length tally (NEXT-2, reading M1): per-voxel totals vs the oracle's
+    sort-the-cuts definition, within 1e-9 relative (summation order), under every scheduler."""
+    spec = MESHED[name]()
+    m = nt.Model.from_spec(spec, device=0)
+    if sched == "rect" and not m.info["rect_specialisable"]:
+        pytest.skip("not rect-specialisable")
+    om = orc.OracleModel.from_spec(spec)
+    n = 400
+    kw = dict(tracker="rect", scheduler="history") if sched == "rect" else dict(scheduler=sched)
+    res = m.track(n, seed=4, mesh=True, **kw)
+    torch.cuda.synchronize()
+    o = om.run(n, seed=4, mesh=True)
+    g = m.unpack(res["out"])
+    assert g["counters"] == o["counters"]
+    gm, ref = res["mesh"].cpu().numpy(), o["mesh"]
+    assert gm.shape == ref.shape and (ref > 0).sum() > 10
+    assert np.all(np.abs(gm - ref) <= 1e-9 * np.abs(ref) + 1e-12 * ref.max())
+    if name == "c1":                                  # mesh covers the model: conservation
+        assert np.isclose(gm.sum(), g["len"].sum(), rtol=1e-12)
+
+
+def test_mesh_tally_off_without_buffer(nt):
+    """A model with a mesh run without outputs.mesh: cell tallies only, identical to no mesh."""
+    spec = MESHED["c1"]()
+    a = nt.Model.from_spec(spec, device=0)
+    b = nt.Model.from_spec(workloads.config("c1")[0], device=0)
+    ra, rb = a.track(500, seed=2), b.track(500, seed=2)
+    torch.cuda.synchronize()
+    assert torch.equal(ra["out"], rb["out"]) or np.allclose(ra["out"].cpu().numpy(), rb["out"].cpu().numpy(), rtol=1e-13)
+
+
 def test_dp_dispatch_rejects_other_schedulers(nt):
     """NT_DP is a dispatch mode of the block-queue scheduler only (nestrack.h)."""
     spec, _ = workloads.config("c1")
