@@ -422,6 +422,8 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   if (run->tracker == NT_TRACKER_GENERIC && !(run->flags & (NT_WARPQ | NT_HISTORY)) && block != 128 && block != 256)
     return err(NT_E_ARG, std::string(who) + ": the event scheduler needs block_dim 128 or 256");
   if (run->n > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": at most 2^32-1 histories per call");
+  if (trace && o->mesh && m->mesh_on)
+    return err(NT_E_UNSUPPORTED, std::string(who) + ": the mesh tally cannot be combined with NT_TRACE");
   const bool dp = (run->flags & NT_DP) != 0;
   if (dp && (run->tracker != NT_TRACKER_GENERIC || (run->flags & (NT_WARPQ | NT_HISTORY)) || block != 256))
     return err(NT_E_ARG, std::string(who) + ": NT_DP needs the generic tracker, block queues and block_dim 256");

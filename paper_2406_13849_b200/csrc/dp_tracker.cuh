@@ -26,7 +26,7 @@ struct UnivTracker {
   // material cell.
   __device__ virtual int find_cell(const DevGeom& g, double x, double y, double z, int fsid, int fsense,
                                    int& ia, int& ib, int& ic, double& tx, double& ty, double& tz,
-                                   uint32_t& flags, uint32_t dir) const = 0;
+                                   uint32_t& flags) const = 0;
   // distance_to_boundary candidates of the current cell / tile at level l (canonical order, O13)
   __device__ virtual void distance(const DevGeom& g, int ia, int ib, int ic, int l, double x, double y,
                                    double z, double u, double v, double w, int os_l, int os_s, Best& b) const = 0;
@@ -38,9 +38,9 @@ struct UnivTracker {
 
 struct CsgTracker final : UnivTracker {
   __device__ int find_cell(const DevGeom& g, double x, double y, double z, int fsid, int fsense, int& ia,
-                           int& ib, int& ic, double& tx, double& ty, double& tz, uint32_t& flags,
-                           uint32_t dir) const override {
-    const int cell = csg_find(g, ld(&U->i0), x, y, z, fsid, fsense, flags, dir);
+                           int& ib, int& ic, double& tx, double& ty, double& tz,
+                           uint32_t& flags) const override {
+    const int cell = csg_find(g, ld(&U->i0), x, y, z, fsid, fsense, flags);
     if (cell < 0) return -1;
     ia = cell; ib = 0; ic = 0;
     const int f = ld(g.cell_fill + cell);
@@ -57,7 +57,7 @@ struct CsgTracker final : UnivTracker {
       const int e = ld(g.hs + h);
       const int sid = hs_sid(e);
       const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, g.surf + sid, x, y, z, u, v, w);
-      if (d < NT_INF) b.consider(d, l, sid, hs_sense(e));
+      b.consider(d, l, sid, hs_sense(e));
     }
   }
   __device__ int next_tile(const DevGeom&, int, int&, int&, int&, double&, double&, double&) const override {
@@ -67,7 +67,7 @@ struct CsgTracker final : UnivTracker {
 
 struct RectTracker final : UnivTracker {
   __device__ int find_cell(const DevGeom& g, double x, double y, double z, int, int, int& ia, int& ib, int& ic,
-                           double& tx, double& ty, double& tz, uint32_t& flags, uint32_t) const override {
+                           double& tx, double& ty, double& tz, uint32_t& flags) const override {
     int i, j, k;
     rect_locate(g, U, x, y, z, i, j, k, flags);
     ia = i; ib = j; ic = k;
@@ -87,7 +87,7 @@ struct RectTracker final : UnivTracker {
 
 struct HexTracker final : UnivTracker {
   __device__ int find_cell(const DevGeom& g, double x, double y, double z, int, int, int& ia, int& ib, int& ic,
-                           double& tx, double& ty, double& tz, uint32_t& flags, uint32_t) const override {
+                           double& tx, double& ty, double& tz, uint32_t& flags) const override {
     int q, r, k = 0;
     hex_locate(U, x, y, q, r, flags);
     if (ld(&U->i1) > 0) {
@@ -156,7 +156,7 @@ __global__ void k_dp_init(const DevGeom g, unsigned char* objs, const void** tab
 template <bool STORE_T = true>
 __device__ __forceinline__ bool descend_dp(const DevGeom& g, Stack& st, int l0, int u, double Tx, double Ty,
                                            double Tz, double rx, double ry, double rz, int fsid, int fsense,
-                                           int& L, int& mc, uint32_t& flags, uint32_t dir) {
+                                           int& L, int& mc, uint32_t& flags) {
 #pragma unroll 1
   for (int l = l0; l < kMaxDepth; ++l) {
     st.u(l) = u;
@@ -168,7 +168,7 @@ __device__ __forceinline__ bool descend_dp(const DevGeom& g, Stack& st, int l0, 
     int ia = 0, ib = 0, ic = 0;
     double tx = 0.0, ty = 0.0, tz = 0.0;
     const int r = get_tracker(g, u)->find_cell(g, rx - Tx, ry - Ty, rz - Tz, l == l0 ? fsid : -1, fsense, ia,
-                                               ib, ic, tx, ty, tz, flags, dir);
+                                               ib, ic, tx, ty, tz, flags);
     if (r == -1) return false;
     st.a(l) = ia; st.b(l) = ib; st.c(l) = ic;
     if (r <= -2) { L = l + 1; mc = -2 - r; return true; }

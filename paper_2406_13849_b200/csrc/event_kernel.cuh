@@ -54,8 +54,8 @@ size_t event_smem_bytes(const DevGeom& g, int B, bool trace) {
 }
 
 // DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh)
-template <int B, bool TRACE, bool STATES, bool DP = false>
-__global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R) {
+template <int B, bool TRACE, bool STATES, bool DP = false, bool MESH = false>
+__global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmc = g.n_mc, maxd = g.max_depth;
@@ -238,9 +238,8 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
               fsense = 0;
             }
           }
-          const uint32_t dir = dir_bits(su[slot], sv[slot], sw[slot]);
-          if constexpr (DP) ok = du >= 0 && descend_dp(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags, dir);
-          else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags, dir);
+          if constexpr (DP) ok = du >= 0 && descend_dp(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
+          else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
           done = true;
           if (!ok) flags |= NT_F3;
           sflags[slot] = static_cast<uint8_t>(flags);
@@ -286,7 +285,7 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
                         NT_T_CAPPED, flags);
           } else {
             Best b;
-            b.d = NT_INF; b.d2 = NT_INF; b.l = -1; b.j = -1; b.sense = 0;
+            b.init();
             for (int l = 0; l < L; ++l) {
               if constexpr (DP) level_distances_dp(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
               else level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
@@ -306,7 +305,7 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
               const bool cross = ds < dc;
               const double s = cross ? ds : dc;
               atomicAdd(gl + mc, s);
-              if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+              if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
               rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
               ++nseg;
               seg = true;
@@ -314,7 +313,7 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
               if (cross) {
                 const double tt = tau - sig * s;
                 tau = tt > 0.0 ? tt : 0.0;
-                const int l = b.l, j = b.j;
+                const int l = b.l(), j = b.j();
                 const int meta = (l == 0 && g.root_kind == U_CSG) ? ld(g.surf_meta + j) : 0;
                 const int bc = meta >> 4;
                 if (bc == NT_BC_VACUUM) {
@@ -335,7 +334,7 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
                   lcross = l;
                   const int uk = ld(&g.univ[st.u(l)].kind);
                   if (uk == U_CSG) {
-                    sdesc[slot] = l | ((b.sense ^ 1) << 4) | ((j + 1) << 5);
+                    sdesc[slot] = l | ((b.sense() ^ 1) << 4) | ((j + 1) << 5);
                     os_l = l; os_s = j;
                     outc = 3;
                   } else {
@@ -361,11 +360,9 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
           if (outc == 5) finalize(slot, term);
         }
         // per-event counters (one shared atomic per warp and counter)
-        warp_count(seg && (outc == 3 || outc == 4 || lcross == -2), s_cnt + C_CROSS, lane);
         warp_count(outc == 1, s_cnt + C_REFL, lane);
         warp_count(outc == 2, s_cnt + C_COLL, lane);
-        if (__any_sync(0xffffffffu, lcross >= 0))
-          for (int lv = 0; lv < maxd; ++lv) warp_count(lcross == lv, s_cnt + C_CBL0 + lv, lane);
+        if (lcross >= 0) atomicAdd(s_cnt + C_CBL0 + lcross, 1u);   // crossings = leaks + sum over levels (flush)
         // enqueue for the next event
         int pos;
         pos = warp_append(outc == 1, &QN(wr, Q_M), lane);
@@ -386,6 +383,12 @@ __global__ void __launch_bounds__(B) k_track_event(const DevGeom g, const KRun R
   }
 
   // ---- flush block tallies: exits / counters from shared memory, lengths from the block slice
+  __syncthreads();
+  if (tid == 0) {                        // crossings = leaks + non-leak crossings at every level
+    unsigned int c = s_cnt[C_LEAK];
+    for (int lv = 0; lv < kMaxDepth; ++lv) c += s_cnt[C_CBL0 + lv];
+    s_cnt[C_CROSS] = c;
+  }
   __syncthreads();
   flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
 }

@@ -134,16 +134,8 @@ struct BihStack {
 #ifdef NT_BIH_STATS
 __device__ unsigned long long g_bih_stats[4];   // calls, node visits, cell tests, root-leaf calls
 #endif
-// dir: bit a set when the particle moves towards +a.  Where both children of a node hold the
-// point (it lies in their overlap, typically on a crossed split plane), the child on the side the
-// particle is heading to is searched first.  Only the search order changes: the containing cell
-// is unique (POS iff f >= 0, forced sense on the crossed surface), so the result does not.
-__device__ __forceinline__ uint32_t dir_bits(double u, double v, double w) {
-  return (u > 0.0 ? 1u : 0u) | (v > 0.0 ? 2u : 0u) | (w > 0.0 ? 4u : 0u);
-}
-
 __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, double y, double z,
-                                        int fsid, int fsense, uint32_t& flags, uint32_t dir = 0) {
+                                        int fsid, int fsense, uint32_t& flags) {
 #ifdef NT_BIH_STATS
   atomicAdd(&g_bih_stats[0], 1ull);
 #endif
@@ -162,10 +154,7 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
       const double c = sel3(meta, x, y, z);
       const bool gl = c <= ld(&n->lmax), gr = c >= ld(&n->rmin);
       const int left = a - root;
-      if (gl && gr) {
-        if ((dir >> meta) & 1u) { stk.push(static_cast<uint32_t>(left + 1)); node = left + 1; }
-        else { stk.push(static_cast<uint32_t>(left + 2)); node = left; }
-      }
+      if (gl && gr) { stk.push(static_cast<uint32_t>(left + 2)); node = left; }
       else if (gl) node = left;
       else if (gr) node = left + 1;
       else {
@@ -211,16 +200,20 @@ __device__ __forceinline__ bool near_wall(double ll, double p, int i, double x) 
 
 // Distance-to-boundary bookkeeping: strict '<' keeps the top-most level / lowest id on exact
 // ties (O13); d2 = smallest other candidate (O16 F2).
+// The winner is packed in one register (level | sense << 4 | surface-or-face << 5) so that the
+// select form costs one integer select, and +inf candidates are harmless no-ops.
 struct Best {
   double d, d2;
-  int l, j, sense;
+  int key;
+  __device__ __forceinline__ void init() { d = NT_INF; d2 = NT_INF; key = -1; }
+  __device__ __forceinline__ int l() const { return key & 15; }
+  __device__ __forceinline__ int sense() const { return (key >> 4) & 1; }
+  __device__ __forceinline__ int j() const { return key >> 5; }
   __device__ __forceinline__ void consider(double dd, int ll, int jj, int ss) {
     const bool lt = dd < d;                       // branch-free select form
     d2 = lt ? d : (dd < d2 ? dd : d2);
     d = lt ? dd : d;
-    l = lt ? ll : l;
-    j = lt ? jj : j;
-    sense = lt ? ss : sense;
+    key = lt ? (ll | (ss << 4) | (jj << 5)) : key;
   }
 };
 

@@ -8,7 +8,7 @@
 
 NT_DEV_BEGIN
 
-template <int K, bool BOX, bool TRACE, bool STATES>
+template <int K, bool BOX, bool TRACE, bool STATES, bool MESH = false>
 __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectGeom rg, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
@@ -198,35 +198,35 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
         emit<TRACE>(R, pid, nseg, NT_EV_COLLIDE, -1, -1, ld(g.mc_cell + mc), -1, 0.0, NT_T_CAPPED, flags);
       } else {
         Best b;
-        b.d = NT_INF; b.d2 = NT_INF; b.l = -1; b.j = -1; b.sense = 0;
+        b.init();
         // level 0: the root cell's half-spaces in surface-id order
         if (BOX) {
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
             const int sid = rg.box_sid[k];
             const double d = surf_dist(k >> 1, (k & 1) ? 0 : 1, false, g.surf + sid, rx, ry, rz, u, v, w);
-            if (d < NT_INF) b.consider(d, 0, sid, (k & 1) ? 0 : 1);
+            b.consider(d, 0, sid, (k & 1) ? 0 : 1);
           }
         } else {
           {
             const int sid = rg.zsid[0];
             const double d = surf_dist(S_PZ, 1, false, g.surf + sid, rx, ry, rz, u, v, w);
-            if (d < NT_INF) b.consider(d, 0, sid, 1);
+            b.consider(d, 0, sid, 1);
           }
           {
             const int sid = rg.zsid[1];
             const double d = surf_dist(S_PZ, 0, false, g.surf + sid, rx, ry, rz, u, v, w);
-            if (d < NT_INF) b.consider(d, 0, sid, 0);
+            b.consider(d, 0, sid, 0);
           }
           if (ann > 0) {
             const int sid = rg.root_sid[ann - 1];
             const double d = surf_dist(S_CZ, 1, os_l == 0 && os_s == sid, g.surf + sid, rx, ry, rz, u, v, w);
-            if (d < NT_INF) b.consider(d, 0, sid, 1);
+            b.consider(d, 0, sid, 1);
           }
           {
             const int sid = rg.root_sid[ann];
             const double d = surf_dist(S_CZ, 0, os_l == 0 && os_s == sid, g.surf + sid, rx, ry, rz, u, v, w);
-            if (d < NT_INF) b.consider(d, 0, sid, 0);
+            b.consider(d, 0, sid, 0);
           }
         }
         if (core) {
@@ -247,12 +247,12 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
           if (pa > 0) {
             const int sid = ld(rg.pin_sid + off + pa - 1);
             const double d = surf_dist(S_CZ, 1, os_l == KP && os_s == sid, g.surf + sid, x, y, z, u, v, w);
-            if (d < NT_INF) b.consider(d, KP, sid, 1);
+            b.consider(d, KP, sid, 1);
           }
           if (pa < ncz) {
             const int sid = ld(rg.pin_sid + off + pa);
             const double d = surf_dist(S_CZ, 0, os_l == KP && os_s == sid, g.surf + sid, x, y, z, u, v, w);
-            if (d < NT_INF) b.consider(d, KP, sid, 0);
+            b.consider(d, KP, sid, 0);
           }
         }
         const double sig = ld(g.mc_st + mc);
@@ -268,12 +268,12 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
         } else if (ds < dc) {
           const double s = ds;
           atomicAdd(gl + mc, s);
-          if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
           ++nseg;
-          const int l = b.l, j = b.j;
+          const int l = b.l(), j = b.j();
           const int meta = l == 0 ? ld(g.surf_meta + j) : 0;
           const int bc = meta >> 4;
           if (bc == NT_BC_VACUUM) {
@@ -293,7 +293,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
             p_l = l; p_j = j; p_cb = cell_before; p_s = s;
             phase = 1;
             if (l == 0 || l == KP) {            // CSG level: far side of surface j (Alg. 10)
-              d_l0 = l; d_fsid = j; d_fsense = b.sense ^ 1;
+              d_l0 = l; d_fsid = j; d_fsense = b.sense() ^ 1;
               os_l = l; os_s = j;
             } else {                            // rect level: tile +- 1 (Alg. 6), then its daughter
               d_fsid = -1; d_fsense = 0;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
         } else {
           const double s = dc;
           atomicAdd(gl + mc, s);
-          if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           ++nseg;
           ++ncoll;

@@ -46,7 +46,7 @@ struct Stack {
 template <bool STORE_T = true>
 __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int u, double Tx, double Ty,
                                      double Tz, double rx, double ry, double rz, int fsid, int fsense,
-                                     int& L, int& mc, uint32_t& flags, uint32_t dir = 0) {
+                                     int& L, int& mc, uint32_t& flags) {
 #pragma unroll 1
   for (int l = l0; l < kMaxDepth; ++l) {
     st.u(l) = u;
@@ -61,7 +61,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
     double tx, ty, tz;
     int dau;
     if (kind == U_CSG) {
-      const int cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags, dir);
+      const int cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags);
       if (cell < 0) return false;
       st.a(l) = cell;
       const int f = ld(g.cell_fill + cell);
@@ -102,12 +102,13 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
   if (kind == U_CSG) {
     const int cell = ia;
     const int h0 = ld(g.cell_hs + cell), h1 = ld(g.cell_hs + cell + 1);
+#pragma unroll 1
     for (int h = h0; h < h1; ++h) {
       const int e = ld(g.hs + h);
       const int sid = hs_sid(e);
       const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, g.surf + sid, x, y, z, u,
                                  v, w);
-      if (d < NT_INF) b.consider(d, l, sid, hs_sense(e));
+      b.consider(d, l, sid, hs_sense(e));        // +inf (no hit) is a no-op
     }
   } else if (!kHex || kind == U_RECT) {
     rect_candidates(g, U, ia, ib, ic, l, x, y, z, u, v, w, b);
@@ -178,7 +179,7 @@ __device__ __forceinline__ void flush_tallies(const KRun& R, double* gl, const u
 
 enum { C_PART = 0, C_SEG, C_CROSS, C_REFL, C_LEAK, C_COLL, C_ABS, C_LOST, C_CAP, C_FLAG, C_CBL0 };
 
-template <bool TRACE, bool STATES>
+template <bool TRACE, bool STATES, bool MESH = false>
 __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
@@ -247,8 +248,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
     }
     if (phase == 1) {
       // ---- Alg. 7 / Alg. 8 descent (single call site for birth and every crossing)
-      const bool ok = descend(g, st, d_l0, d_u, d_Tx, d_Ty, d_Tz, rx, ry, rz, d_fsid, d_fsense, L, mc, flags,
-                              dir_bits(u, v, w));
+      const bool ok = descend(g, st, d_l0, d_u, d_Tx, d_Ty, d_Tz, rx, ry, rz, d_fsid, d_fsense, L, mc, flags);
       if (!ok) {
         flags |= NT_F3;
         term = NT_T_LOST;
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
         emit<TRACE>(R, pid, nseg, NT_EV_COLLIDE, -1, -1, ld(g.mc_cell + mc), -1, 0.0, NT_T_CAPPED, flags);
       } else {
         Best b;
-        b.d = NT_INF; b.d2 = NT_INF; b.l = -1; b.j = -1; b.sense = 0;
+        b.init();
         for (int l = 0; l < L; ++l) level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
         const double sig = ld(g.mc_st + mc);
         const double ds = b.d;
@@ -285,12 +285,12 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           // Alg. 2 "while d < tau/Sigma": tau -= Sigma d, move, cross
           const double s = ds;
           atomicAdd(gl + mc, s);
-          if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
           ++nseg;
-          const int l = b.l, j = b.j;
+          const int l = b.l(), j = b.j();
           const int meta = (l == 0 && g.root_kind == U_CSG) ? ld(g.surf_meta + j) : 0;
           const int bc = meta >> 4;
           if (bc == NT_BC_VACUUM) {
@@ -313,7 +313,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
             p_l = l; p_j = j; p_cb = cell_before; p_s = s;
             if (kind == U_CSG) {   // O9': far side of surface j in universe(l)
               d_l0 = l; d_u = ul; d_Tx = st.T(l, 0); d_Ty = st.T(l, 1); d_Tz = st.T(l, 2);
-              d_fsid = j; d_fsense = b.sense ^ 1;
+              d_fsid = j; d_fsense = b.sense() ^ 1;
               os_l = l; os_s = j;
               phase = 1;
             } else {               // Alg. 6: tile +- 1, then the new tile's daughter
@@ -347,7 +347,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           // ---- collision at tau / Sigma_t: absorb or scatter isotropically (O14, O15)
           const double s = dc;
           atomicAdd(gl + mc, s);
-          if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           ++nseg;
           ++ncoll;
@@ -459,6 +459,10 @@ cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool sta
       return cudaGetLastError();
     });
   };
+  if (R.mesh) {                       // mesh tally: separate instantiations (no call in the others)
+    if (trace) return cudaErrorNotSupported;
+    return states ? pick(k_track_generic<false, true, true>) : pick(k_track_generic<false, false, true>);
+  }
   if (trace) return states ? pick(k_track_generic<true, true>) : pick(k_track_generic<true, false>);
   return states ? pick(k_track_generic<false, true>) : pick(k_track_generic<false, false>);
 }
@@ -485,25 +489,31 @@ cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, boo
       return cudaGetLastError();
     });
   };
-  auto pick_k = [&](auto box, auto tr, auto st) -> cudaError_t {
-    constexpr bool BOX = decltype(box)::value, TR = decltype(tr)::value, ST = decltype(st)::value;
+  auto pick_k = [&](auto box, auto tr, auto st, auto me) -> cudaError_t {
+    constexpr bool BOX = decltype(box)::value, TR = decltype(tr)::value, ST = decltype(st)::value,
+                   ME = decltype(me)::value;
     switch (rg.K) {
-      case 0: return go(k_track_rect<0, BOX, TR, ST>);
-      case 1: return go(k_track_rect<1, BOX, TR, ST>);
-      case 2: return go(k_track_rect<2, BOX, TR, ST>);
-      case 3: return go(k_track_rect<3, BOX, TR, ST>);
-      case 4: return go(k_track_rect<4, BOX, TR, ST>);
+      case 0: return go(k_track_rect<0, BOX, TR, ST, ME>);
+      case 1: return go(k_track_rect<1, BOX, TR, ST, ME>);
+      case 2: return go(k_track_rect<2, BOX, TR, ST, ME>);
+      case 3: return go(k_track_rect<3, BOX, TR, ST, ME>);
+      case 4: return go(k_track_rect<4, BOX, TR, ST, ME>);
       default: return cudaErrorNotSupported;
     }
   };
   using T = std::true_type;
   using F = std::false_type;
-  if (rg.root_box) {
-    if (trace) return states ? pick_k(T{}, T{}, T{}) : pick_k(T{}, T{}, F{});
-    return states ? pick_k(T{}, F{}, T{}) : pick_k(T{}, F{}, F{});
+  if (R.mesh) {                       // mesh tally: separate instantiations, no trace
+    if (trace) return cudaErrorNotSupported;
+    if (rg.root_box) return states ? pick_k(T{}, F{}, T{}, T{}) : pick_k(T{}, F{}, F{}, T{});
+    return states ? pick_k(F{}, F{}, T{}, T{}) : pick_k(F{}, F{}, F{}, T{});
   }
-  if (trace) return states ? pick_k(F{}, T{}, T{}) : pick_k(F{}, T{}, F{});
-  return states ? pick_k(F{}, F{}, T{}) : pick_k(F{}, F{}, F{});
+  if (rg.root_box) {
+    if (trace) return states ? pick_k(T{}, T{}, T{}, F{}) : pick_k(T{}, T{}, F{}, F{});
+    return states ? pick_k(T{}, F{}, T{}, F{}) : pick_k(T{}, F{}, F{}, F{});
+  }
+  if (trace) return states ? pick_k(F{}, T{}, T{}, F{}) : pick_k(F{}, T{}, F{}, F{});
+  return states ? pick_k(F{}, F{}, T{}, F{}) : pick_k(F{}, F{}, F{}, F{});
 }
 
 #else
@@ -533,10 +543,17 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
       return cudaGetLastError();
     });
   };
+  if (R.mesh && trace) return cudaErrorNotSupported;
   if (g.trk) {                     // DP dispatch (virtual tracker calls), block 256 only
     if (block != 256) return cudaErrorInvalidValue;
+    if (R.mesh) return states ? go(k_track_event<256, false, true, true, true>) : go(k_track_event<256, false, false, true, true>);
     if (trace) return states ? go(k_track_event<256, true, true, true>) : go(k_track_event<256, true, false, true>);
     return states ? go(k_track_event<256, false, true, true>) : go(k_track_event<256, false, false, true>);
+  }
+  if (R.mesh) {                    // mesh tally: separate instantiations (no call in the others)
+    if (block == 128) return states ? go(k_track_event<128, false, true, false, true>) : go(k_track_event<128, false, false, false, true>);
+    if (block != 256) return cudaErrorInvalidValue;
+    return states ? go(k_track_event<256, false, true, false, true>) : go(k_track_event<256, false, false, false, true>);
   }
   if (block == 128) {
     if (trace) return states ? go(k_track_event<128, true, true>) : go(k_track_event<128, true, false>);
@@ -578,6 +595,10 @@ cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, 
       return cudaGetLastError();
     });
   };
+  if (R.mesh) {
+    if (trace) return cudaErrorNotSupported;
+    return states ? go(k_track_wq<false, true, true>) : go(k_track_wq<false, false, true>);
+  }
   if (trace) return states ? go(k_track_wq<true, true>) : go(k_track_wq<true, false>);
   return states ? go(k_track_wq<false, true>) : go(k_track_wq<false, false>);
 }

@@ -68,7 +68,7 @@ size_t wq_smem_bytes(const DevGeom& g, bool trace) {
   return head + warp * kWqWarps;
 }
 
-template <bool TRACE, bool STATES>
+template <bool TRACE, bool STATES, bool MESH = false>
 __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, const KRun R) {
   constexpr int S = kWqSlots, W = kWqWarps, B = W * 32;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -223,8 +223,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
             fsense = 0;
           }
         }
-        ok = du >= 0 && descend<false>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags,
-                                       dir_bits(su[slot], sv[slot], sw[slot]));
+        ok = du >= 0 && descend<false>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
         done = true;
         if (!ok) flags |= NT_F3;
         sflags[slot] = static_cast<uint8_t>(flags);
@@ -270,16 +269,16 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
                       NT_T_CAPPED, flags);
         } else {
           Best b;
-          b.d = NT_INF; b.d2 = NT_INF; b.l = -1; b.j = -1; b.sense = 0;
+          b.init();
           double Tx = 0.0, Ty = 0.0, Tz = 0.0;
           int kind_l = 0;                                    // universe kind of the crossing level
           for (int l = 0; l < L; ++l) {
             const DUniv* U = g.univ + st.u(l);
             const int kind = ld(&U->kind);
             const int ia = st.a(l), ib = st.b(l), ic = st.c(l);
-            const int before = b.l;
+            const int before = b.key;
             level_candidates(g, U, kind, ia, ib, ic, l, rx - Tx, ry - Ty, rz - Tz, u, v, w, os_l, os_s, b);
-            if (b.l != before) kind_l = kind;
+            if (b.key != before) kind_l = kind;
             if (l + 1 < L) {
               double tx, ty, tz;
               level_translation(g, U, kind, ia, ib, ic, tx, ty, tz);
@@ -301,7 +300,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
             const bool cross = ds < dc;
             const double s = cross ? ds : dc;
             atomicAdd(gl + mc, s);
-            if (R.mesh) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+            if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
             rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
             ++nseg;
             seg = true;
@@ -309,7 +308,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
             if (cross) {
               const double tt = tau - sig * s;
               tau = tt > 0.0 ? tt : 0.0;
-              const int l = b.l, j = b.j;
+              const int l = b.l(), j = b.j();
               const int meta = (l == 0 && g.root_kind == U_CSG) ? ld(g.surf_meta + j) : 0;
               const int bc = meta >> 4;
               if (bc == NT_BC_VACUUM) {
@@ -329,7 +328,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
                 atomicAdd(s_exit + mc, 1u);
                 lcross = l;
                 if (kind_l == U_CSG) {
-                  sdesc[slot] = l | ((b.sense ^ 1) << 4) | ((j + 1) << 5);
+                  sdesc[slot] = l | ((b.sense() ^ 1) << 4) | ((j + 1) << 5);
                   os_l = l; os_s = j;
                   outc = 3;
                 } else {
@@ -354,11 +353,9 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
         sos[slot] = os_s;
         if (outc == 5) finalize(slot, term);
       }
-      warp_count(seg && (outc == 3 || outc == 4 || lcross == -2), s_cnt + C_CROSS, lane);
       warp_count(outc == 1, s_cnt + C_REFL, lane);
       warp_count(outc == 2, s_cnt + C_COLL, lane);
-      if (__any_sync(0xffffffffu, lcross >= 0))
-        for (int lv = 0; lv < maxd; ++lv) warp_count(lcross == lv, s_cnt + C_CBL0 + lv, lane);
+      if (lcross >= 0) atomicAdd(s_cnt + C_CBL0 + lcross, 1u);   // crossings = leaks + sum over levels (flush)
       mM &= ~warp_or64(valid, slot);
       mM |= warp_or64(outc == 1, slot);
       mC |= warp_or64(outc == 2, slot);
@@ -399,6 +396,12 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
     }
   }
 
+  __syncthreads();
+  if (tid == 0) {                        // crossings = leaks + non-leak crossings at every level
+    unsigned int c = s_cnt[C_LEAK];
+    for (int lv = 0; lv < kMaxDepth; ++lv) c += s_cnt[C_CBL0 + lv];
+    s_cnt[C_CROSS] = c;
+  }
   __syncthreads();
   flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
 }
