@@ -41,20 +41,29 @@ __device__ __forceinline__ void warp_count(bool pred, unsigned int* counter, int
   if (lane == 0 && m) atomicAdd(counter, (unsigned)__popc(m));
 }
 
-size_t event_smem_bytes(const DevGeom& g, int B, bool trace) {
+size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false) {
   const size_t nmc = g.n_mc, d = g.max_depth;
   size_t s = 0;
   s += (7 + 3 * d + (trace ? 1 : 0)) * 8 * (size_t)B;                 // doubles
   s += (6 + 4 * d + (trace ? 2 : 0)) * 4 * (size_t)B;                 // ints
   s += (3 + (trace ? 1 : 0)) * (size_t)B;                             // bytes
   s = (s + 15) & ~size_t(15);
-  s += 3 * NQ * sizeof(QIdx) * (size_t)B;                              // queues (triple-buffered)
+  if (async) s += NQ * sizeof(uint32_t) * (size_t)B;                  // ring queues
+  else s += 3 * NQ * sizeof(QIdx) * (size_t)B;                        // queues (triple-buffered)
   s += (nmc + kNC + 3 * NQ + 4) * 4;                                    // exits, counters, queue counts
   return (s + 15) & ~size_t(15);
 }
 
-// DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh)
-template <int B, bool TRACE, bool STATES, bool DP = false, bool MESH = false>
+__device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
+__device__ __forceinline__ void vstore(uint32_t* p, uint32_t v) { *reinterpret_cast<volatile uint32_t*>(p) = v; }
+
+// DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh).
+// ASYNC = true: no rounds and no block barrier.  Each queue is a ring of B entries with a head
+// and a tail counter in shared memory; a warp claims up to 32 entries of the fullest queue (CAS on
+// the head), runs that EVENT and MOVE on them, and appends every slot to the ring of its next
+// event (warp-aggregated atomic on the tail, entry published after a block fence).  The block
+// ends when the pids are exhausted and no history is live.
+template <int B, bool TRACE, bool STATES, bool DP = false, bool MESH = false, bool ASYNC = false>
 __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -79,18 +88,29 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
   int8_t* spl = sosl + B;                           // TRACE: pending level
   size_t off = (size_t)(reinterpret_cast<unsigned char*>(spl + (TRACE ? B : 0)) - smem);
   off = (off + 15) & ~size_t(15);
-  QIdx* sq = reinterpret_cast<QIdx*>(smem + off);            // [3][NQ][B]
-  unsigned int* s_exit = reinterpret_cast<unsigned int*>(sq + 3 * NQ * B);
+  QIdx* sq = reinterpret_cast<QIdx*>(smem + off);            // [3][NQ][B]        (rounds)
+  uint32_t* ring = reinterpret_cast<uint32_t*>(smem + off);  // [NQ][B] slot + 1, 0 = empty (ASYNC)
+  unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NQ * B)
+                               : reinterpret_cast<unsigned int*>(sq + 3 * NQ * B);
   unsigned int* s_cnt = s_exit + nmc;
   int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [3][NQ]
-  int* s_flag = s_qn + 3 * NQ;                              // [0] = pids exhausted
+  int* s_flag = s_qn + 3 * NQ;                              // [0] = pids exhausted, [1] live (ASYNC)
+  uint32_t* a_head = reinterpret_cast<uint32_t*>(s_qn);      // ASYNC: [NQ] heads, [NQ] tails
+  uint32_t* a_tail = a_head + NQ;
   double* gl = R.slices + (size_t)blockIdx.x * nmc;         // per-block track-length tally (global)
 
   for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
   if (tid < 3 * NQ) s_qn[tid] = 0;
-  if (tid == 0) { s_flag[0] = 0; s_qn[0 * NQ + Q_F] = B; }
-  for (int i = tid; i < B; i += B) sq[(0 * NQ + Q_F) * B + i] = static_cast<QIdx>(i);   // round 0 reads set 0: all slots free
+  if (ASYNC) {
+    for (int i = tid; i < NQ * B; i += B) ring[i] = 0u;
+    __syncthreads();
+    for (int i = tid; i < B; i += B) ring[Q_F * B + i] = static_cast<uint32_t>(i) + 1u;   // all slots free
+    if (tid == 0) { a_tail[Q_F] = B; s_flag[0] = 0; s_flag[1] = 0; }
+  } else {
+    if (tid == 0) { s_flag[0] = 0; s_qn[0 * NQ + Q_F] = B; }
+    for (int i = tid; i < B; i += B) sq[(0 * NQ + Q_F) * B + i] = static_cast<QIdx>(i);   // round 0 reads set 0: all slots free
+  }
   __syncthreads();
 
   auto Q = [&](int p, int q) { return sq + (p * NQ + q) * B; };
@@ -108,27 +128,90 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
     if (R.pnseg) R.pnseg[id] = snseg[slot];
     if (R.pterm) R.pterm[id] = static_cast<uint8_t>(term);
     atomicAdd(s_cnt + C_SEG, snseg[slot]);
+    if (ASYNC) atomicSub(reinterpret_cast<unsigned int*>(s_flag + 1), 1u);   // one history fewer live
   };
 
   for (int round = 0;; ++round) {
     // queues triple-buffered by round: read rd (filled in round-1), append wr, reset rs
     const int rd = round % 3, wr = (round + 1) % 3, rs = (round + 2) % 3;
-    if (tid == 0)
-      for (int k = 0; k < NQ; ++k) QN(rs, k) = 0;          // read in round-1, refilled in round+1
-    const int nmv = QN(rd, Q_M), nco = QN(rd, Q_C), ndc = QN(rd, Q_DC), nda = QN(rd, Q_DA), nfr = QN(rd, Q_F);
-    const int total = nmv + nco + ndc + nda + nfr;
-    for (int base = warp * 32; base < total; base += B) {
+    int nmv = 0, nco = 0, ndc = 0, nda = 0, nfr = 0, total = 32;
+    if (!ASYNC) {
+      if (tid == 0)
+        for (int k = 0; k < NQ; ++k) QN(rs, k) = 0;          // read in round-1, refilled in round+1
+      nmv = QN(rd, Q_M); nco = QN(rd, Q_C); ndc = QN(rd, Q_DC); nda = QN(rd, Q_DA); nfr = QN(rd, Q_F);
+      total = nmv + nco + ndc + nda + nfr;
+    }
+    for (int base = ASYNC ? 0 : warp * 32; base < total; base += B) {
       const int i = base + lane;
-      const bool valid = i < total;
       // kind: 5 move only (reflected), 4 collide, 0 CSG descent, 1 array descent, 2 birth, 3 none
       int slot = 0, kind = 3;
-      if (valid) {
+      bool valid = i < total;
+      if constexpr (ASYNC) {
+        // ---- claim up to 32 entries of the fullest queue (lane 0), or finish
+        int q = -1;
+        uint32_t h = 0, take = 0;
+        if (lane == 0) {
+          for (;;) {
+            int best = -1;
+            uint32_t bh = 0, bav = 0;
+            const bool births = vload(reinterpret_cast<uint32_t*>(s_flag)) == 0u;
+#pragma unroll
+            for (int k = 0; k < NQ; ++k) {
+              if (k == Q_F && !births) continue;
+              const uint32_t hk = vload(a_head + k), av = vload(a_tail + k) - hk;
+              if (av > bav) { bav = av; best = k; bh = hk; }
+            }
+            if (best >= 0) {
+              const uint32_t tk = bav < 32u ? bav : 32u;
+              if (atomicCAS(a_head + best, bh, bh + tk) == bh) { q = best; h = bh; take = tk; break; }
+              continue;
+            }
+            if (!births && vload(reinterpret_cast<uint32_t*>(s_flag + 1)) == 0u) break;   // all done
+            __nanosleep(64);
+          }
+        }
+        q = __shfl_sync(0xffffffffu, q, 0);
+        if (q < 0) break;
+        h = __shfl_sync(0xffffffffu, h, 0);
+        take = __shfl_sync(0xffffffffu, take, 0);
+        valid = static_cast<uint32_t>(lane) < take;
+        if (valid) {
+          uint32_t* e = ring + q * B + ((h + lane) & (B - 1));
+          uint32_t v;
+          while ((v = vload(e)) == 0u) {}
+          vstore(e, 0u);
+          slot = static_cast<int>(v) - 1;
+          kind = (0x21045 >> (4 * q)) & 15;          // Q_M, Q_C, Q_DC, Q_DA, Q_F -> kinds 5, 4, 0, 1, 2
+        }
+        __threadfence_block();
+      } else if (valid) {
         if (i < nmv) { slot = Q(rd, Q_M)[i]; kind = 5; }
         else if (i < nmv + nco) { slot = Q(rd, Q_C)[i - nmv]; kind = 4; }
         else if (i < nmv + nco + ndc) { slot = Q(rd, Q_DC)[i - nmv - nco]; kind = 0; }
         else if (i < nmv + nco + ndc + nda) { slot = Q(rd, Q_DA)[i - nmv - nco - ndc]; kind = 1; }
         else { slot = Q(rd, Q_F)[i - nmv - nco - ndc - nda]; kind = 2; }
       }
+      // append this lane's slot to queue q of the next event (warp-aggregated)
+      auto push = [&](int qq, bool pred) {
+        if constexpr (ASYNC) {
+          const unsigned m = __ballot_sync(0xffffffffu, pred);
+          if (m) {
+            const int leader = __ffs(m) - 1;
+            uint32_t base2 = 0;
+            if (lane == leader) base2 = atomicAdd(a_tail + qq, static_cast<uint32_t>(__popc(m)));
+            base2 = __shfl_sync(0xffffffffu, base2, leader);
+            if (pred) {
+              __threadfence_block();                               // slot state before the entry
+              uint32_t* e = ring + qq * B + ((base2 + __popc(m & ((1u << lane) - 1u))) & (B - 1));
+              while (vload(e) != 0u) {}                            // previous lap consumed
+              vstore(e, static_cast<uint32_t>(slot) + 1u);
+            }
+          }
+        } else {
+          const int pos = warp_append(pred, &QN(wr, qq), lane);
+          if (pos >= 0) Q(wr, qq)[pos] = static_cast<QIdx>(slot);
+        }
+      };
       // ---------------- EVENT: change_direction / descent / birth of this chunk's slots
         // births: claim pids for this warp's birth lanes (warp-aggregated)
         const unsigned bm = __ballot_sync(0xffffffffu, kind == 2);
@@ -142,6 +225,10 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
             const unsigned long long id = b0 + __popc(bm & ((1u << lane) - 1u));
             if (id < R.n) { born = true; sidx[slot] = static_cast<uint32_t>(id); }
             else s_flag[0] = 1;                          // pids exhausted: slot stays unused
+          }
+          if (ASYNC) {
+            const unsigned nb = __ballot_sync(0xffffffffu, born);
+            if (lane == leader && nb) atomicAdd(reinterpret_cast<unsigned int*>(s_flag + 1), static_cast<unsigned>(__popc(nb)));
           }
         }
         bool ok = false, done = false, scat = false, absorbed = false;
@@ -257,10 +344,7 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
           if (!ok) finalize(slot, NT_T_LOST);
         }
       const bool ready = kind == 5 || (done && ok) || scat;
-      {
-        const int pf = warp_append((done && !ok) || absorbed, &QN(wr, Q_F), lane);
-        if (pf >= 0) Q(wr, Q_F)[pf] = static_cast<QIdx>(slot);
-      }
+      push(Q_F, (done && !ok) || absorbed);
       // ---------------- MOVE the same slots (no barrier between a slot's event and its move)
       {
         // outcome: 0 none, 1 reflect (-> M), 2 collide, 3 CSG descent, 4 array descent, 5 ended
@@ -364,19 +448,15 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
         warp_count(outc == 2, s_cnt + C_COLL, lane);
         if (lcross >= 0) atomicAdd(s_cnt + C_CBL0 + lcross, 1u);   // crossings = leaks + sum over levels (flush)
         // enqueue for the next event
-        int pos;
-        pos = warp_append(outc == 1, &QN(wr, Q_M), lane);
-        if (pos >= 0) Q(wr, Q_M)[pos] = static_cast<QIdx>(slot);
-        pos = warp_append(outc == 2, &QN(wr, Q_C), lane);
-        if (pos >= 0) Q(wr, Q_C)[pos] = static_cast<QIdx>(slot);
-        pos = warp_append(outc == 3, &QN(wr, Q_DC), lane);
-        if (pos >= 0) Q(wr, Q_DC)[pos] = static_cast<QIdx>(slot);
-        pos = warp_append(outc == 4, &QN(wr, Q_DA), lane);
-        if (pos >= 0) Q(wr, Q_DA)[pos] = static_cast<QIdx>(slot);
-        pos = warp_append(outc == 5, &QN(wr, Q_F), lane);
-        if (pos >= 0) Q(wr, Q_F)[pos] = static_cast<QIdx>(slot);
+        push(Q_M, outc == 1);
+        push(Q_C, outc == 2);
+        push(Q_DC, outc == 3);
+        push(Q_DA, outc == 4);
+        push(Q_F, outc == 5);
       }
+      if (ASYNC) base -= B;                       // ASYNC: keep claiming until the block is done
     }
+    if (ASYNC) break;
     __syncthreads();
     // termination: no live history queued for the next round and no more pids
     if (QN(wr, Q_M) + QN(wr, Q_C) + QN(wr, Q_DC) + QN(wr, Q_DA) == 0 && s_flag[0]) break;

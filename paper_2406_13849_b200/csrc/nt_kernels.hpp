@@ -33,7 +33,7 @@ cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool sta
 cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states, \
                         int block, int blocks_per_sm, cudaStream_t stream, int* grid_out); \
 cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block, \
-                         int blocks_per_sm, cudaStream_t stream, int* grid_out); \
+                         int blocks_per_sm, cudaStream_t stream, int* grid_out, bool async = false); \
 cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, int blocks_per_sm, \
                       cudaStream_t stream, int* grid_out); \
 cudaError_t dp_init(const DevGeom& g, void* objs, void* tab, cudaStream_t stream); \

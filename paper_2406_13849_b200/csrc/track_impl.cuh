@@ -523,8 +523,8 @@ cudaError_t launch_rect(const DevGeom&, const RectGeom&, const KRun&, bool, bool
 #endif
 
 cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
-                         int blocks_per_sm, cudaStream_t stream, int* grid_out) {
-  const size_t smem = event_smem_bytes(g, block, trace);
+                         int blocks_per_sm, cudaStream_t stream, int* grid_out, bool async) {
+  const size_t smem = event_smem_bytes(g, block, trace, async);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -544,6 +544,12 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
     });
   };
   if (R.mesh && trace) return cudaErrorNotSupported;
+  if (async) {                     // barrier-free ring queues (block 256, SP dispatch)
+    if (block != 256 || g.trk) return cudaErrorInvalidValue;
+    if (R.mesh) return states ? go(k_track_event<256, false, true, false, true, true>) : go(k_track_event<256, false, false, false, true, true>);
+    if (trace) return states ? go(k_track_event<256, true, true, false, false, true>) : go(k_track_event<256, true, false, false, false, true>);
+    return states ? go(k_track_event<256, false, true, false, false, true>) : go(k_track_event<256, false, false, false, false, true>);
+  }
   if (g.trk) {                     // DP dispatch (virtual tracker calls), block 256 only
     if (block != 256) return cudaErrorInvalidValue;
     if (R.mesh) return states ? go(k_track_event<256, false, true, true, true>) : go(k_track_event<256, false, false, true, true>);
