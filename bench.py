@@ -36,7 +36,7 @@ def _args():
     ap.add_argument("--config", default="c3")
     ap.add_argument("--particles", type=float, default=None, help="histories per GPU per step")
     ap.add_argument("--tracker", default="generic", choices=["generic", "rect"])
-    ap.add_argument("--scheduler", default="block", choices=["block", "warp", "history", "dp", "async"])
+    ap.add_argument("--scheduler", default="block", choices=["block", "rounds", "warp", "history", "dp", "dp-rounds"])
     ap.add_argument("--pseudo-array", action="store_true")
     ap.add_argument("--block-dim", type=int, default=0)
     ap.add_argument("--blocks-per-sm", type=int, default=0)

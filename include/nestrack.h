@@ -85,11 +85,12 @@ typedef enum { NT_TRACKER_GENERIC = 0, NT_TRACKER_RECT = 1 } nt_tracker;
  * tracker, block queues (not NT_HISTORY / NT_WARPQ) and block_dim 0 or 256, else NT_E_ARG.
  * ST (pseudo-array universes) is the build option nt_build_opts.pseudo_array.   */
 #define NT_DP 8u
-/* NT_ASYNC: block queues without rounds or block barriers -- each queue is a ring in shared memory,
- * a warp claims up to 32 entries of the fullest ring, runs that event and the move, and appends
- * each slot to the ring of its next event.  Results are identical.  Same restrictions as NT_DP
- * (generic tracker, block queues, block_dim 0 or 256) and SP dispatch only, else NT_E_ARG.     */
-#define NT_ASYNC 16u
+/* Block queues run without rounds or block barriers by default: each event queue is a ring in
+ * shared memory, a warp claims up to 32 entries of the fullest ring, runs that event and the move,
+ * and appends each slot to the ring of its next event.  NT_ROUNDS selects the earlier round-based
+ * form instead (every warp takes one 32-slot chunk per round, one block barrier per round); runs
+ * with block_dim 128 always use rounds.  Results are identical.                                */
+#define NT_ROUNDS 16u
 
 /* Per-particle flag bits written to outputs.pflags (reading O16):
  *   F1: a cell/tile chosen by a descent has another surface within 1e-10 cm

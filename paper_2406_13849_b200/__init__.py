@@ -22,10 +22,12 @@ NT_TRACE = 1
 NT_HISTORY = 2
 NT_WARPQ = 4
 NT_DP = 8
-NT_ASYNC = 16
-# "dp": block queues with dynamic-polymorphism dispatch (virtual tracker calls);
-# "async": block queues as shared-memory rings, no rounds / barriers
-SCHEDULERS = {"block": 0, "event": 0, "warp": NT_WARPQ, "history": NT_HISTORY, "dp": NT_DP, "async": NT_ASYNC}
+NT_ROUNDS = 16
+# "block": block queues as shared-memory rings, no rounds / barriers (default); "rounds": the
+# round-based form with one block barrier per round; "dp" / "dp-rounds": dynamic-polymorphism
+# dispatch (virtual tracker calls) in either form
+SCHEDULERS = {"block": 0, "event": 0, "rounds": NT_ROUNDS, "warp": NT_WARPQ, "history": NT_HISTORY,
+              "dp": NT_DP, "dp-rounds": NT_DP | NT_ROUNDS}
 COUNTERS = ["particles", "segments", "crossings", "reflections", "leaks", "collisions",
             "absorptions", "lost", "capped", "flagged"] + [f"cross_l{i}" for i in range(8)]
 NC = len(COUNTERS)

@@ -425,8 +425,9 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   if (trace && o->mesh && m->mesh_on)
     return err(NT_E_UNSUPPORTED, std::string(who) + ": the mesh tally cannot be combined with NT_TRACE");
   const bool dp = (run->flags & NT_DP) != 0;
-  if ((run->flags & NT_ASYNC) && (dp || run->tracker != NT_TRACKER_GENERIC || (run->flags & (NT_WARPQ | NT_HISTORY)) || block != 256))
-    return err(NT_E_ARG, std::string(who) + ": NT_ASYNC needs the generic tracker, block queues, SP dispatch and block_dim 256");
+  // block queues: ring queues without rounds (default, block 256) or rounds + barrier (NT_ROUNDS,
+  // also every block_dim 128 run)
+  const bool async = !(run->flags & NT_ROUNDS) && block == 256;
   if (dp && (run->tracker != NT_TRACKER_GENERIC || (run->flags & (NT_WARPQ | NT_HISTORY)) || block != 256))
     return err(NT_E_ARG, std::string(who) + ": NT_DP needs the generic tracker, block queues and block_dim 256");
   m->last_launches = 0;
@@ -486,8 +487,8 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
       e = f0 ? f0::launch_wq(m->g, R, trace, st, run->blocks_per_sm, s, &grid)
              : f7::launch_wq(m->g, R, trace, st, run->blocks_per_sm, s, &grid);
     else
-      e = f0 ? f0::launch_event(g, R, trace, st, block, run->blocks_per_sm, s, &grid, (run->flags & NT_ASYNC) != 0)
-             : f7::launch_event(g, R, trace, st, block, run->blocks_per_sm, s, &grid, (run->flags & NT_ASYNC) != 0);
+      e = f0 ? f0::launch_event(g, R, trace, st, block, run->blocks_per_sm, s, &grid, async)
+             : f7::launch_event(g, R, trace, st, block, run->blocks_per_sm, s, &grid, async);
   }
   if (prev != m->device) cudaSetDevice(prev);
   if (e != cudaSuccess) return cuda_err(e, who);

@@ -544,11 +544,15 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
     });
   };
   if (R.mesh && trace) return cudaErrorNotSupported;
-  if (async) {                     // barrier-free ring queues (block 256, SP dispatch)
-    if (block != 256 || g.trk) return cudaErrorInvalidValue;
-    if (R.mesh) return states ? go(k_track_event<256, false, true, false, true, true>) : go(k_track_event<256, false, false, false, true, true>);
-    if (trace) return states ? go(k_track_event<256, true, true, false, false, true>) : go(k_track_event<256, true, false, false, false, true>);
-    return states ? go(k_track_event<256, false, true, false, false, true>) : go(k_track_event<256, false, false, false, false, true>);
+  if (async) {                     // barrier-free ring queues (block 256), SP or DP dispatch
+    if (block != 256) return cudaErrorInvalidValue;
+    auto pick = [&](auto dp) -> cudaError_t {
+      constexpr bool D = decltype(dp)::value;
+      if (R.mesh) return states ? go(k_track_event<256, false, true, D, true, true>) : go(k_track_event<256, false, false, D, true, true>);
+      if (trace) return states ? go(k_track_event<256, true, true, D, false, true>) : go(k_track_event<256, true, false, D, false, true>);
+      return states ? go(k_track_event<256, false, true, D, false, true>) : go(k_track_event<256, false, false, D, false, true>);
+    };
+    return g.trk ? pick(std::true_type{}) : pick(std::false_type{});
   }
   if (g.trk) {                     // DP dispatch (virtual tracker calls), block 256 only
     if (block != 256) return cudaErrorInvalidValue;

@@ -10,8 +10,9 @@ timeout 900 python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.er
 timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref_$R.json 2> gpurun_out/bench_ref_$R.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu_launches_$R.csv \
     python bench.py --no-cpu-baseline --no-e2e --no-ratio > gpurun_out/ncu_launches_bench_$R.log 2>&1
-timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_track_event -s 3 -c 1 -o /tmp/prof_bench_$R \
+timeout 2400 ncu --set full --clock-control none --import-source on -k regex:k_track_event -s 3 -c 1 -o /tmp/prof_bench_$R \
     python bench.py --no-cpu-baseline --no-e2e --no-ratio --steps 1 --warmup 3 > gpurun_out/ncu_full_bench_$R.log 2>&1
 ncu -i /tmp/prof_bench_$R.ncu-rep --page raw --csv > gpurun_out/ncu_full_$R.raw.csv 2>/dev/null
 ncu -i /tmp/prof_bench_$R.ncu-rep --page details > gpurun_out/ncu_full_$R.details.txt 2>/dev/null
+ncu -i /tmp/prof_bench_$R.ncu-rep --page source --csv --print-source sass > gpurun_out/ncu_full_$R.sass.csv 2>/dev/null
 echo done

@@ -68,7 +68,7 @@ def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, t
 CONFIG_N = {"c1": 2000, "c2": 600, "c3": 600, "c4": 600, "c5m": 600, "c5r": 600}
 
 
-@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp", "async"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp", "rounds", "dp-rounds"])
 @pytest.mark.parametrize("cfg", list(CONFIG_N))
 def test_config_trace_parity(nt, orc, cfg, sched):
     """Every BASELINE config: full traces bit-exact vs the oracle (seeded, small batch), with
@@ -87,7 +87,7 @@ def test_c3_parity_seeds(nt, orc, seed):
 @pytest.mark.parametrize("name", ["sphere_in_box", "hex_pins_small_pointy", "hex_pins_small_flat",
                                   "rect3d_small", "lattice3_nested", "lattice3_flat", "infinite_medium",
                                   "c1_void_vacuum"])
-@pytest.mark.parametrize("sched", ["block", "dp", "async"])
+@pytest.mark.parametrize("sched", ["block", "dp", "rounds"])
 def test_test_models_parity(nt, orc, name, sched):
     """Planes, spheres, 3-D rect and hex z-stacks, translations, void + vacuum leakage."""
     M = workloads.models
@@ -104,7 +104,7 @@ NONUNIFORM = {"gap_lattice": lambda: workloads.models.gap_lattice(True),
               "nonuniform_slabs": lambda: workloads.models.nonuniform_slabs()}
 
 
-@pytest.mark.parametrize("sched", ["block", "warp", "history", "dp", "async"])
+@pytest.mark.parametrize("sched", ["block", "warp", "history", "dp", "rounds"])
 @pytest.mark.parametrize("name", list(NONUNIFORM))
 def test_nonuniform_rect_parity(nt, orc, name, sched):
     """Non-uniform rect arrays (Alg. 5 binary search, reading N1): traces bit-exact vs the oracle
@@ -144,7 +144,7 @@ MESHED = {
 }
 
 
-@pytest.mark.parametrize("sched", ["block", "warp", "history", "dp", "async", "rect"])
+@pytest.mark.parametrize("sched", ["block", "warp", "history", "dp", "rounds", "rect"])
 @pytest.mark.parametrize("name", list(MESHED))
 def test_mesh_tally_parity(nt, orc, name, sched):
     """Superimposed mesh track-length tally (NEXT-2, reading M1): per-voxel totals vs the oracle's
@@ -202,7 +202,7 @@ def test_ragged_batches_and_large_pids(nt, orc, n, block):
     _compare(nt, orc, spec, n, seed=3, pid_begin=(1 << 33) + 17, scheduler="warp")
 
 
-@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp", "async"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp", "rounds"])
 def test_capped_histories(nt, orc, sched):
     """max_segments reached -> CAPPED (F3) on both sides, same extra trace record."""
     spec, _ = workloads.config("c1")
@@ -210,7 +210,7 @@ def test_capped_histories(nt, orc, sched):
     assert g["counters"]["capped"] > 0
 
 
-@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp", "async"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp", "rounds"])
 def test_lost_at_birth(nt, orc, sched):
     """Births outside every root cell are LOST at birth (source box larger than the model)."""
     spec = workloads.c1_pincell()
@@ -219,7 +219,7 @@ def test_lost_at_birth(nt, orc, sched):
     assert g["counters"]["lost"] > 0
 
 
-@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp", "async"])
+@pytest.mark.parametrize("sched", ["warp", "block", "history", "dp", "rounds"])
 def test_explicit_states(nt, orc, sched):
     """nt_track_states: explicit birth states (chord rays through the void pincell)."""
     spec = workloads.c1_pincell(bc="vacuum", void=True)
