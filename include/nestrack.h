@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define NT_ABI_VERSION 2
+#define NT_ABI_VERSION 3
 
 typedef enum {
     NT_OK = 0,
@@ -224,9 +224,18 @@ typedef struct {
     int64_t out_len;              /* 2*n_material_cells + NT_NC */
     size_t device_bytes;          /* size of the device geometry blob */
     int64_t mesh_bins;            /* voxels of the mesh set by nt_set_mesh (0: none) */
+    int64_t n_instances;          /* material-cell instances (reading D1); 0 for pseudo-array
+                                     builds or more than 2^31 - 1 instances (no instance tallies) */
 } nt_model_info;
 
 nt_status nt_model_info_get(const nt_model* m, nt_model_info* info);
+
+/* Per-instance tallies (reading D1): material-cell instances are numbered by a depth-first
+ * enumeration of the model -- a CSG universe's cells in id order (a material cell is one
+ * instance, a fill cell contributes its universe's instances), an array's tiles in fill order,
+ * then its outer universe once.  out[i] = material-cell bin of instance i; writes
+ * min(cap, n_instances) entries.  NT_E_ORDER before nt_finalize. */
+nt_status nt_instance_cells(const nt_model* m, int32_t* out, int64_t cap);
 
 /* Tally bin b (0 <= b < n_material_cells) -> global cell id, ascending; writes min(cap, n). */
 nt_status nt_material_cell_ids(const nt_model* m, int32_t* out, int32_t cap);
@@ -259,6 +268,10 @@ typedef struct {
     double* mesh;             /* device, optional (NULL = no mesh tally): per-voxel track length of the
                                  model's mesh (nt_set_mesh), x fastest, accumulated; ignored when the
                                  model has no mesh */
+    double* inst;             /* device, optional (NULL = none): track length per material-cell instance
+                                 (distributed-cell tally, reading D1), n_instances entries,
+                                 accumulated.  Generic tracker, no NT_TRACE, no pseudo-array build,
+                                 else NT_E_UNSUPPORTED */
 } nt_outputs;
 
 /* Track run->n histories born from (seed, pid) in the source box. Asynchronous on cuda_stream. */

@@ -66,8 +66,12 @@ def lib():
             getattr(L, f).argtypes = [vp]
         L.orc_material_cell_ids.argtypes = [vp, dp]
         L.orc_cell_material.argtypes = [vp, i32]
-        L.orc_run.argtypes = [vp, u64, u64, u64, dp, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp]
-        L.orc_run_states.argtypes = [vp, u64, u64, u64, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp]
+        L.orc_run.argtypes = [vp, u64, u64, u64, dp, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp]
+        L.orc_run_states.argtypes = [vp, u64, u64, u64, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp]
+        L.orc_n_instances.argtypes = [vp]
+        L.orc_n_instances.restype = C.c_long
+        L.orc_instance_cells.argtypes = [vp, dp]
+        L.orc_instance_cells.restype = C.c_long
         L.orc_set_mesh.argtypes = [vp, dp, dp, dp]
         L.orc_find_cells.argtypes = [vp, dp, u64, dp, dp]
         L.orc_count_containing.argtypes = [vp, i32, dp]
@@ -195,9 +199,11 @@ class OracleModel:
     # ------------------------------------------------------------------ runs
     def run(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
             max_segments: int = 1_000_000, threads: int | None = None, pflags: bool = False,
-            trace_cap: int = 0, states: np.ndarray | None = None, mesh: bool = False):
+            trace_cap: int = 0, states: np.ndarray | None = None, mesh: bool = False,
+            instances: bool = False):
         """Track particles [pid_begin, pid_begin+n).  Returns dict with out, counters, ...
-        mesh=True (model spec with a "mesh"): res["mesh"] = per-voxel track length, x fastest."""
+        mesh=True (model spec with a "mesh"): res["mesh"] = per-voxel track length, x fastest.
+        instances=True: res["inst"] = track length per material-cell instance (reading D1)."""
         if threads is None:
             threads = len(os.sched_getaffinity(0))
         out = np.zeros(self.out_len)
@@ -209,6 +215,7 @@ class OracleModel:
         if mesh:
             assert self.mesh_shape is not None, "model has no mesh"
             mo = np.zeros(int(np.prod(self.mesh_shape)))
+        io = np.zeros(max(self.n_instances(), 1)) if instances else None
         if states is None:
             src = self.spec["source"]
             lo = np.asarray(src["lo"] if lo is None else lo, dtype=np.float64)
@@ -216,19 +223,22 @@ class OracleModel:
             rc = self.L.orc_run(self.h, seed, pid_begin, n, _p(lo), _p(hi), max_segments, threads,
                                 _p(out), _p(pf) if pf is not None else None,
                                 _p(tr) if tr is not None else None, trace_cap, _p(tcount), _p(ev),
-                                _p(mo) if mo is not None else None)
+                                _p(mo) if mo is not None else None, _p(io) if io is not None else None)
         else:
             st = np.ascontiguousarray(states, dtype=np.float64)
             assert st.shape == (6, n)
             rc = self.L.orc_run_states(self.h, seed, pid_begin, n, _p(st), max_segments, threads,
                                        _p(out), _p(pf) if pf is not None else None,
                                        _p(tr) if tr is not None else None, trace_cap, _p(tcount),
-                                       _p(ev), _p(mo) if mo is not None else None)
+                                       _p(ev), _p(mo) if mo is not None else None,
+                                       _p(io) if io is not None else None)
         assert rc == 0
         res = self.unpack(out)
         res["evals"] = {k: int(ev[i]) for i, k in enumerate(EVAL_KINDS)}
         if mo is not None:
             res["mesh"] = mo
+        if io is not None:
+            res["inst"] = io[:self.n_instances()]
         if pf is not None:
             res["pflags"] = pf[:n]
         if tr is not None:
@@ -237,6 +247,16 @@ class OracleModel:
             t = tr[:cnt]
             res["trace"] = np.sort(t, order=["pid", "seg", "terminal"])
         return res
+
+    def n_instances(self) -> int:
+        """Material-cell instances in the model (reading D1)."""
+        return int(self.L.orc_n_instances(self.h))
+
+    def instance_cells(self) -> np.ndarray:
+        """Material-cell index of every instance, by explicit depth-first enumeration (D1)."""
+        out = np.zeros(max(self.n_instances(), 1), dtype=np.int32)
+        self.L.orc_instance_cells(self.h, _p(out))
+        return out[:self.n_instances()]
 
     def unpack(self, out: np.ndarray) -> dict:
         n = self.n_mc

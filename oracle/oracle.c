@@ -20,6 +20,10 @@
  *     every segment's [0, s] is cut at every mesh-plane crossing, the cut
  *     parameters are sorted, and each piece goes to the voxel that holds its
  *     midpoint (found by the same explicit search as a rect index).
+ *   - per-instance (distributed-cell) tallies (NEXT-3; reading
+ *     D1): the instance of a material cell is its position in the depth-first
+ *     enumeration of all material-cell instances; counted by summing the leaves
+ *     of every earlier sibling at every level.
  *   - non-uniform rect arrays (Alg. 5, P:513-525 and its footnote P:500-505):
  *     the tile is found by a linear scan over the mesh divisions (reading N1
  *     in DESIGN.md: index -1 below the first edge, n at or above the last).
@@ -95,6 +99,7 @@ typedef struct {
     /* superimposed Cartesian mesh (M1): voxel edges lo + i * d per axis, n[a] voxels */
     int mesh_on, mesh_n[3];
     double mesh_lo[3], mesh_d[3];
+    long *leaves;                /* D1: material-cell instances below each universe (finalize) */
     int *mc_cell;                /* mc index -> global cell id */
 } Model;
 
@@ -111,7 +116,7 @@ void orc_model_free(void *vm) {
         free(m->u[i].cells); free(m->u[i].fill); free(m->u[i].hexmap);
         for (int a = 0; a < 3; ++a) free(m->u[i].e[a]);
     }
-    free(m->s); free(m->m); free(m->c); free(m->u); free(m->mc_cell); free(m);
+    free(m->s); free(m->m); free(m->c); free(m->u); free(m->mc_cell); free(m->leaves); free(m);
 }
 
 int orc_add_surface(void *vm, int kind, const double *coef, int bc) {
@@ -282,6 +287,26 @@ static int depth_of(Model *m, int u, int guard) {
     return best;
 }
 
+/* D1: number of material-cell instances below universe u in the depth-first enumeration: a CSG
+ * universe's cells in id order (a material cell is one instance, a fill cell contributes its
+ * universe's instances), an array's tiles in fill order and then its outer universe once. */
+static long leaves_of(Model *m, int u) {
+    if (m->leaves[u] >= 0) return m->leaves[u];
+    const Univ *U = &m->u[u];
+    long n = 0;
+    if (U->kind == U_CSG) {
+        for (int i = 0; i < U->ncells; ++i) {
+            const Cell *c = &m->c[U->cells[i]];
+            n += c->fill_kind == FILL_MAT ? 1 : leaves_of(m, c->fill);
+        }
+    } else {
+        for (int i = 0; i < U->nfill; ++i) n += leaves_of(m, U->fill[i]);
+        if (U->outer >= 0) n += leaves_of(m, U->outer);
+    }
+    m->leaves[u] = n;
+    return n;
+}
+
 int orc_finalize(void *vm) {
     Model *m = vm;
     if (m->root < 0 || m->root >= m->nu) return -1;
@@ -301,6 +326,10 @@ int orc_finalize(void *vm) {
     }
     m->max_depth = depth_of(m, m->root, 0);
     if (m->max_depth > MAXD) return -6;
+    free(m->leaves);
+    m->leaves = malloc(sizeof(long) * (size_t)(m->nu + 1));
+    for (int i = 0; i < m->nu; ++i) m->leaves[i] = -1;
+    for (int i = 0; i < m->nu; ++i) leaves_of(m, i);
     /* material cells get dense tally indices in global cell-id order (O20) */
     free(m->mc_cell);
     m->mc_cell = malloc(sizeof(int) * (size_t)(m->nc + 1));
@@ -776,6 +805,7 @@ static void neu_add(Neu *a, double x) {        /* Neumaier compensated summation
 typedef struct {
     Neu *len; uint64_t *exits; uint64_t cnt[NCOUNT]; uint64_t ev[NEVAL];
     Neu *mesh;                   /* per-voxel track length (M1), NULL when not tallied */
+    Neu *inst;                   /* per-instance track length (D1), NULL when not tallied */
 } Acc;
 
 typedef struct {
@@ -784,6 +814,7 @@ typedef struct {
     const double *states;    /* optional explicit births: SoA 6 x n */
     uint8_t *pflags; TraceRec *trace; uint64_t trace_cap; uint64_t *trace_count;
     double *mesh_out;        /* optional per-voxel track length (M1), accumulated */
+    double *inst_out;        /* optional per-instance track length (D1), accumulated */
 } RunCtx;
 
 static void emit(const RunCtx *R, uint64_t pid, uint32_t seg, int kind, int level, int j, int cb,
@@ -797,6 +828,61 @@ static void emit(const RunCtx *R, uint64_t pid, uint32_t seg, int kind, int leve
     memset(t, 0, sizeof(*t));
     t->pid = pid; t->s = s; t->seg = seg; t->cell_before = cb; t->cell_after = ca; t->j = j;
     t->kind = (uint8_t)kind; t->level = (int8_t)level; t->terminal = (uint8_t)terminal; t->flags = flags;
+}
+
+/* D1: the instance index of the material cell reached by the stack S[0 .. depth-1]: the number
+ * of instances that precede it in the enumeration, i.e. the leaves of every earlier sibling at
+ * every level (earlier cells of the CSG universe, earlier tiles of the array; the outer universe
+ * comes after every tile). */
+static long instance_of(const Model *m, const Level *S, int depth) {
+    long inst = 0;
+    for (int l = 0; l < depth; ++l) {
+        const Univ *U = &m->u[S[l].u];
+        if (U->kind == U_CSG) {
+            for (int i = 0; i < U->ncells && U->cells[i] != S[l].cell; ++i) {
+                const Cell *c = &m->c[U->cells[i]];
+                inst += c->fill_kind == FILL_MAT ? 1 : m->leaves[c->fill];
+            }
+        } else {
+            int idx;
+            if (U->kind == U_RECT) {
+                int in = S[l].i >= 0 && S[l].i < U->n[0] && S[l].j >= 0 && S[l].j < U->n[1] &&
+                         (U->is2d || (S[l].k >= 0 && S[l].k < U->n[2]));
+                idx = in ? S[l].i + U->n[0] * (S[l].j + U->n[1] * (U->is2d ? 0 : S[l].k)) : U->nfill;
+            } else {
+                int R = U->rings - 1, W = 2 * R + 1, q = S[l].i, r = S[l].j, kz = S[l].k;
+                int a = abs(q), b = abs(r), c = abs(q + r);
+                int d = a > b ? a : b; d = d > c ? d : c;
+                int in = d <= R && (U->nz == 0 || (kz >= 0 && kz < U->nz));
+                idx = in ? U->hexmap[(r + R) * W + (q + R)] + (U->nz > 0 ? kz * (U->nfill / U->nz) : 0) : U->nfill;
+            }
+            for (int t = 0; t < idx; ++t) inst += m->leaves[U->fill[t]];
+        }
+    }
+    return inst;
+}
+
+/* D1: the enumeration itself, by explicit depth-first recursion: out[i] = material-cell index of
+ * instance i. */
+static long enumerate_leaves(const Model *m, int u, int32_t *out, long pos) {
+    const Univ *U = &m->u[u];
+    if (U->kind == U_CSG) {
+        for (int i = 0; i < U->ncells; ++i) {
+            const Cell *c = &m->c[U->cells[i]];
+            if (c->fill_kind == FILL_MAT) out[pos++] = c->mc;
+            else pos = enumerate_leaves(m, c->fill, out, pos);
+        }
+    } else {
+        for (int i = 0; i < U->nfill; ++i) pos = enumerate_leaves(m, U->fill[i], out, pos);
+        if (U->outer >= 0) pos = enumerate_leaves(m, U->outer, out, pos);
+    }
+    return pos;
+}
+
+long orc_n_instances(void *vm) { Model *m = vm; return m->finalized ? m->leaves[m->root] : -1; }
+long orc_instance_cells(void *vm, int32_t *out) {
+    Model *m = vm;
+    return m->finalized ? enumerate_leaves(m, m->root, out, 0) : -1;
 }
 
 /* M1: mesh plane i of axis a */
@@ -914,6 +1000,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
             double s = ds;
             neu_add(&A->len[mc], s);
             mesh_score(m, A, r, om, s);
+            if (A->inst) neu_add(&A->inst[instance_of(m, S, depth)], s);
             for (int a = 0; a < 3; ++a) r[a] = r[a] + s * om[a];
             double tt = tau - M->st * s;
             tau = tt > 0.0 ? tt : 0.0;                            /* O12 */
@@ -990,6 +1077,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
             double s = dc;
             neu_add(&A->len[mc], s);
             mesh_score(m, A, r, om, s);
+            if (A->inst) neu_add(&A->inst[instance_of(m, S, depth)], s);
             for (int a = 0; a < 3; ++a) r[a] = r[a] + s * om[a];
             nseg++;
             A->cnt[C_COLLISIONS]++;
@@ -1023,7 +1111,7 @@ done:
 static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *lo,
                       const double *hi, const double *states, uint64_t max_seg, int nthreads,
                       double *out, uint8_t *pflags, void *trace, uint64_t trace_cap,
-                      uint64_t *trace_count, uint64_t *evals, double *mesh_out) {
+                      uint64_t *trace_count, uint64_t *evals, double *mesh_out, double *inst_out) {
     Model *m = vm;
     if (!m->finalized) return -1;
     RunCtx R;
@@ -1032,6 +1120,8 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
     R.states = states; R.pflags = pflags; R.trace = trace; R.trace_cap = trace_cap;
     R.trace_count = trace_count;
     R.mesh_out = m->mesh_on ? mesh_out : NULL;
+    R.inst_out = inst_out;
+    const size_t ninst = inst_out ? (size_t)m->leaves[m->root] : 0;
     const size_t nbins = m->mesh_on ? (size_t)m->mesh_n[0] * m->mesh_n[1] * m->mesh_n[2] : 0;
     for (int a = 0; a < 3; ++a) { R.lo[a] = lo ? lo[a] : 0.0; R.w[a] = lo ? hi[a] - lo[a] : 0.0; }
     int nmc = m->n_mc;
@@ -1044,6 +1134,7 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
         acc[t].len = calloc((size_t)nmc + 1, sizeof(Neu));
         acc[t].exits = calloc((size_t)nmc + 1, sizeof(uint64_t));
         acc[t].mesh = R.mesh_out ? calloc(nbins, sizeof(Neu)) : NULL;
+        acc[t].inst = R.inst_out ? calloc(ninst, sizeof(Neu)) : NULL;
     }
 #pragma omp parallel num_threads(T)
     {
@@ -1075,23 +1166,31 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
             for (int t = 0; t < T; ++t) { neu_add(&tot, acc[t].mesh[v].sum); neu_add(&tot, acc[t].mesh[v].comp); }
             R.mesh_out[v] += tot.sum + tot.comp;
         }
-    for (int t = 0; t < T; ++t) { free(acc[t].len); free(acc[t].exits); free(acc[t].mesh); }
+    if (R.inst_out)
+        for (size_t v = 0; v < ninst; ++v) {
+            Neu tot = {0.0, 0.0};
+            for (int t = 0; t < T; ++t) { neu_add(&tot, acc[t].inst[v].sum); neu_add(&tot, acc[t].inst[v].comp); }
+            R.inst_out[v] += tot.sum + tot.comp;
+        }
+    for (int t = 0; t < T; ++t) { free(acc[t].len); free(acc[t].exits); free(acc[t].mesh); free(acc[t].inst); }
     free(acc);
     return 0;
 }
 
 int orc_run(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *lo, const double *hi,
             uint64_t max_seg, int nthreads, double *out, uint8_t *pflags, void *trace,
-            uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out) {
+            uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out,
+            double *inst_out) {
     return run_common(vm, seed, pid0, n, lo, hi, NULL, max_seg, nthreads, out, pflags, trace,
-                      trace_cap, trace_count, evals, mesh_out);
+                      trace_cap, trace_count, evals, mesh_out, inst_out);
 }
 
 int orc_run_states(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *states,
                    uint64_t max_seg, int nthreads, double *out, uint8_t *pflags, void *trace,
-                   uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out) {
+                   uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out,
+                   double *inst_out) {
     return run_common(vm, seed, pid0, n, NULL, NULL, states, max_seg, nthreads, out, pflags, trace,
-                      trace_cap, trace_count, evals, mesh_out);
+                      trace_cap, trace_count, evals, mesh_out, inst_out);
 }
 
 /* ---------------------------------------------------------------- unit queries */

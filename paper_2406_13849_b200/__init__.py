@@ -55,7 +55,7 @@ class ModelInfo(C.Structure):
                 ("n_universes", C.c_int32), ("max_depth", C.c_int32),
                 ("rect_specialisable", C.c_int32), ("rect_levels", C.c_int32),
                 ("n_bih_nodes", C.c_int32), ("out_len", C.c_int64), ("device_bytes", C.c_size_t),
-                ("mesh_bins", C.c_int64)]
+                ("mesh_bins", C.c_int64), ("n_instances", C.c_int64)]
 
 
 class Run(C.Structure):
@@ -68,7 +68,8 @@ class Run(C.Structure):
 class Outputs(C.Structure):
     _fields_ = [("out", C.c_void_p), ("pflags", C.c_void_p), ("pnseg", C.c_void_p),
                 ("pterm", C.c_void_p), ("trace", C.c_void_p),
-                ("trace_cap", C.c_uint64), ("trace_count", C.c_void_p), ("mesh", C.c_void_p)]
+                ("trace_cap", C.c_uint64), ("trace_count", C.c_void_p), ("mesh", C.c_void_p),
+                ("inst", C.c_void_p)]
 
 
 _lib = None
@@ -76,7 +77,7 @@ _lib = None
 SYMBOLS = ["nt_last_error", "nt_abi_version", "nt_model_create", "nt_model_destroy", "nt_add_surface",
            "nt_add_material", "nt_add_csg_universe", "nt_add_cell", "nt_add_rect_array", "nt_add_rect_edges",
            "nt_add_hex_array", "nt_set_root", "nt_set_mesh", "nt_build_opts_default", "nt_finalize",
-           "nt_model_info_get", "nt_material_cell_ids", "nt_bih_info", "nt_track",
+           "nt_model_info_get", "nt_material_cell_ids", "nt_instance_cells", "nt_bih_info", "nt_track",
            "nt_track_states", "nt_track_host", "nt_find_cells", "nt_last_launch_count",
            "nt_selftest_arith"]
 
@@ -102,6 +103,7 @@ def lib():
                                        i32, C.POINTER(i32)]
         L.nt_set_root.argtypes = [vp, i32]
         L.nt_set_mesh.argtypes = [vp, dp, dp, dp]
+        L.nt_instance_cells.argtypes = [vp, dp, C.c_int64]
         L.nt_build_opts_default.argtypes = [C.POINTER(BuildOpts)]
         L.nt_finalize.argtypes = [vp, C.POINTER(BuildOpts)]
         L.nt_model_info_get.argtypes = [vp, C.POINTER(ModelInfo)]
@@ -290,7 +292,8 @@ class Model:
     def track(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
               max_segments: int = 0, tracker: str = "generic", pflags: bool = False,
               trace_cap: int = 0, states=None, out=None, stream=None, block_dim: int = 0,
-              blocks_per_sm: int = 0, per_history: bool = False, scheduler: str = "block", mesh=None):
+              blocks_per_sm: int = 0, per_history: bool = False, scheduler: str = "block", mesh=None,
+              instances=None):
         """Track histories [pid_begin, pid_begin+n) on this model's GPU (async on `stream`).
         Returns a dict of device tensors: out (accumulated), pflags, trace, trace_count."""
         import torch
@@ -320,6 +323,13 @@ class Model:
             assert mesh.dtype == torch.float64 and mesh.is_cuda and mesh.numel() >= self.info["mesh_bins"] > 0
             o.mesh = mesh.data_ptr()
             res["mesh"] = mesh
+        if instances is not None:                  # per-instance tally (reading D1)
+            if instances is True:
+                instances = torch.zeros(max(self.info["n_instances"], 1), dtype=torch.float64, device=dev)
+            assert instances.dtype == torch.float64 and instances.is_cuda
+            assert instances.numel() >= self.info["n_instances"] > 0
+            o.inst = instances.data_ptr()
+            res["inst"] = instances
         run = self.make_run(n, seed, pid_begin, lo, hi, max_segments, tracker, bool(trace_cap),
                             block_dim, blocks_per_sm, scheduler)
         sh = _stream_handle(stream)
@@ -354,6 +364,13 @@ class Model:
         _check(self.L.nt_find_cells(self.h, C.c_void_p(xyz.data_ptr()), n, C.c_void_p(cell.data_ptr()),
                                     C.c_void_p(fl.data_ptr()), _stream_handle(stream)))
         return cell, fl
+
+    def instance_cells(self) -> np.ndarray:
+        """Material-cell bin of every material-cell instance (reading D1)."""
+        n = self.info["n_instances"]
+        out = np.zeros(max(n, 1), dtype=np.int32)
+        _check(self.L.nt_instance_cells(self.h, _p(out), n))
+        return out[:n]
 
     def last_launch_count(self) -> int:
         return self.L.nt_last_launch_count(self.h)

@@ -362,6 +362,84 @@ struct BihBuilder {
   }
 };
 
+// ---------------------------------------------------------------- instances (D1)
+// Material-cell instances are numbered by a depth-first enumeration: a CSG universe's cells in
+// id order (material cell = 1 instance, fill cell = its universe's instances), an array's tiles
+// in fill order, then its outer universe once.  The instance of a walk position is the sum, over
+// the levels of its stack, of the instances of the earlier siblings: inst_off[univ_inst[u] + k]
+// for child k (CSG: cell position; rect: fill index, outer = n; hex: (kz, r, q) grid position,
+// outer = W*W*nz).  inst_mc lists the material-cell bin of every instance (the enumeration).
+void build_instance_tables(const std::vector<HCell>& C, const std::vector<HUniv>& U, int root, Flat& F) {
+  const int nu = (int)U.size();
+  std::vector<int64_t> leaves(nu, -1);
+  std::function<int64_t(int)> count = [&](int u) -> int64_t {
+    if (leaves[u] >= 0) return leaves[u];
+    const HUniv& X = U[u];
+    int64_t n = 0;
+    if (X.kind == U_CSG) {
+      for (int c : X.cells) n += C[c].fill_kind == 0 ? 1 : count(C[c].fill);
+    } else {
+      for (int f : X.fill) n += count(f);
+      if (X.outer >= 0) n += count(X.outer);
+    }
+    return leaves[u] = std::min<int64_t>(n, int64_t(1) << 40);
+  };
+  for (int u = 0; u < nu; ++u) count(u);
+  F.n_inst = leaves[root];
+  if (F.n_inst >= (int64_t(1) << 31)) { F.n_inst = 0; return; }   // too many to index in 32 bits
+  F.cell_pos.assign(C.size(), 0);
+  F.univ_inst.assign(nu, 0);
+  for (int u = 0; u < nu; ++u) {
+    const HUniv& X = U[u];
+    F.univ_inst[u] = (int32_t)F.inst_off.size();
+    int64_t acc = 0;
+    if (X.kind == U_CSG) {
+      for (size_t k = 0; k < X.cells.size(); ++k) {
+        const int c = X.cells[k];
+        F.cell_pos[c] = (int32_t)k;
+        F.inst_off.push_back((int32_t)acc);
+        acc += C[c].fill_kind == 0 ? 1 : leaves[C[c].fill];
+      }
+    } else if (X.kind == U_RECT) {
+      for (int f : X.fill) { F.inst_off.push_back((int32_t)acc); acc += leaves[f]; }
+      F.inst_off.push_back((int32_t)acc);                         // outer
+    } else {
+      const int R = X.rings - 1, W = 2 * R + 1, nzl = X.zp > 0 ? X.nz : 1;
+      const int per = (int)X.fill.size() / nzl;
+      std::vector<int64_t> prefix(X.fill.size() + 1, 0);
+      for (size_t t = 0; t < X.fill.size(); ++t) prefix[t + 1] = prefix[t] + leaves[X.fill[t]];
+      std::vector<int32_t> grid((size_t)W * W * nzl + 1, 0);
+      for (int kz = 0; kz < nzl; ++kz) {
+        int o = 0;
+        for (int r = -R; r <= R; ++r)
+          for (int q = -R; q <= R; ++q)
+            if (std::max({std::abs(q), std::abs(r), std::abs(q + r)}) <= R)
+              grid[(size_t)kz * W * W + (r + R) * W + (q + R)] = (int32_t)prefix[(size_t)kz * per + o++];
+      }
+      grid[(size_t)W * W * nzl] = (int32_t)prefix[X.fill.size()];   // outer
+      F.inst_off.insert(F.inst_off.end(), grid.begin(), grid.end());
+    }
+  }
+  // the enumeration itself (material-cell bins are the material cells in global id order)
+  std::vector<int32_t> mc_of(C.size(), -1);
+  for (int i = 0, k = 0; i < (int)C.size(); ++i) if (C[i].fill_kind == 0) mc_of[i] = k++;
+  F.inst_mc.clear();
+  F.inst_mc.reserve((size_t)F.n_inst);
+  std::function<void(int)> walk = [&](int u) {
+    const HUniv& X = U[u];
+    if (X.kind == U_CSG) {
+      for (int c : X.cells) {
+        if (C[c].fill_kind == 0) F.inst_mc.push_back(mc_of[c]);
+        else walk(C[c].fill);
+      }
+    } else {
+      for (int f : X.fill) walk(f);
+      if (X.outer >= 0) walk(X.outer);
+    }
+  };
+  walk(root);
+}
+
 // ---------------------------------------------------------------- pseudo-arrays
 // Replace every rect/hex array universe by a CSG universe of explicit tile cells (same uid,
 // same depth), covering the in-lattice tiles and every out-of-lattice tile that meets the
@@ -630,6 +708,7 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
         if (!a.valid()) a = ubox[u].valid() ? ubox[u] : Aabb{{0, 0, 0}, {0, 0, 0}};
         cb[c] = pad(a);
       }
+  if (!opts.pseudo) build_instance_tables(C, U, root, F);
   // universes
   F.bih_depth.assign(U.size(), 0);
   for (int u = 0; u < (int)U.size(); ++u) {
@@ -691,6 +770,9 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
   if (F.bih_leaf.empty()) F.bih_leaf.push_back(0);
   if (F.fills.empty()) F.fills.push_back(-1);
   if (F.edges.empty()) F.edges.push_back(0.0);
+  if (F.univ_inst.empty()) F.univ_inst.push_back(0);
+  if (F.inst_off.empty()) F.inst_off.push_back(0);
+  if (F.cell_pos.empty()) F.cell_pos.push_back(0);
   if (F.hs.empty()) F.hs.push_back(0);
   if (F.mc_st.empty()) fail("model has no material cells");
 }

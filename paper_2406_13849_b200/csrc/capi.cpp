@@ -289,7 +289,8 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
                o_ctr = place(blob, F.cell_tr), o_univ = place(blob, F.univ), o_bih = place(blob, F.bih),
                o_leaf = place(blob, F.bih_leaf), o_fills = place(blob, F.fills), o_st = place(blob, F.mc_st),
                o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell),
-               o_edges = place(blob, F.edges);
+               o_edges = place(blob, F.edges), o_uinst = place(blob, F.univ_inst),
+               o_ioff = place(blob, F.inst_off), o_cpos = place(blob, F.cell_pos);
   const size_t o_pou = place(blob, F.r_pin_of_univ), o_poff = place(blob, F.r_pin_off),
                o_psid = place(blob, F.r_pin_sid), o_pmc = place(blob, F.r_pin_mc);
   m->blob_bytes = blob.size();
@@ -327,6 +328,9 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     g.mc_pabs = (const double*)(b + o_pabs);
     g.mc_cell = (const int32_t*)(b + o_mcc);
     g.edges = (const double*)(b + o_edges);
+    g.univ_inst = (const int32_t*)(b + o_uinst);
+    g.inst_off = (const int32_t*)(b + o_ioff);
+    g.cell_pos = (const int32_t*)(b + o_cpos);
     m->rg = F.rg;
     m->rg.pin_of_univ = (const int32_t*)(b + o_pou);
     m->rg.pin_off = (const int32_t*)(b + o_poff);
@@ -363,6 +367,14 @@ nt_status nt_model_info_get(const nt_model* m, nt_model_info* info) {
   info->out_len = 2 * (int64_t)F.n_mc + NT_NC;
   info->device_bytes = m->blob_bytes;
   info->mesh_bins = m->mesh_on ? (int64_t)m->mesh_n[0] * m->mesh_n[1] * m->mesh_n[2] : 0;
+  info->n_instances = F.n_inst;
+  return NT_OK;
+}
+
+nt_status nt_instance_cells(const nt_model* m, int32_t* out, int64_t cap) {
+  if (!m || !out) return err(NT_E_ARG, "nt_instance_cells: NULL argument");
+  if (!m->finalized) return err(NT_E_ORDER, "nt_instance_cells: model not finalized");
+  for (int64_t i = 0; i < m->F.n_inst && i < cap; ++i) out[i] = m->F.inst_mc[(size_t)i];
   return NT_OK;
 }
 
@@ -424,6 +436,9 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   if (run->n > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": at most 2^32-1 histories per call");
   if (trace && o->mesh && m->mesh_on)
     return err(NT_E_UNSUPPORTED, std::string(who) + ": the mesh tally cannot be combined with NT_TRACE");
+  if (o->inst && (trace || m->F.n_inst == 0 || run->tracker == NT_TRACKER_RECT))
+    return err(NT_E_UNSUPPORTED, std::string(who) + ": instance tallies need a generic-tracker run without "
+               "NT_TRACE on a model built without pseudo-arrays");
   const bool dp = (run->flags & NT_DP) != 0;
   // block queues: ring queues without rounds (default, block 256) or rounds + barrier (NT_ROUNDS,
   // also every block_dim 128 run)
@@ -450,6 +465,7 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   R.trace_cap = trace ? o->trace_cap : 0;
   R.trace_count = reinterpret_cast<unsigned long long*>(o->trace_count);
   R.mesh = m->g.mesh_on ? o->mesh : nullptr;
+  R.inst = o->inst;
   const unsigned slot = m->slot.fetch_add(1) % kSlots;
   R.counter = m->counters + slot;
   cudaStream_t s = static_cast<cudaStream_t>(stream);

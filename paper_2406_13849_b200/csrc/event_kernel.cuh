@@ -58,12 +58,13 @@ __device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpr
 __device__ __forceinline__ void vstore(uint32_t* p, uint32_t v) { *reinterpret_cast<volatile uint32_t*>(p) = v; }
 
 // DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh).
+// TALLY: bit 0 mesh tally (M1), bit 1 per-instance tally (D1); separate instantiations.
 // ASYNC = true: no rounds and no block barrier.  Each queue is a ring of B entries with a head
 // and a tail counter in shared memory; a warp claims up to 32 entries of the fullest queue (CAS on
 // the head), runs that EVENT and MOVE on them, and appends every slot to the ring of its next
 // event (warp-aggregated atomic on the tail, entry published after a block fence).  The block
 // ends when the pids are exhausted and no history is live.
-template <int B, bool TRACE, bool STATES, bool DP = false, bool MESH = false, bool ASYNC = false>
+template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false>
 __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -389,7 +390,8 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
               const bool cross = ds < dc;
               const double s = cross ? ds : dc;
               atomicAdd(gl + mc, s);
-              if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+              if (TALLY & 1) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+              if (TALLY & 2) atomicAdd(R.inst + instance_of(g, st, L), s);
               rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
               ++nseg;
               seg = true;

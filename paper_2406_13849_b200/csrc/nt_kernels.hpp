@@ -23,6 +23,7 @@ struct KRun {
   unsigned long long* counter;      // work counter (pid claims), zeroed before launch
   double* slices;                   // [grid][n_mc] zeroed per-block track-length tallies (global)
   double* mesh;                     // optional per-voxel track length (M1), accumulated
+  double* inst;                     // optional per-instance track length (D1), accumulated
 };
 
 // one copy of the launchers per compiled feature set (track_f0.cu, track_f7.cu)

@@ -85,6 +85,9 @@ struct DevGeom {
   const double* mc_pabs;      // per material cell: sigma_a / sigma_t (O14)
   const int32_t* mc_cell;     // per material cell: global cell id (trace)
   const double* edges;        // non-uniform rect edges (N1): per array x[n0+1] y[n1+1] z[n2+1]
+  const int32_t* univ_inst;   // per-instance tallies (D1): per universe, base into inst_off
+  const int32_t* inst_off;    //   instances before child k of the universe
+  const int32_t* cell_pos;    //   per cell: its position in its universe
   int32_t root, n_mc, max_depth, n_univ;
   int32_t n_cells, n_surf, root_kind, features;   // features: F_* bits present in the model
   const void* const* trk;     // DP dispatch only: per-universe tracker object pointers (dp_tracker.cuh)

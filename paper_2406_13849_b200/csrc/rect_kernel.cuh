@@ -8,7 +8,7 @@
 
 NT_DEV_BEGIN
 
-template <int K, bool BOX, bool TRACE, bool STATES, bool MESH = false>
+template <int K, bool BOX, bool TRACE, bool STATES, int TALLY = 0>
 __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectGeom rg, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
@@ -268,7 +268,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
         } else if (ds < dc) {
           const double s = ds;
           atomicAdd(gl + mc, s);
-          if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (TALLY & 1) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
@@ -322,7 +322,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
         } else {
           const double s = dc;
           atomicAdd(gl + mc, s);
-          if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (TALLY & 1) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           ++nseg;
           ++ncoll;

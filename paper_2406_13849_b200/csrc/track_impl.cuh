@@ -41,6 +41,34 @@ struct Stack {
   __device__ __forceinline__ double& T(int l, int k) { return sT[(3 * l + k) * B]; }
 };
 
+// D1: instance of the material cell at the bottom of the stack (levels 0 .. L-1): the sum over the
+// levels of the instances that precede the chosen child (builder: build_instance_tables).
+__device__ __forceinline__ int instance_of(const DevGeom& g, Stack& st, int L) {
+  int inst = 0;
+#pragma unroll 1
+  for (int l = 0; l < L; ++l) {
+    const int u = st.u(l);
+    const DUniv* U = g.univ + u;
+    const int kind = ld(&U->kind);
+    int k;
+    if (kind == U_CSG) {
+      k = ld(g.cell_pos + st.a(l));
+    } else if (!kHex || kind == U_RECT) {
+      const int n0 = ld(&U->i0), n1 = ld(&U->i1), n2 = ld(&U->i2), is2d = ld(&U->is2d);
+      const int a = st.a(l), b = st.b(l), c = st.c(l);
+      const bool in = a >= 0 && a < n0 && b >= 0 && b < n1 && (is2d || (c >= 0 && c < n2));
+      k = in ? a + n0 * (b + n1 * (is2d ? 0 : c)) : n0 * n1 * n2;
+    } else {
+      const int R = ld(&U->i0), nz = ld(&U->i1), W = 2 * R + 1;
+      const int q = st.a(l), r = st.b(l), kz = st.c(l);
+      const bool in = max(abs(q), max(abs(r), abs(q + r))) <= R && (nz == 0 || (kz >= 0 && kz < nz));
+      k = in ? (nz > 0 ? kz : 0) * W * W + (r + R) * W + (q + R) : W * W * (nz > 0 ? nz : 1);
+    }
+    inst += ld(g.inst_off + ld(g.univ_inst + u) + k);
+  }
+  return inst;
+}
+
 // Alg. 7 descent from level l0 in universe u with frame translation T; forced sense applies
 // at level l0 only (CSG cross_surface).  Returns false when a level has no cell (LOST).
 template <bool STORE_T = true>
@@ -179,7 +207,7 @@ __device__ __forceinline__ void flush_tallies(const KRun& R, double* gl, const u
 
 enum { C_PART = 0, C_SEG, C_CROSS, C_REFL, C_LEAK, C_COLL, C_ABS, C_LOST, C_CAP, C_FLAG, C_CBL0 };
 
-template <bool TRACE, bool STATES, bool MESH = false>
+template <bool TRACE, bool STATES, int TALLY = 0>
 __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
@@ -285,7 +313,8 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           // Alg. 2 "while d < tau/Sigma": tau -= Sigma d, move, cross
           const double s = ds;
           atomicAdd(gl + mc, s);
-          if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (TALLY & 1) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (TALLY & 2) atomicAdd(R.inst + instance_of(g, st, L), s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
@@ -347,7 +376,8 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           // ---- collision at tau / Sigma_t: absorb or scatter isotropically (O14, O15)
           const double s = dc;
           atomicAdd(gl + mc, s);
-          if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (TALLY & 1) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+          if (TALLY & 2) atomicAdd(R.inst + instance_of(g, st, L), s);
           rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
           ++nseg;
           ++ncoll;
@@ -459,9 +489,12 @@ cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool sta
       return cudaGetLastError();
     });
   };
-  if (R.mesh) {                       // mesh tally: separate instantiations (no call in the others)
+  const int tally = (R.mesh ? 1 : 0) | (R.inst ? 2 : 0);
+  if (tally) {                        // tallies: separate instantiations (no extra code in the others)
     if (trace) return cudaErrorNotSupported;
-    return states ? pick(k_track_generic<false, true, true>) : pick(k_track_generic<false, false, true>);
+    if (tally == 1) return states ? pick(k_track_generic<false, true, 1>) : pick(k_track_generic<false, false, 1>);
+    if (tally == 2) return states ? pick(k_track_generic<false, true, 2>) : pick(k_track_generic<false, false, 2>);
+    return states ? pick(k_track_generic<false, true, 3>) : pick(k_track_generic<false, false, 3>);
   }
   if (trace) return states ? pick(k_track_generic<true, true>) : pick(k_track_generic<true, false>);
   return states ? pick(k_track_generic<false, true>) : pick(k_track_generic<false, false>);
@@ -490,8 +523,8 @@ cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, boo
     });
   };
   auto pick_k = [&](auto box, auto tr, auto st, auto me) -> cudaError_t {
-    constexpr bool BOX = decltype(box)::value, TR = decltype(tr)::value, ST = decltype(st)::value,
-                   ME = decltype(me)::value;
+    constexpr bool BOX = decltype(box)::value, TR = decltype(tr)::value, ST = decltype(st)::value;
+    constexpr int ME = decltype(me)::value ? 1 : 0;
     switch (rg.K) {
       case 0: return go(k_track_rect<0, BOX, TR, ST, ME>);
       case 1: return go(k_track_rect<1, BOX, TR, ST, ME>);
@@ -503,6 +536,7 @@ cudaError_t launch_rect(const DevGeom& g, const RectGeom& rg, const KRun& R, boo
   };
   using T = std::true_type;
   using F = std::false_type;
+  if (R.inst) return cudaErrorNotSupported;   // instance tallies: generic tracker only
   if (R.mesh) {                       // mesh tally: separate instantiations, no trace
     if (trace) return cudaErrorNotSupported;
     if (rg.root_box) return states ? pick_k(T{}, F{}, T{}, T{}) : pick_k(T{}, F{}, F{}, T{});
@@ -543,27 +577,37 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
       return cudaGetLastError();
     });
   };
-  if (R.mesh && trace) return cudaErrorNotSupported;
+  const int tally = (R.mesh ? 1 : 0) | (R.inst ? 2 : 0);
+  if (tally && trace) return cudaErrorNotSupported;
   if (async) {                     // barrier-free ring queues (block 256), SP or DP dispatch
     if (block != 256) return cudaErrorInvalidValue;
     auto pick = [&](auto dp) -> cudaError_t {
       constexpr bool D = decltype(dp)::value;
-      if (R.mesh) return states ? go(k_track_event<256, false, true, D, true, true>) : go(k_track_event<256, false, false, D, true, true>);
-      if (trace) return states ? go(k_track_event<256, true, true, D, false, true>) : go(k_track_event<256, true, false, D, false, true>);
-      return states ? go(k_track_event<256, false, true, D, false, true>) : go(k_track_event<256, false, false, D, false, true>);
+      if (tally == 1) return states ? go(k_track_event<256, false, true, D, 1, true>) : go(k_track_event<256, false, false, D, 1, true>);
+      if (tally == 2) return states ? go(k_track_event<256, false, true, D, 2, true>) : go(k_track_event<256, false, false, D, 2, true>);
+      if (tally == 3) return states ? go(k_track_event<256, false, true, D, 3, true>) : go(k_track_event<256, false, false, D, 3, true>);
+      if (trace) return states ? go(k_track_event<256, true, true, D, 0, true>) : go(k_track_event<256, true, false, D, 0, true>);
+      return states ? go(k_track_event<256, false, true, D, 0, true>) : go(k_track_event<256, false, false, D, 0, true>);
     };
     return g.trk ? pick(std::true_type{}) : pick(std::false_type{});
   }
   if (g.trk) {                     // DP dispatch (virtual tracker calls), block 256 only
     if (block != 256) return cudaErrorInvalidValue;
-    if (R.mesh) return states ? go(k_track_event<256, false, true, true, true>) : go(k_track_event<256, false, false, true, true>);
+    if (tally == 1) return states ? go(k_track_event<256, false, true, true, 1>) : go(k_track_event<256, false, false, true, 1>);
+    if (tally) return cudaErrorNotSupported;     // DP with instance tallies: ring scheduler only
     if (trace) return states ? go(k_track_event<256, true, true, true>) : go(k_track_event<256, true, false, true>);
     return states ? go(k_track_event<256, false, true, true>) : go(k_track_event<256, false, false, true>);
   }
-  if (R.mesh) {                    // mesh tally: separate instantiations (no call in the others)
-    if (block == 128) return states ? go(k_track_event<128, false, true, false, true>) : go(k_track_event<128, false, false, false, true>);
+  if (tally) {                     // tallies: separate instantiations (no extra code in the others)
+    if (block == 128) {
+      if (tally == 1) return states ? go(k_track_event<128, false, true, false, 1>) : go(k_track_event<128, false, false, false, 1>);
+      if (tally == 2) return states ? go(k_track_event<128, false, true, false, 2>) : go(k_track_event<128, false, false, false, 2>);
+      return states ? go(k_track_event<128, false, true, false, 3>) : go(k_track_event<128, false, false, false, 3>);
+    }
     if (block != 256) return cudaErrorInvalidValue;
-    return states ? go(k_track_event<256, false, true, false, true>) : go(k_track_event<256, false, false, false, true>);
+    if (tally == 1) return states ? go(k_track_event<256, false, true, false, 1>) : go(k_track_event<256, false, false, false, 1>);
+    if (tally == 2) return states ? go(k_track_event<256, false, true, false, 2>) : go(k_track_event<256, false, false, false, 2>);
+    return states ? go(k_track_event<256, false, true, false, 3>) : go(k_track_event<256, false, false, false, 3>);
   }
   if (block == 128) {
     if (trace) return states ? go(k_track_event<128, true, true>) : go(k_track_event<128, true, false>);
@@ -605,9 +649,12 @@ cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, 
       return cudaGetLastError();
     });
   };
-  if (R.mesh) {
+  const int tally = (R.mesh ? 1 : 0) | (R.inst ? 2 : 0);
+  if (tally) {
     if (trace) return cudaErrorNotSupported;
-    return states ? go(k_track_wq<false, true, true>) : go(k_track_wq<false, false, true>);
+    if (tally == 1) return states ? go(k_track_wq<false, true, 1>) : go(k_track_wq<false, false, 1>);
+    if (tally == 2) return states ? go(k_track_wq<false, true, 2>) : go(k_track_wq<false, false, 2>);
+    return states ? go(k_track_wq<false, true, 3>) : go(k_track_wq<false, false, 3>);
   }
   if (trace) return states ? go(k_track_wq<true, true>) : go(k_track_wq<true, false>);
   return states ? go(k_track_wq<false, true>) : go(k_track_wq<false, false>);

@@ -68,7 +68,7 @@ size_t wq_smem_bytes(const DevGeom& g, bool trace) {
   return head + warp * kWqWarps;
 }
 
-template <bool TRACE, bool STATES, bool MESH = false>
+template <bool TRACE, bool STATES, int TALLY = 0>
 __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, const KRun R) {
   constexpr int S = kWqSlots, W = kWqWarps, B = W * 32;
   extern __shared__ __align__(16) unsigned char smem[];
@@ -300,7 +300,8 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
             const bool cross = ds < dc;
             const double s = cross ? ds : dc;
             atomicAdd(gl + mc, s);
-            if (MESH) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+            if (TALLY & 1) mesh_score(g, R.mesh, rx, ry, rz, u, v, w, s);
+            if (TALLY & 2) atomicAdd(R.inst + instance_of(g, st, L), s);
             rx = rx + s * u; ry = ry + s * v; rz = rz + s * w;
             ++nseg;
             seg = true;

@@ -29,7 +29,7 @@ def test_exports_every_header_symbol(nt):
     missing = [s for s in declared if not hasattr(L, s)]
     assert not missing, missing
     assert set(declared) == set(nt.SYMBOLS)
-    assert L.nt_abi_version() == 2
+    assert L.nt_abi_version() == 3
 
 
 def _host(nt, spec, **kw):
@@ -193,3 +193,15 @@ def test_mesh_host_validation(nt):
         s2["mesh"] = dict(spec["mesh"], **bad)
         with pytest.raises(nt.NtError, match="nt_set_mesh"):
             _host(nt, s2)
+
+
+def test_instance_tables_host(nt, oracle_mod):
+    """D1 instance numbering: the builder's enumeration equals the oracle's (independent DFS),
+    and pseudo-array builds report no instances."""
+    for cfg in ("c1", "c2", "c4", "c5m", "c5r"):
+        spec, _ = workloads.config(cfg)
+        m = _host(nt, spec)
+        om = oracle_mod.OracleModel.from_spec(spec)
+        assert m.info["n_instances"] == om.n_instances()
+        assert np.array_equal(m.instance_cells(), om.instance_cells())
+    assert _host(nt, workloads.config("c2")[0], pseudo_array=True).info["n_instances"] == 0

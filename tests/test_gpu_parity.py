@@ -178,6 +178,39 @@ def test_mesh_tally_off_without_buffer(nt):
     assert torch.equal(ra["out"], rb["out"]) or np.allclose(ra["out"].cpu().numpy(), rb["out"].cpu().numpy(), rtol=1e-13)
 
 
+@pytest.mark.parametrize("sched", ["block", "rounds", "warp", "history", "dp"])
+@pytest.mark.parametrize("cfg", ["c2", "c4", "c5m"])
+def test_instance_tally_parity(nt, orc, cfg, sched):
+    """Per-instance (distributed-cell) tally, reading D1: every instance's track length vs the
+    oracle (which numbers instances by summing earlier siblings' leaves level by level)."""
+    spec, _ = workloads.config(cfg)
+    m = nt.Model.from_spec(spec, device=0)
+    om = orc.OracleModel.from_spec(spec)
+    n = 400
+    res = m.track(n, seed=6, instances=True, scheduler=sched)
+    torch.cuda.synchronize()
+    o = om.run(n, seed=6, instances=True)
+    gi = res["inst"].cpu().numpy()[:om.n_instances()]
+    ref = o["inst"]
+    assert (ref > 0).sum() > 20
+    assert np.all(np.abs(gi - ref) <= 1e-9 * np.abs(ref) + 1e-12 * ref.max())
+
+
+def test_mesh_and_instance_tallies_together(nt, orc):
+    """Both extra tallies in one run (separate kernel instantiation) on the full-core model."""
+    spec = MESHED["c3"]()
+    m = nt.Model.from_spec(spec, device=0)
+    om = orc.OracleModel.from_spec(spec)
+    res = m.track(300, seed=9, mesh=True, instances=True)
+    torch.cuda.synchronize()
+    o = om.run(300, seed=9, mesh=True, instances=True)
+    g = m.unpack(res["out"])
+    assert g["counters"] == o["counters"]
+    for key in ("mesh", "inst"):
+        got, ref = res[key].cpu().numpy()[:len(o[key])], o[key]
+        assert np.all(np.abs(got - ref) <= 1e-9 * np.abs(ref) + 1e-12 * ref.max()), key
+
+
 def test_dp_dispatch_rejects_other_schedulers(nt):
     """NT_DP is a dispatch mode of the block-queue scheduler only (nestrack.h)."""
     spec, _ = workloads.config("c1")
