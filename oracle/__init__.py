@@ -66,8 +66,12 @@ def lib():
             getattr(L, f).argtypes = [vp]
         L.orc_material_cell_ids.argtypes = [vp, dp]
         L.orc_cell_material.argtypes = [vp, i32]
-        L.orc_run.argtypes = [vp, u64, u64, u64, dp, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp]
-        L.orc_run_states.argtypes = [vp, u64, u64, u64, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp]
+        L.orc_run.argtypes = [vp, u64, u64, u64, dp, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp, dp, dp]
+        L.orc_run_states.argtypes = [vp, u64, u64, u64, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp, dp, dp]
+        L.orc_set_fission.argtypes = [vp, i32, C.c_double]
+        L.orc_max_sites.argtypes = [vp]
+        L.orc_fission_source.argtypes = [vp, dp, dp, u64, u64, C.c_uint32, u64, dp]
+        L.orc_fission_source.restype = u64
         L.orc_n_instances.argtypes = [vp]
         L.orc_n_instances.restype = C.c_long
         L.orc_instance_cells.argtypes = [vp, dp]
@@ -145,7 +149,10 @@ class OracleModel:
             r = L.orc_add_surface(m.h, KIND[s["kind"]], _p(coef), BC[s["bc"]])
             assert r >= 0
         for mt in spec["materials"]:
-            L.orc_add_material(m.h, mt["sigma_t"], mt["sigma_a"])
+            k = L.orc_add_material(m.h, mt["sigma_t"], mt["sigma_a"])
+            if mt.get("nu_sigma_f", 0.0):
+                if L.orc_set_fission(m.h, k, mt["nu_sigma_f"]) != 0:
+                    raise ValueError("oracle: bad nu_sigma_f")
         for u in spec["universes"]:
             if u["kind"] == "csg":
                 uid = L.orc_add_csg_universe(m.h)
@@ -200,10 +207,11 @@ class OracleModel:
     def run(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
             max_segments: int = 1_000_000, threads: int | None = None, pflags: bool = False,
             trace_cap: int = 0, states: np.ndarray | None = None, mesh: bool = False,
-            instances: bool = False):
+            instances: bool = False, bank: bool = False):
         """Track particles [pid_begin, pid_begin+n).  Returns dict with out, counters, ...
         mesh=True (model spec with a "mesh"): res["mesh"] = per-voxel track length, x fastest.
-        instances=True: res["inst"] = track length per material-cell instance (reading D1)."""
+        instances=True: res["inst"] = track length per material-cell instance (reading D1).
+        bank=True: res["bank"] [n, max_sites, 3] fission sites, res["bank_n"] sites per history (F1)."""
         if threads is None:
             threads = len(os.sched_getaffinity(0))
         out = np.zeros(self.out_len)
@@ -216,6 +224,10 @@ class OracleModel:
             assert self.mesh_shape is not None, "model has no mesh"
             mo = np.zeros(int(np.prod(self.mesh_shape)))
         io = np.zeros(max(self.n_instances(), 1)) if instances else None
+        ms = self.L.orc_max_sites(self.h)
+        bk = np.zeros((max(n, 1), ms, 3)) if bank else None
+        bn = np.zeros(max(n, 1), dtype=np.uint8) if bank else None
+        bargs = (_p(bk), _p(bn)) if bank else (None, None)
         if states is None:
             src = self.spec["source"]
             lo = np.asarray(src["lo"] if lo is None else lo, dtype=np.float64)
@@ -223,7 +235,8 @@ class OracleModel:
             rc = self.L.orc_run(self.h, seed, pid_begin, n, _p(lo), _p(hi), max_segments, threads,
                                 _p(out), _p(pf) if pf is not None else None,
                                 _p(tr) if tr is not None else None, trace_cap, _p(tcount), _p(ev),
-                                _p(mo) if mo is not None else None, _p(io) if io is not None else None)
+                                _p(mo) if mo is not None else None, _p(io) if io is not None else None,
+                                *bargs)
         else:
             st = np.ascontiguousarray(states, dtype=np.float64)
             assert st.shape == (6, n)
@@ -231,7 +244,7 @@ class OracleModel:
                                        _p(out), _p(pf) if pf is not None else None,
                                        _p(tr) if tr is not None else None, trace_cap, _p(tcount),
                                        _p(ev), _p(mo) if mo is not None else None,
-                                       _p(io) if io is not None else None)
+                                       _p(io) if io is not None else None, *bargs)
         assert rc == 0
         res = self.unpack(out)
         res["evals"] = {k: int(ev[i]) for i, k in enumerate(EVAL_KINDS)}
@@ -239,6 +252,8 @@ class OracleModel:
             res["mesh"] = mo
         if io is not None:
             res["inst"] = io[:self.n_instances()]
+        if bank:
+            res["bank"], res["bank_n"] = bk[:n], bn[:n]
         if pf is not None:
             res["pflags"] = pf[:n]
         if tr is not None:
@@ -247,6 +262,29 @@ class OracleModel:
             t = tr[:cnt]
             res["trace"] = np.sort(t, order=["pid", "seg", "terminal"])
         return res
+
+    def max_sites(self) -> int:
+        return int(self.L.orc_max_sites(self.h))
+
+    def fission_source(self, bank: np.ndarray, bank_n: np.ndarray, seed: int, cycle: int, n_next: int):
+        """F1: next cycle's birth states [6, n_next] drawn from the bank; returns (states, M)."""
+        bank = np.ascontiguousarray(bank, dtype=np.float64)
+        bank_n = np.ascontiguousarray(bank_n, dtype=np.uint8)
+        st = np.zeros((6, max(n_next, 1)))
+        M = self.L.orc_fission_source(self.h, _p(bank), _p(bank_n), len(bank_n), seed, cycle, n_next, _p(st))
+        return st[:, :n_next], int(M)
+
+    def power_iteration(self, n: int, cycles: int, seed: int = 240613849):
+        """F1 power iteration (Alg. 1): cycle 0 born in the source box, then from the bank; histories
+        of cycle c use pids [c << 32, (c << 32) + n).  Returns the k estimate of every cycle."""
+        ks, states = [], None
+        for c in range(cycles):
+            res = self.run(n, seed=seed, pid_begin=c << 32, bank=True, states=states)
+            ks.append(int(res["bank_n"].sum()) / n)
+            states, M = self.fission_source(res["bank"], res["bank_n"], seed, c, n)
+            if M == 0:
+                raise RuntimeError("fission source collapsed (no sites banked)")
+        return ks
 
     def n_instances(self) -> int:
         """Material-cell instances in the model (reading D1)."""

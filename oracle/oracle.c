@@ -24,6 +24,10 @@
  *     D1): the instance of a material cell is its position in the depth-first
  *     enumeration of all material-cell instances; counted by summing the leaves
  *     of every earlier sibling at every level.
+ *   - fission source and k (NEXT-4, Alg. 1-2; reading F1): an
+ *     absorption banks floor(nu Sigma_f / Sigma_a + xi) sites at the absorption
+ *     point; the next cycle's source is drawn uniformly, with replacement, from
+ *     the bank in (history, site) order.
  *   - non-uniform rect arrays (Alg. 5, P:513-525 and its footnote P:500-505):
  *     the tile is found by a linear scan over the mesh divisions (reading N1
  *     in DESIGN.md: index -1 below the first edge, n at or above the last).
@@ -69,7 +73,7 @@ static const double H_SQRT3_2 = 0.8660254037844386;   /* O9: nearest double to s
 
 /* ---------------------------------------------------------------- model */
 typedef struct { int kind, bc; double c[4]; double r2; double tol; } Surf;
-typedef struct { double st, sa, pabs; } Mat;
+typedef struct { double st, sa, pabs, nut; } Mat;   /* nut = nu Sigma_f / Sigma_a (F1) */
 typedef struct {
     int uid, n, *sid, *sense;    /* half-spaces sorted by surface id */
     int fill_kind, fill;
@@ -142,7 +146,26 @@ int orc_add_material(void *vm, double st, double sa) {
     GROW(m->m, m->nm, m->cm);
     m->m[m->nm].st = st; m->m[m->nm].sa = sa;
     m->m[m->nm].pabs = st > 0.0 ? sa / st : 0.0;     /* O14: IEEE division, once */
+    m->m[m->nm].nut = 0.0;
     return m->nm++;
+}
+
+/* F1: one-group nu Sigma_f of a material (>= 0; > 0 needs Sigma_a > 0).  Stored as the expected
+ * number of sites per absorption, nu Sigma_f / Sigma_a (IEEE division, once). */
+int orc_set_fission(void *vm, int mat, double nusf) {
+    Model *m = vm;
+    if (mat < 0 || mat >= m->nm || !(nusf >= 0.0) || !isfinite(nusf)) return -1;
+    if (nusf > 0.0 && !(m->m[mat].sa > 0.0)) return -1;
+    m->m[mat].nut = nusf > 0.0 ? nusf / m->m[mat].sa : 0.0;
+    return 0;
+}
+
+/* F1: maximum number of sites one absorption can bank: floor(max nut) + 1 */
+int orc_max_sites(void *vm) {
+    Model *m = vm;
+    double mx = 0.0;
+    for (int i = 0; i < m->nm; ++i) if (m->m[i].nut > mx) mx = m->m[i].nut;
+    return (int)floor(mx) + 1;
 }
 
 static int new_univ(Model *m, int kind) {
@@ -815,6 +838,9 @@ typedef struct {
     uint8_t *pflags; TraceRec *trace; uint64_t trace_cap; uint64_t *trace_count;
     double *mesh_out;        /* optional per-voxel track length (M1), accumulated */
     double *inst_out;        /* optional per-instance track length (D1), accumulated */
+    double *bank;            /* optional fission sites (F1): [n][max_sites][3] */
+    uint8_t *bank_n;         /*   sites banked by each history */
+    int max_sites;
 } RunCtx;
 
 static void emit(const RunCtx *R, uint64_t pid, uint32_t seg, int kind, int level, int j, int cb,
@@ -1086,6 +1112,13 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
             draw(R->seed, pid, epoch, 0, &xa, &xb);
             if (xa < M->pabs) {                                   /* O14 absorption */
                 A->cnt[C_ABSORPTIONS]++;
+                if (R->bank && M->nut > 0.0) {                    /* F1: floor(nut + xi) sites here */
+                    int ns = (int)floor(M->nut + xb);
+                    if (ns > R->max_sites) ns = R->max_sites;     /* cannot happen: max_sites > nut */
+                    for (int k = 0; k < ns; ++k)
+                        for (int a = 0; a < 3; ++a) R->bank[((size_t)idx * R->max_sites + k) * 3 + a] = r[a];
+                    R->bank_n[idx] = (uint8_t)ns;
+                }
                 emit(R, pid, (uint32_t)(nseg - 1), EV_COLLIDE, -1, -1, cell, cell, s, T_ABSORBED, flags);
                 goto done;
             }
@@ -1111,7 +1144,8 @@ done:
 static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *lo,
                       const double *hi, const double *states, uint64_t max_seg, int nthreads,
                       double *out, uint8_t *pflags, void *trace, uint64_t trace_cap,
-                      uint64_t *trace_count, uint64_t *evals, double *mesh_out, double *inst_out) {
+                      uint64_t *trace_count, uint64_t *evals, double *mesh_out, double *inst_out,
+                      double *bank, uint8_t *bank_n) {
     Model *m = vm;
     if (!m->finalized) return -1;
     RunCtx R;
@@ -1121,6 +1155,8 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
     R.trace_count = trace_count;
     R.mesh_out = m->mesh_on ? mesh_out : NULL;
     R.inst_out = inst_out;
+    R.bank = bank; R.bank_n = bank_n; R.max_sites = orc_max_sites(m);
+    if (bank_n) memset(bank_n, 0, (size_t)n);
     const size_t ninst = inst_out ? (size_t)m->leaves[m->root] : 0;
     const size_t nbins = m->mesh_on ? (size_t)m->mesh_n[0] * m->mesh_n[1] * m->mesh_n[2] : 0;
     for (int a = 0; a < 3; ++a) { R.lo[a] = lo ? lo[a] : 0.0; R.w[a] = lo ? hi[a] - lo[a] : 0.0; }
@@ -1180,17 +1216,45 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
 int orc_run(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *lo, const double *hi,
             uint64_t max_seg, int nthreads, double *out, uint8_t *pflags, void *trace,
             uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out,
-            double *inst_out) {
+            double *inst_out, double *bank, uint8_t *bank_n) {
     return run_common(vm, seed, pid0, n, lo, hi, NULL, max_seg, nthreads, out, pflags, trace,
-                      trace_cap, trace_count, evals, mesh_out, inst_out);
+                      trace_cap, trace_count, evals, mesh_out, inst_out, bank, bank_n);
 }
 
 int orc_run_states(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *states,
                    uint64_t max_seg, int nthreads, double *out, uint8_t *pflags, void *trace,
                    uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out,
-                   double *inst_out) {
+                   double *inst_out, double *bank, uint8_t *bank_n) {
     return run_common(vm, seed, pid0, n, NULL, NULL, states, max_seg, nthreads, out, pflags, trace,
-                      trace_cap, trace_count, evals, mesh_out, inst_out);
+                      trace_cap, trace_count, evals, mesh_out, inst_out, bank, bank_n);
+}
+
+/* F1: next-cycle source.  M = total banked sites (history order, then site order).  Source
+ * particle j takes the site with flat index floor(u_j * M), u_j = first uniform of Philox block
+ * (seed; j, cycle, 0xF155), and an isotropic direction from block (seed; j, cycle, 0xF156).
+ * states_out: SoA [6][n_next].  Returns M (0: nothing banked, states untouched). */
+uint64_t orc_fission_source(void *vm, const double *bank, const uint8_t *bank_n, uint64_t n_prev,
+                            uint64_t seed, uint32_t cycle, uint64_t n_next, double *states_out) {
+    Model *m = vm;
+    const int ms = orc_max_sites(m);
+    uint64_t M = 0;
+    for (uint64_t h = 0; h < n_prev; ++h) M += bank_n[h];
+    if (M == 0) return 0;
+    for (uint64_t j = 0; j < n_next; ++j) {
+        double u, unused, xmu, xphi, om[3];
+        draw(seed, j, cycle, 0xF155u, &u, &unused);
+        uint64_t t = (uint64_t)floor(u * (double)M);
+        uint64_t h = 0, acc = 0;
+        while (!(t < acc + bank_n[h])) { acc += bank_n[h]; ++h; }  /* the site's history (plain scan) */
+        const double *site = bank + ((size_t)h * ms + (t - acc)) * 3;
+        draw(seed, j, cycle, 0xF156u, &xmu, &xphi);
+        iso(xmu, xphi, om);
+        for (int a = 0; a < 3; ++a) {
+            states_out[a * n_next + j] = site[a];
+            states_out[(3 + a) * n_next + j] = om[a];
+        }
+    }
+    return M;
 }
 
 /* ---------------------------------------------------------------- unit queries */

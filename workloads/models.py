@@ -46,8 +46,11 @@ class Spec:
         self.surfaces.append({"kind": kind, "coef": [float(c) for c in coef], "bc": bc})
         return len(self.surfaces) - 1
 
-    def mat(self, name: str, sigma_t: float, sigma_a: float) -> int:
-        self.materials.append({"name": name, "sigma_t": float(sigma_t), "sigma_a": float(sigma_a)})
+    def mat(self, name: str, sigma_t: float, sigma_a: float, nu_sigma_f: float = 0.0) -> int:
+        m = {"name": name, "sigma_t": float(sigma_t), "sigma_a": float(sigma_a)}
+        if nu_sigma_f:
+            m["nu_sigma_f"] = float(nu_sigma_f)            # one-group fission (reading F1)
+        self.materials.append(m)
         return len(self.materials) - 1
 
     def csg(self, name: str) -> int:
@@ -190,6 +193,15 @@ def c1_pincell(bc="reflect", uniform=None, void=False) -> dict:
     sp.root = root
     sp.source = {"lo": [-hp, -hp, 0.0], "hi": [hp, hp, HEIGHT]}
     return sp.to_dict()
+
+
+def with_fission(spec: dict, nu_sigma_f: dict) -> dict:
+    """Copy of a model spec with one-group nu Sigma_f on the named materials (reading F1)."""
+    out = copy.deepcopy(spec)
+    for m in out["materials"]:
+        if m["name"] in nu_sigma_f:
+            m["nu_sigma_f"] = float(nu_sigma_f[m["name"]])
+    return out
 
 
 # ---------------------------------------------------------------------------
@@ -452,12 +464,13 @@ def c5_deep(mixed: bool) -> dict:
 # ---------------------------------------------------------------------------
 # test models (P8-P12, O13)
 # ---------------------------------------------------------------------------
-def infinite_medium(sigma_t=1.0, sigma_a=0.25) -> dict:
-    """One material in an all-REFLECT box (P10): track length per history ~ Exp(Sigma_a)."""
+def infinite_medium(sigma_t=1.0, sigma_a=0.25, nu_sigma_f=0.0) -> dict:
+    """One material in an all-REFLECT box (P10): track length per history ~ Exp(Sigma_a).
+    With nu_sigma_f: k_inf = nu Sigma_f / Sigma_a (F1)."""
     sp = Spec("infinite_medium")
     root = sp.csg("root")
     box = _box(sp, (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0), "reflect")
-    m = sp.mat("m", sigma_t, sigma_a)
+    m = sp.mat("m", sigma_t, sigma_a, nu_sigma_f)
     sp.cell(root, box, material=m)
     sp.root = root
     sp.source = {"lo": [-1.0, -1.0, -1.0], "hi": [1.0, 1.0, 1.0]}
