@@ -40,7 +40,7 @@
 extern "C" {
 #endif
 
-#define NT_ABI_VERSION 3
+#define NT_ABI_VERSION 4
 
 typedef enum {
     NT_OK = 0,
@@ -149,6 +149,12 @@ nt_status nt_add_surface(nt_model* m, nt_surface_kind kind, const double* coef, 
 /* One-group macroscopic cross sections (1/cm): 0 <= sigma_a <= sigma_t (sigma_t = 0: void). */
 nt_status nt_add_material(nt_model* m, double sigma_t, double sigma_a, int32_t* id);
 
+/* One-group fission (Alg. 1-2; reading F1): material
+ * `mat` gets nu*Sigma_f >= 0 (> 0 needs sigma_a > 0; nu_sigma_f / sigma_a <= 200).  An absorption
+ * in it then banks floor(nu_sigma_f / sigma_a + xi) fission sites at the absorption point when
+ * the run passes outputs.bank.  NT_E_ID for a bad id; values are validated at nt_finalize. */
+nt_status nt_set_fission(nt_model* m, int32_t mat, double nu_sigma_f);
+
 nt_status nt_add_csg_universe(nt_model* m, int32_t* uid);
 
 /* A cell of CSG universe `uid` = intersection of signed half-spaces (Fig. 2):
@@ -226,9 +232,21 @@ typedef struct {
     int64_t mesh_bins;            /* voxels of the mesh set by nt_set_mesh (0: none) */
     int64_t n_instances;          /* material-cell instances (reading D1); 0 for pseudo-array
                                      builds or more than 2^31 - 1 instances (no instance tallies) */
+    int32_t max_sites;            /* fission sites one absorption can bank: floor(max nu_sigma_f/sigma_a) + 1 */
 } nt_model_info;
 
 nt_status nt_model_info_get(const nt_model* m, nt_model_info* info);
+
+/* Next cycle's fission source (F1, Alg. 1 power iteration): from the bank of n_prev histories
+ * (outputs.bank / bank_n of the previous nt_track*), draw n_next birth states into d_states
+ * (device SoA fp64 [6][n_next], for nt_track_states): particle j takes the site with flat index
+ * floor(u_j * M) in (history, site) order, M = total sites, u_j the first uniform of Philox block
+ * (key seed; counter j, cycle, 0xF155), and an isotropic direction from block (j, cycle, 0xF156).
+ * *total_sites = M; M = 0 leaves d_states untouched (the caller decides: subcritical collapse).
+ * Synchronises `cuda_stream` (M is needed on the host). */
+nt_status nt_fission_source(nt_model* m, const double* d_bank, const uint8_t* d_bank_n, uint64_t n_prev,
+                            uint64_t seed, uint32_t cycle, uint64_t n_next, double* d_states,
+                            uint64_t* total_sites, void* cuda_stream);
 
 /* Per-instance tallies (reading D1): material-cell instances are numbered by a depth-first
  * enumeration of the model -- a CSG universe's cells in id order (a material cell is one
@@ -272,6 +290,10 @@ typedef struct {
                                  (distributed-cell tally, reading D1), n_instances entries,
                                  accumulated.  Generic tracker, no NT_TRACE, no pseudo-array build,
                                  else NT_E_UNSUPPORTED */
+    double* bank;             /* device, optional (NULL = no fission bank, F1): n * max_sites * 3 fp64,
+                                 site k of history i at [(i * max_sites + k) * 3] (x, y, z) */
+    uint8_t* bank_n;          /* device, with bank: n entries, sites banked by each history (zeroed
+                                 by the call first); k = sum(bank_n) / n is the cycle's estimate */
 } nt_outputs;
 
 /* Track run->n histories born from (seed, pid) in the source box. Asynchronous on cuda_stream. */

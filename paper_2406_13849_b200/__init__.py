@@ -55,7 +55,7 @@ class ModelInfo(C.Structure):
                 ("n_universes", C.c_int32), ("max_depth", C.c_int32),
                 ("rect_specialisable", C.c_int32), ("rect_levels", C.c_int32),
                 ("n_bih_nodes", C.c_int32), ("out_len", C.c_int64), ("device_bytes", C.c_size_t),
-                ("mesh_bins", C.c_int64), ("n_instances", C.c_int64)]
+                ("mesh_bins", C.c_int64), ("n_instances", C.c_int64), ("max_sites", C.c_int32)]
 
 
 class Run(C.Structure):
@@ -69,7 +69,7 @@ class Outputs(C.Structure):
     _fields_ = [("out", C.c_void_p), ("pflags", C.c_void_p), ("pnseg", C.c_void_p),
                 ("pterm", C.c_void_p), ("trace", C.c_void_p),
                 ("trace_cap", C.c_uint64), ("trace_count", C.c_void_p), ("mesh", C.c_void_p),
-                ("inst", C.c_void_p)]
+                ("inst", C.c_void_p), ("bank", C.c_void_p), ("bank_n", C.c_void_p)]
 
 
 _lib = None
@@ -77,7 +77,8 @@ _lib = None
 SYMBOLS = ["nt_last_error", "nt_abi_version", "nt_model_create", "nt_model_destroy", "nt_add_surface",
            "nt_add_material", "nt_add_csg_universe", "nt_add_cell", "nt_add_rect_array", "nt_add_rect_edges",
            "nt_add_hex_array", "nt_set_root", "nt_set_mesh", "nt_build_opts_default", "nt_finalize",
-           "nt_model_info_get", "nt_material_cell_ids", "nt_instance_cells", "nt_bih_info", "nt_track",
+           "nt_model_info_get", "nt_material_cell_ids", "nt_instance_cells", "nt_set_fission",
+           "nt_fission_source", "nt_bih_info", "nt_track",
            "nt_track_states", "nt_track_host", "nt_find_cells", "nt_last_launch_count",
            "nt_selftest_arith"]
 
@@ -104,6 +105,9 @@ def lib():
         L.nt_set_root.argtypes = [vp, i32]
         L.nt_set_mesh.argtypes = [vp, dp, dp, dp]
         L.nt_instance_cells.argtypes = [vp, dp, C.c_int64]
+        L.nt_set_fission.argtypes = [vp, i32, C.c_double]
+        L.nt_fission_source.argtypes = [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, vp,
+                                        C.POINTER(C.c_uint64), vp]
         L.nt_build_opts_default.argtypes = [C.POINTER(BuildOpts)]
         L.nt_finalize.argtypes = [vp, C.POINTER(BuildOpts)]
         L.nt_model_info_get.argtypes = [vp, C.POINTER(ModelInfo)]
@@ -242,7 +246,9 @@ class Model:
         for s in spec["surfaces"]:
             m.add_surface(s["kind"], s["coef"], s["bc"])
         for mt in spec["materials"]:
-            m.add_material(mt["sigma_t"], mt["sigma_a"])
+            k = m.add_material(mt["sigma_t"], mt["sigma_a"])
+            if mt.get("nu_sigma_f", 0.0):
+                _check(m.L.nt_set_fission(m.h, k, mt["nu_sigma_f"]))
         for u in spec["universes"]:
             if u["kind"] == "csg":
                 uid = m.add_csg_universe()
@@ -293,7 +299,7 @@ class Model:
               max_segments: int = 0, tracker: str = "generic", pflags: bool = False,
               trace_cap: int = 0, states=None, out=None, stream=None, block_dim: int = 0,
               blocks_per_sm: int = 0, per_history: bool = False, scheduler: str = "block", mesh=None,
-              instances=None):
+              instances=None, bank: bool = False):
         """Track histories [pid_begin, pid_begin+n) on this model's GPU (async on `stream`).
         Returns a dict of device tensors: out (accumulated), pflags, trace, trace_count."""
         import torch
@@ -330,6 +336,12 @@ class Model:
             assert instances.numel() >= self.info["n_instances"] > 0
             o.inst = instances.data_ptr()
             res["inst"] = instances
+        if bank:                                   # fission bank (reading F1)
+            ms = self.info["max_sites"]
+            bk = torch.empty(max(n, 1) * ms * 3, dtype=torch.float64, device=dev)
+            bn = torch.empty(max(n, 1), dtype=torch.uint8, device=dev)
+            o.bank, o.bank_n = bk.data_ptr(), bn.data_ptr()
+            res["bank"], res["bank_n"] = bk, bn
         run = self.make_run(n, seed, pid_begin, lo, hi, max_segments, tracker, bool(trace_cap),
                             block_dim, blocks_per_sm, scheduler)
         sh = _stream_handle(stream)
@@ -364,6 +376,31 @@ class Model:
         _check(self.L.nt_find_cells(self.h, C.c_void_p(xyz.data_ptr()), n, C.c_void_p(cell.data_ptr()),
                                     C.c_void_p(fl.data_ptr()), _stream_handle(stream)))
         return cell, fl
+
+    def fission_source(self, bank, bank_n, n_prev: int, seed: int, cycle: int, n_next: int, stream=None):
+        """F1: next cycle's birth states [6, n_next] (device) drawn from a bank; returns (states, M)."""
+        import torch
+        st = torch.empty((6, max(n_next, 1)), dtype=torch.float64, device=torch.device("cuda", self.device))
+        M = C.c_uint64()
+        _check(self.L.nt_fission_source(self.h, C.c_void_p(bank.data_ptr()), C.c_void_p(bank_n.data_ptr()),
+                                        n_prev, seed, cycle, n_next, C.c_void_p(st.data_ptr()), C.byref(M),
+                                        _stream_handle(stream)))
+        return st[:, :n_next], int(M.value)
+
+    def power_iteration(self, n: int, cycles: int, seed: int = 240613849, scheduler: str = "block"):
+        """F1 power iteration (Alg. 1) on the device: cycle 0 born in the source box, later cycles
+        from the previous bank; cycle c uses pids [c << 32, (c << 32) + n).  Returns per-cycle k."""
+        import torch
+        ks, states = [], None
+        for c in range(cycles):
+            res = self.track(n, seed=seed, pid_begin=c << 32, bank=True, states=states, scheduler=scheduler)
+            nb = int(res["bank_n"][:n].sum().item())
+            ks.append(nb / n)
+            states, M = self.fission_source(res["bank"], res["bank_n"], n, seed, c, n)
+            if M == 0:
+                raise RuntimeError("fission source collapsed (no sites banked)")
+            states = states.contiguous()
+        return ks
 
     def instance_cells(self) -> np.ndarray:
         """Material-cell bin of every material-cell instance (reading D1)."""

@@ -66,9 +66,12 @@ void validate(const std::vector<HSurf>& S, const std::vector<HMat>& M, const std
       fail("surface %ld: zero plane normal", i);
     if (s.bc == 2 && s.kind > S_PZ) fail("surface %ld: REFLECT only on PX/PY/PZ", i);
   }
-  for (int i = 0; i < nm; ++i)
+  for (int i = 0; i < nm; ++i) {
     if (!finite(M[i].st) || !finite(M[i].sa) || M[i].st < 0 || M[i].sa < 0 || M[i].sa > M[i].st)
       fail("material %ld: need 0 <= sigma_a <= sigma_t", i);
+    if (!finite(M[i].nusf) || M[i].nusf < 0 || (M[i].nusf > 0 && !(M[i].sa > 0)) || M[i].nusf / (M[i].sa > 0 ? M[i].sa : 1) > 200)
+      fail("material %ld: need nu_sigma_f >= 0, sigma_a > 0 when fissile, nu_sigma_f / sigma_a <= 200", i);
+  }
   for (int i = 0; i < (int)C.size(); ++i) {
     const HCell& c = C[i];
     std::vector<int> ids = c.sid;
@@ -692,6 +695,9 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
       const HMat& m = M[c.fill];
       F.mc_st.push_back(m.st);
       F.mc_pabs.push_back(m.st > 0.0 ? m.sa / m.st : 0.0);
+      const double nut = m.nusf > 0.0 ? m.nusf / m.sa : 0.0;      // F1: IEEE division, once
+      F.mc_nut.push_back(nut);
+      F.max_sites = std::max(F.max_sites, (int)std::floor(nut) + 1);
       F.mc_cell.push_back(i);
     } else {
       F.cell_fill.push_back(-1 - c.fill);

@@ -126,8 +126,15 @@ nt_status nt_add_surface(nt_model* m, nt_surface_kind kind, const double* coef, 
 
 nt_status nt_add_material(nt_model* m, double st, double sa, int32_t* id) {
   CHECK_BUILDER(m);
-  m->m.push_back({st, sa});
+  m->m.push_back({st, sa, 0.0});
   if (id) *id = (int32_t)m->m.size() - 1;
+  return NT_OK;
+}
+
+nt_status nt_set_fission(nt_model* m, int32_t mat, double nu_sigma_f) {
+  CHECK_BUILDER(m);
+  if (mat < 0 || mat >= (int)m->m.size()) return err(NT_E_ID, "nt_set_fission: material id out of range");
+  m->m[mat].nusf = nu_sigma_f;        // validated at nt_finalize
   return NT_OK;
 }
 
@@ -288,7 +295,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
                o_hs = place(blob, F.hs), o_chs = place(blob, F.cell_hs), o_cf = place(blob, F.cell_fill),
                o_ctr = place(blob, F.cell_tr), o_univ = place(blob, F.univ), o_bih = place(blob, F.bih),
                o_leaf = place(blob, F.bih_leaf), o_fills = place(blob, F.fills), o_st = place(blob, F.mc_st),
-               o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell),
+               o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell), o_nut = place(blob, F.mc_nut),
                o_edges = place(blob, F.edges), o_uinst = place(blob, F.univ_inst),
                o_ioff = place(blob, F.inst_off), o_cpos = place(blob, F.cell_pos);
   const size_t o_pou = place(blob, F.r_pin_of_univ), o_poff = place(blob, F.r_pin_off),
@@ -326,6 +333,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     g.fills = (const int32_t*)(b + o_fills);
     g.mc_st = (const double*)(b + o_st);
     g.mc_pabs = (const double*)(b + o_pabs);
+    g.mc_nut = (const double*)(b + o_nut);
     g.mc_cell = (const int32_t*)(b + o_mcc);
     g.edges = (const double*)(b + o_edges);
     g.univ_inst = (const int32_t*)(b + o_uinst);
@@ -347,6 +355,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
   g.root_kind = F.univ[F.root].kind;
   g.features = F.features;
   g.mesh_on = m->mesh_on ? 1 : 0;
+  g.max_sites = F.max_sites;
   for (int a = 0; a < 3; ++a) { g.mesh_lo[a] = m->mesh_lo[a]; g.mesh_d[a] = m->mesh_d[a]; g.mesh_n[a] = m->mesh_n[a]; }
   m->finalized = true;
   return NT_OK;
@@ -368,6 +377,28 @@ nt_status nt_model_info_get(const nt_model* m, nt_model_info* info) {
   info->device_bytes = m->blob_bytes;
   info->mesh_bins = m->mesh_on ? (int64_t)m->mesh_n[0] * m->mesh_n[1] * m->mesh_n[2] : 0;
   info->n_instances = F.n_inst;
+  info->max_sites = F.max_sites;
+  return NT_OK;
+}
+
+nt_status nt_fission_source(nt_model* m, const double* d_bank, const uint8_t* d_bank_n, uint64_t n_prev,
+                            uint64_t seed, uint32_t cycle, uint64_t n_next, double* d_states,
+                            uint64_t* total_sites, void* stream) {
+  if (!m || !total_sites || (n_prev && (!d_bank || !d_bank_n)) || (n_next && !d_states))
+    return err(NT_E_ARG, "nt_fission_source: NULL argument");
+  if (!m->finalized || !m->blob) return err(NT_E_ORDER, "nt_fission_source: model not finalized on a device");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != m->device) cudaSetDevice(m->device);
+  unsigned long long M = 0;
+  const bool f0 = m->g.features == 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = f0 ? f0::fission_source(m->g, d_bank, d_bank_n, n_prev, seed, cycle, n_next, d_states, &M, s)
+                     : f7::fission_source(m->g, d_bank, d_bank_n, n_prev, seed, cycle, n_next, d_states, &M, s);
+  if (prev != m->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_err(e, "nt_fission_source");
+  *total_sites = M;
+  m->last_launches = M ? 5 : 3;
   return NT_OK;
 }
 
@@ -466,6 +497,10 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   R.trace_count = reinterpret_cast<unsigned long long*>(o->trace_count);
   R.mesh = m->g.mesh_on ? o->mesh : nullptr;
   R.inst = o->inst;
+  R.bank = o->bank;
+  R.bank_n = o->bank_n;
+  if ((o->bank == nullptr) != (o->bank_n == nullptr))
+    return err(NT_E_ARG, std::string(who) + ": outputs.bank and outputs.bank_n go together");
   const unsigned slot = m->slot.fetch_add(1) % kSlots;
   R.counter = m->counters + slot;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
@@ -491,6 +526,7 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
     }
     if (e == cudaSuccess) g.trk = reinterpret_cast<const void* const*>(static_cast<char*>(m->dp_objs) + tab_off);
   }
+  if (e == cudaSuccess && R.bank_n) e = cudaMemsetAsync(R.bank_n, 0, run->n, s);   // F1: no sites by default
   int grid = 0;
   if (e == cudaSuccess) {
     const bool st = d_states != nullptr, f0 = m->g.features == 0;

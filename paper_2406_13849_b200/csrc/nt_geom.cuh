@@ -217,6 +217,19 @@ struct Best {
   }
 };
 
+// ---- F1 fission bank: an absorption in material cell mc banks floor(nut + xi) sites at the
+// absorption point (xi = the collision draw's second uniform, unused by an absorption).
+__device__ __forceinline__ void bank_sites(const DevGeom& g, double* bank, uint8_t* bank_n, int mc, uint64_t idx,
+                                           double xi, double x, double y, double z) {
+  const double nut = ld(g.mc_nut + mc);
+  if (!(nut > 0.0)) return;
+  int ns = static_cast<int>(floor(nut + xi));
+  if (ns > g.max_sites) ns = g.max_sites;
+  double* p = bank + idx * static_cast<uint64_t>(g.max_sites) * 3;
+  for (int k = 0; k < ns; ++k) { p[3 * k] = x; p[3 * k + 1] = y; p[3 * k + 2] = z; }
+  bank_n[idx] = static_cast<uint8_t>(ns);
+}
+
 // ---- superimposed mesh track-length tally (NEXT-2; reading M1).  3-D DDA along the
 // segment r + t om, t in [0, s].  The cut parameters are (E_a(i) - r_a) / om_a with
 // E_a(i) = lo_a + i d_a -- the oracle's -- so every scored piece is the oracle's piece.  Pieces

@@ -24,6 +24,8 @@ struct KRun {
   double* slices;                   // [grid][n_mc] zeroed per-block track-length tallies (global)
   double* mesh;                     // optional per-voxel track length (M1), accumulated
   double* inst;                     // optional per-instance track length (D1), accumulated
+  double* bank;                     // optional fission sites (F1): [n][max_sites][3]
+  uint8_t* bank_n;                  //   sites banked by each history (zeroed by the caller)
 };
 
 // one copy of the launchers per compiled feature set (track_f0.cu, track_f7.cu)
@@ -39,6 +41,9 @@ cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, 
                       cudaStream_t stream, int* grid_out); \
 cudaError_t dp_init(const DevGeom& g, void* objs, void* tab, cudaStream_t stream); \
 size_t dp_object_bytes(); \
+cudaError_t fission_source(const DevGeom& g, const double* bank, const uint8_t* bank_n, uint64_t n_prev, \
+                           uint64_t seed, uint32_t cycle, uint64_t n_next, double* states, \
+                           unsigned long long* M_host, cudaStream_t stream); \
 cudaError_t selftest_arith(uint64_t n, uint64_t seed, unsigned long long* d_bad); \
 cudaError_t bih_stats(unsigned long long* host4, bool reset); \
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell, \

@@ -83,6 +83,7 @@ struct DevGeom {
   const int32_t* fills;
   const double* mc_st;        // per material cell: sigma_t
   const double* mc_pabs;      // per material cell: sigma_a / sigma_t (O14)
+  const double* mc_nut;       // per material cell: nu Sigma_f / Sigma_a (F1)
   const int32_t* mc_cell;     // per material cell: global cell id (trace)
   const double* edges;        // non-uniform rect edges (N1): per array x[n0+1] y[n1+1] z[n2+1]
   const int32_t* univ_inst;   // per-instance tallies (D1): per universe, base into inst_off
@@ -93,6 +94,7 @@ struct DevGeom {
   const void* const* trk;     // DP dispatch only: per-universe tracker object pointers (dp_tracker.cuh)
   double mesh_lo[3], mesh_d[3];   // superimposed mesh (M1): voxel edges lo + i d
   int32_t mesh_n[3], mesh_on;
+  int32_t max_sites;              // F1: sites one absorption can bank
 };
 
 // Rect-specialised tracker tables (Alg. 9-10): root = axis box or concentric CZ annuli between a

@@ -11,7 +11,7 @@
 namespace nt {
 
 struct HSurf { int kind, bc; double c[4]; };
-struct HMat { double st, sa; };
+struct HMat { double st, sa, nusf = 0.0; };
 struct HCell {
   int uid;
   std::vector<int> sid, sense;   // as given; sorted during flattening
@@ -55,7 +55,8 @@ struct Flat {
   std::vector<DUniv> univ;
   std::vector<BihNode> bih;
   std::vector<int32_t> bih_leaf, fills;
-  std::vector<double> mc_st, mc_pabs;
+  std::vector<double> mc_st, mc_pabs, mc_nut;   // mc_nut: nu Sigma_f / Sigma_a (F1)
+  int max_sites = 1;                           // F1: floor(max nut) + 1
   std::vector<int32_t> mc_cell;
   std::vector<double> edges;        // non-uniform rect edges (N1)
   // per-instance tallies (D1): instance = sum over levels of inst_off[univ_inst[u] + child]

@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
           draw2(R.seed, pid, epoch, 0, xa, xb);
           if (xa < ld(g.mc_pabs + mc)) {
             term = NT_T_ABSORBED;
+            if (R.bank) bank_sites(g, R.bank, R.bank_n, mc, idx, xb, rx, ry, rz);
             emit<TRACE>(R, pid, nseg - 1, NT_EV_COLLIDE, -1, -1, cell_before, cell_before, s, NT_T_ABSORBED,
                         flags);
           } else {

@@ -387,6 +387,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           draw2(R.seed, pid, epoch, 0, xa, xb);
           if (xa < ld(g.mc_pabs + mc)) {
             term = NT_T_ABSORBED;
+            if (R.bank) bank_sites(g, R.bank, R.bank_n, mc, idx, xb, rx, ry, rz);
             emit<TRACE>(R, pid, nseg - 1, NT_EV_COLLIDE, -1, -1, cell_before, cell_before, s, NT_T_ABSORBED,
                         flags);
           } else {
@@ -679,6 +680,101 @@ __global__ void k_selftest_arith(uint64_t n, uint64_t seed, unsigned long long* 
     const double q3 = fdiv(e - xx, x1 - 0.5), q4 = (e - xx) / (x1 - 0.5);
     if (__double_as_longlong(q3) != __double_as_longlong(q4)) atomicAdd(bad, 1ull);
   }
+}
+
+// ---------------------------------------------------------------- F1: next-cycle fission source
+// exclusive prefix of the per-history site counts (three passes: block sums, one-block scan of
+// the sums, per-element prefix), then one thread per source particle: flat site index
+// floor(u * M), binary search for its history, isotropic direction (see nt_fission_source).
+constexpr int kScanB = 1024;
+
+__global__ void __launch_bounds__(kScanB) k_bank_block_sums(const uint8_t* bn, uint64_t n, unsigned long long* sums) {
+  __shared__ unsigned long long sh[kScanB / 32];
+  const uint64_t i = blockIdx.x * (uint64_t)kScanB + threadIdx.x;
+  unsigned long long v = i < n ? bn[i] : 0ull;
+  for (int o = 16; o; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (int k = 0; k < kScanB / 32; ++k) t += sh[k];
+    sums[blockIdx.x] = t;
+  }
+}
+
+__global__ void k_bank_scan_sums(unsigned long long* sums, uint64_t nb, unsigned long long* total) {
+  if (threadIdx.x != 0) return;                       // nb <= ~1e5: one thread is plenty
+  unsigned long long acc = 0;
+  for (uint64_t b = 0; b < nb; ++b) { const unsigned long long v = sums[b]; sums[b] = acc; acc += v; }
+  *total = acc;
+}
+
+__global__ void __launch_bounds__(kScanB) k_bank_prefix(const uint8_t* bn, uint64_t n, const unsigned long long* offs,
+                                                        unsigned long long* prefix) {
+  __shared__ unsigned long long sh[kScanB / 32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const uint64_t i = blockIdx.x * (uint64_t)kScanB + threadIdx.x;
+  const unsigned long long v = i < n ? bn[i] : 0ull;
+  unsigned long long x = v;                           // inclusive warp scan
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) sh[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    unsigned long long acc = 0;
+    for (int k = 0; k < kScanB / 32; ++k) { const unsigned long long t = sh[k]; sh[k] = acc; acc += t; }
+  }
+  __syncthreads();
+  if (i < n) prefix[i] = offs[blockIdx.x] + sh[w] + (x - v);
+}
+
+__global__ void k_fission_source(const DevGeom g, const double* bank, const uint8_t* bn,
+                                 const unsigned long long* prefix, uint64_t n_prev, unsigned long long M,
+                                 uint64_t seed, uint32_t cycle, uint64_t n_next, double* st) {
+  for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_next; j += (uint64_t)gridDim.x * blockDim.x) {
+    double u, unused, xmu, xphi, ox, oy, oz;
+    draw2(seed, j, cycle, 0xF155u, u, unused);
+    const unsigned long long t = static_cast<unsigned long long>(floor(u * static_cast<double>(M)));
+    uint64_t lo = 0, hi = n_prev;                     // last h with prefix[h] <= t
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (prefix[mid] <= t) lo = mid; else hi = mid;
+    }
+    const double* p = bank + (lo * static_cast<uint64_t>(g.max_sites) + (t - prefix[lo])) * 3;
+    draw2(seed, j, cycle, 0xF156u, xmu, xphi);
+    isotropic(xmu, xphi, ox, oy, oz);
+    st[j] = p[0]; st[n_next + j] = p[1]; st[2 * n_next + j] = p[2];
+    st[3 * n_next + j] = ox; st[4 * n_next + j] = oy; st[5 * n_next + j] = oz;
+    (void)bn;
+  }
+}
+
+cudaError_t fission_source(const DevGeom& g, const double* bank, const uint8_t* bank_n, uint64_t n_prev,
+                           uint64_t seed, uint32_t cycle, uint64_t n_next, double* states,
+                           unsigned long long* M_host, cudaStream_t stream) {
+  *M_host = 0;
+  if (n_prev == 0) return cudaSuccess;
+  const uint64_t nb = (n_prev + kScanB - 1) / kScanB;
+  unsigned long long* scratch = nullptr;             // sums[nb] | total | prefix[n_prev]
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (nb + 1 + n_prev) * sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  unsigned long long *sums = scratch, *total = scratch + nb, *prefix = scratch + nb + 1;
+  k_bank_block_sums<<<(unsigned)nb, kScanB, 0, stream>>>(bank_n, n_prev, sums);
+  k_bank_scan_sums<<<1, 32, 0, stream>>>(sums, nb, total);
+  k_bank_prefix<<<(unsigned)nb, kScanB, 0, stream>>>(bank_n, n_prev, sums, prefix);
+  e = cudaMemcpyAsync(M_host, total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  if (e == cudaSuccess && *M_host > 0 && n_next > 0) {
+    uint64_t grid = (n_next + 255) / 256;
+    if (grid > 148 * 16) grid = 148 * 16;
+    k_fission_source<<<(unsigned)grid, 256, 0, stream>>>(g, bank, bank_n, prefix, n_prev, *M_host, seed, cycle,
+                                                          n_next, states);
+    e = cudaGetLastError();
+  }
+  const cudaError_t e2 = cudaFreeAsync(scratch, stream);
+  return e != cudaSuccess ? e : e2;
 }
 
 cudaError_t bih_stats(unsigned long long* host4, bool reset) {

@@ -379,6 +379,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
         const int cb = TRACE ? ld(g.mc_cell + mc) : 0;
         if (xa < ld(g.mc_pabs + mc)) {
           absorbed = true;
+          if (R.bank) bank_sites(g, R.bank, R.bank_n, mc, sidx[slot], xb, sx[slot], sy[slot], sz[slot]);
           if (TRACE) emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_ABSORBED, sflags[slot]);
           finalize(slot, NT_T_ABSORBED);
         } else {

@@ -29,7 +29,7 @@ def test_exports_every_header_symbol(nt):
     missing = [s for s in declared if not hasattr(L, s)]
     assert not missing, missing
     assert set(declared) == set(nt.SYMBOLS)
-    assert L.nt_abi_version() == 3
+    assert L.nt_abi_version() == 4
 
 
 def _host(nt, spec, **kw):
@@ -205,3 +205,15 @@ def test_instance_tables_host(nt, oracle_mod):
         assert m.info["n_instances"] == om.n_instances()
         assert np.array_equal(m.instance_cells(), om.instance_cells())
     assert _host(nt, workloads.config("c2")[0], pseudo_array=True).info["n_instances"] == 0
+
+
+def test_fission_host_validation(nt):
+    """nt_set_fission (F1): max_sites in the model info; a fissile material without absorption is
+    rejected at nt_finalize."""
+    spec = workloads.models.with_fission(workloads.config("c1")[0], {"uo2": 0.15})
+    m = _host(nt, spec)
+    assert m.info["max_sites"] == int(np.floor(0.15 / 0.12)) + 1
+    assert _host(nt, workloads.config("c1")[0]).info["max_sites"] == 1
+    bad = workloads.models.with_fission(workloads.config("c1")[0], {"gap": 0.1})   # sigma_a = 0
+    with pytest.raises(nt.NtError, match="nu_sigma_f"):
+        _host(nt, bad)

@@ -211,6 +211,63 @@ def test_mesh_and_instance_tallies_together(nt, orc):
         assert np.all(np.abs(got - ref) <= 1e-9 * np.abs(ref) + 1e-12 * ref.max()), key
 
 
+FISSILE = {
+    "c1": lambda: workloads.models.with_fission(workloads.config("c1")[0], {"uo2": 0.15}),
+    "c3": lambda: workloads.models.with_fission(workloads.config("c3")[0],
+                                                 {"uo2_a": 0.13, "uo2_b": 0.16, "uo2_c": 0.19}),
+}
+
+
+@pytest.mark.parametrize("sched", ["block", "rounds", "warp", "history", "dp", "rect"])
+@pytest.mark.parametrize("cfg", list(FISSILE))
+def test_fission_bank_parity(nt, orc, cfg, sched):
+    """F1 fission bank: sites per history and site coordinates bit-exact vs the oracle."""
+    spec = FISSILE[cfg]()
+    m = nt.Model.from_spec(spec, device=0)
+    om = orc.OracleModel.from_spec(spec)
+    assert m.info["max_sites"] == om.max_sites()
+    n = 700
+    kw = dict(tracker="rect", scheduler="history") if sched == "rect" else dict(scheduler=sched)
+    res = m.track(n, seed=12, bank=True, **kw)
+    torch.cuda.synchronize()
+    o = om.run(n, seed=12, bank=True)
+    bn = res["bank_n"].cpu().numpy()[:n]
+    assert np.array_equal(bn, o["bank_n"]) and bn.sum() > 50
+    bk = res["bank"].cpu().numpy()[:n * om.max_sites() * 3].reshape(n, om.max_sites(), 3)
+    for h in np.nonzero(bn)[0]:
+        assert np.array_equal(bk[h, :bn[h]], o["bank"][h, :bn[h]])
+
+
+def test_fission_source_and_power_iteration_parity(nt, orc):
+    """F1 source resampling on the device = the oracle's (bit-exact states), and three power
+    iteration cycles give the oracle's k sequence exactly."""
+    spec = FISSILE["c1"]()
+    m = nt.Model.from_spec(spec, device=0)
+    om = orc.OracleModel.from_spec(spec)
+    n = 1500
+    res = m.track(n, seed=3, bank=True)
+    torch.cuda.synchronize()
+    st, M = m.fission_source(res["bank"], res["bank_n"], n, seed=3, cycle=0, n_next=1200)
+    torch.cuda.synchronize()
+    ms = om.max_sites()
+    bank = res["bank"].cpu().numpy()[:n * ms * 3].reshape(n, ms, 3)
+    bank_n = res["bank_n"].cpu().numpy()[:n]
+    ost, oM = om.fission_source(np.where(np.arange(ms)[None, :, None] < bank_n[:, None, None], bank, 0.0),
+                                bank_n, seed=3, cycle=0, n_next=1200)
+    assert M == oM == int(bank_n.sum())
+    assert np.array_equal(st.cpu().numpy(), ost)
+    assert m.power_iteration(n, cycles=3, seed=5) == om.power_iteration(n, cycles=3, seed=5)
+
+
+def test_fission_k_inf_on_device(nt):
+    """Infinite medium with fission: the device's k estimates k_inf = nu Sigma_f / Sigma_a."""
+    spec = workloads.infinite_medium(1.0, 0.25, 0.55)
+    m = nt.Model.from_spec(spec, device=0)
+    ks = m.power_iteration(200000, cycles=3, seed=9)
+    nut, p = 2.2, 0.2
+    assert abs(np.mean(ks) - nut) < 4.5 * np.sqrt(p * (1 - p) / (3 * 200000))
+
+
 def test_dp_dispatch_rejects_other_schedulers(nt):
     """NT_DP is a dispatch mode of the block-queue scheduler only (nestrack.h)."""
     spec, _ = workloads.config("c1")
