@@ -248,6 +248,19 @@ nt_status nt_fission_source(nt_model* m, const double* d_bank, const uint8_t* d_
                             uint64_t seed, uint32_t cycle, uint64_t n_next, double* d_states,
                             uint64_t* total_sites, void* cuda_stream);
 
+/* The two halves of nt_fission_source, for multi-GPU power iteration (the all-gather of the sites
+ * happens between them, see paper_2406_13849_b200.power_iteration_distributed):
+ * nt_bank_compact writes the banked sites as a flat list in (history, site) order into d_sites
+ * (device, capacity n * max_sites * 3 fp64) and returns their number (synchronises the stream);
+ * nt_source_from_sites draws source particles J = j_begin .. j_begin + n_next - 1 from a flat list
+ * of total_sites sites (site floor(u_J * total_sites), u_J from Philox(seed; J, cycle, 0xF155),
+ * direction from block 0xF156) into d_states [6][n_next].  NT_E_ARG when total_sites = 0. */
+nt_status nt_bank_compact(nt_model* m, const double* d_bank, const uint8_t* d_bank_n, uint64_t n, double* d_sites,
+                          uint64_t* total_sites, void* cuda_stream);
+nt_status nt_source_from_sites(nt_model* m, const double* d_sites, uint64_t total_sites, uint64_t seed,
+                               uint32_t cycle, uint64_t j_begin, uint64_t n_next, double* d_states,
+                               void* cuda_stream);
+
 /* Per-instance tallies (reading D1): material-cell instances are numbered by a depth-first
  * enumeration of the model -- a CSG universe's cells in id order (a material cell is one
  * instance, a fill cell contributes its universe's instances), an array's tiles in fill order,

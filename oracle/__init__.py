@@ -72,6 +72,7 @@ def lib():
         L.orc_max_sites.argtypes = [vp]
         L.orc_fission_source.argtypes = [vp, dp, dp, u64, u64, C.c_uint32, u64, dp]
         L.orc_fission_source.restype = u64
+        L.orc_source_from_sites.argtypes = [dp, u64, u64, C.c_uint32, u64, u64, dp]
         L.orc_n_instances.argtypes = [vp]
         L.orc_n_instances.restype = C.c_long
         L.orc_instance_cells.argtypes = [vp, dp]
@@ -273,6 +274,18 @@ class OracleModel:
         st = np.zeros((6, max(n_next, 1)))
         M = self.L.orc_fission_source(self.h, _p(bank), _p(bank_n), len(bank_n), seed, cycle, n_next, _p(st))
         return st[:, :n_next], int(M)
+
+    @staticmethod
+    def bank_sites(bank: np.ndarray, bank_n: np.ndarray) -> np.ndarray:
+        """Flat (history, site)-ordered list of banked sites [M, 3] (test helper)."""
+        return np.concatenate([bank[h, :bank_n[h]] for h in range(len(bank_n))] + [np.zeros((0, 3))])
+
+    def source_from_sites(self, sites: np.ndarray, seed: int, cycle: int, j_begin: int, n_next: int):
+        """F1 multi-rank form: particles j_begin .. j_begin + n_next - 1 from a flat site list."""
+        sites = np.ascontiguousarray(sites, dtype=np.float64).reshape(-1, 3)
+        st = np.zeros((6, max(n_next, 1)))
+        self.L.orc_source_from_sites(_p(sites), len(sites), seed, cycle, j_begin, n_next, _p(st))
+        return st[:, :n_next]
 
     def power_iteration(self, n: int, cycles: int, seed: int = 240613849):
         """F1 power iteration (Alg. 1): cycle 0 born in the source box, then from the bank; histories

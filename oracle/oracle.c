@@ -1229,6 +1229,24 @@ int orc_run_states(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const dou
                       trace_cap, trace_count, evals, mesh_out, inst_out, bank, bank_n);
 }
 
+/* F1: source particles J = j_begin .. j_begin + n_next - 1 drawn from a flat site list (the
+ * multi-rank form: the list is every rank's bank in rank, history, site order). */
+void orc_source_from_sites(const double *sites, uint64_t M, uint64_t seed, uint32_t cycle, uint64_t j_begin,
+                           uint64_t n_next, double *states_out) {
+    for (uint64_t j = 0; j < n_next; ++j) {
+        const uint64_t J = j_begin + j;
+        double u, unused, xmu, xphi, om[3];
+        draw(seed, J, cycle, 0xF155u, &u, &unused);
+        const uint64_t t = (uint64_t)floor(u * (double)M);
+        draw(seed, J, cycle, 0xF156u, &xmu, &xphi);
+        iso(xmu, xphi, om);
+        for (int a = 0; a < 3; ++a) {
+            states_out[a * n_next + j] = sites[t * 3 + a];
+            states_out[(3 + a) * n_next + j] = om[a];
+        }
+    }
+}
+
 /* F1: next-cycle source.  M = total banked sites (history order, then site order).  Source
  * particle j takes the site with flat index floor(u_j * M), u_j = first uniform of Philox block
  * (seed; j, cycle, 0xF155), and an isotropic direction from block (seed; j, cycle, 0xF156).

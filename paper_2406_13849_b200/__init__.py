@@ -78,7 +78,7 @@ SYMBOLS = ["nt_last_error", "nt_abi_version", "nt_model_create", "nt_model_destr
            "nt_add_material", "nt_add_csg_universe", "nt_add_cell", "nt_add_rect_array", "nt_add_rect_edges",
            "nt_add_hex_array", "nt_set_root", "nt_set_mesh", "nt_build_opts_default", "nt_finalize",
            "nt_model_info_get", "nt_material_cell_ids", "nt_instance_cells", "nt_set_fission",
-           "nt_fission_source", "nt_bih_info", "nt_track",
+           "nt_fission_source", "nt_bank_compact", "nt_source_from_sites", "nt_bih_info", "nt_track",
            "nt_track_states", "nt_track_host", "nt_find_cells", "nt_last_launch_count",
            "nt_selftest_arith"]
 
@@ -106,6 +106,8 @@ def lib():
         L.nt_set_mesh.argtypes = [vp, dp, dp, dp]
         L.nt_instance_cells.argtypes = [vp, dp, C.c_int64]
         L.nt_set_fission.argtypes = [vp, i32, C.c_double]
+        L.nt_bank_compact.argtypes = [vp, vp, vp, C.c_uint64, vp, C.POINTER(C.c_uint64), vp]
+        L.nt_source_from_sites.argtypes = [vp, vp, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, C.c_uint64, vp, vp]
         L.nt_fission_source.argtypes = [vp, vp, vp, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint64, vp,
                                         C.POINTER(C.c_uint64), vp]
         L.nt_build_opts_default.argtypes = [C.POINTER(BuildOpts)]
@@ -459,3 +461,59 @@ def track_distributed(model: Model, n_total: int, seed: int, pid_begin: int = 0,
     if world > 1:
         dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
     return out
+
+
+def power_iteration_distributed(model: Model, n: int, cycles: int, seed: int = 240613849, group=None,
+                                track_fn=None, sample_fn=None, scheduler: str = "block"):
+    """Multi-GPU power iteration (reading F1, Alg. 1): every rank tracks n histories per cycle
+    (cycle c, rank r: pids (c << 32) + r n ...), compacts its fission bank, and the ranks
+    all-gather the site counts and the sites (the cycle's real exchange: the next source is drawn
+    from the global bank).  Rank r then draws source particles J = r n .. (r + 1) n - 1 from the
+    (rank, history, site)-ordered global list, so the result equals one process tracking all
+    world * n histories.  Returns the k estimate of every cycle (the same on every rank).
+
+    track_fn(n, pid_begin, states, cycle) -> (sites [M_r, 3] tensor, M_r) and
+    sample_fn(sites, M, cycle, j_begin, n) -> states override the device calls (CPU tests)."""
+    import torch
+    import torch.distributed as dist
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    if track_fn is None:
+        def track_fn(nn, pid0, states, cycle):
+            res = model.track(nn, seed=seed, pid_begin=pid0, bank=True, states=states, scheduler=scheduler)
+            ms = model.info["max_sites"]
+            sites = torch.empty(max(nn * ms, 1) * 3, dtype=torch.float64, device=res["bank"].device)
+            M = C.c_uint64()
+            _check(model.L.nt_bank_compact(model.h, C.c_void_p(res["bank"].data_ptr()),
+                                           C.c_void_p(res["bank_n"].data_ptr()), nn,
+                                           C.c_void_p(sites.data_ptr()), C.byref(M), None))
+            return sites[:3 * M.value].view(-1, 3), int(M.value)
+    if sample_fn is None:
+        def sample_fn(sites, M, cycle, j0, nn):
+            st = torch.empty((6, max(nn, 1)), dtype=torch.float64, device=sites.device)
+            sites = sites.contiguous()
+            _check(model.L.nt_source_from_sites(model.h, C.c_void_p(sites.data_ptr()), M, seed, cycle, j0, nn,
+                                                C.c_void_p(st.data_ptr()), None))
+            return st[:, :nn].contiguous()
+    ks, states = [], None
+    for c in range(cycles):
+        sites, Mr = track_fn(n, (c << 32) + rank * n, states, c)
+        if world > 1:
+            cnt = torch.tensor([Mr], dtype=torch.int64, device=sites.device)
+            counts = [torch.zeros_like(cnt) for _ in range(world)]
+            dist.all_gather(counts, cnt, group=group)
+            counts = [int(x.item()) for x in counts]
+            pad = max(max(counts), 1)
+            buf = torch.zeros((pad, 3), dtype=torch.float64, device=sites.device)
+            buf[:Mr] = sites
+            bufs = [torch.zeros_like(buf) for _ in range(world)]
+            dist.all_gather(bufs, buf, group=group)
+            sites = torch.cat([bufs[r][:counts[r]] for r in range(world)])
+            M = sum(counts)
+        else:
+            M = Mr
+        ks.append(M / (world * n))
+        if M == 0:
+            raise RuntimeError("fission source collapsed (no sites banked)")
+        states = sample_fn(sites, M, c, rank * n, n)
+    return ks

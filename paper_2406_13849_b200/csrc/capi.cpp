@@ -402,6 +402,41 @@ nt_status nt_fission_source(nt_model* m, const double* d_bank, const uint8_t* d_
   return NT_OK;
 }
 
+nt_status nt_bank_compact(nt_model* m, const double* d_bank, const uint8_t* d_bank_n, uint64_t n, double* d_sites,
+                          uint64_t* total_sites, void* stream) {
+  if (!m || !total_sites || (n && (!d_bank || !d_bank_n || !d_sites)))
+    return err(NT_E_ARG, "nt_bank_compact: NULL argument");
+  if (!m->finalized || !m->blob) return err(NT_E_ORDER, "nt_bank_compact: model not finalized on a device");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != m->device) cudaSetDevice(m->device);
+  unsigned long long M = 0;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = m->g.features == 0 ? f0::bank_compact(m->g, d_bank, d_bank_n, n, d_sites, &M, s)
+                                     : f7::bank_compact(m->g, d_bank, d_bank_n, n, d_sites, &M, s);
+  if (prev != m->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_err(e, "nt_bank_compact");
+  *total_sites = M;
+  return NT_OK;
+}
+
+nt_status nt_source_from_sites(nt_model* m, const double* d_sites, uint64_t total_sites, uint64_t seed,
+                               uint32_t cycle, uint64_t j_begin, uint64_t n_next, double* d_states, void* stream) {
+  if (!m || (total_sites && !d_sites) || (n_next && !d_states)) return err(NT_E_ARG, "nt_source_from_sites: NULL argument");
+  if (!m->finalized || !m->blob) return err(NT_E_ORDER, "nt_source_from_sites: model not finalized on a device");
+  if (total_sites == 0 && n_next) return err(NT_E_ARG, "nt_source_from_sites: no sites (subcritical collapse)");
+  int prev = 0;
+  cudaGetDevice(&prev);
+  if (prev != m->device) cudaSetDevice(m->device);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e = m->g.features == 0 ? f0::source_from_sites(d_sites, total_sites, seed, cycle, j_begin, n_next, d_states, s)
+                                     : f7::source_from_sites(d_sites, total_sites, seed, cycle, j_begin, n_next, d_states, s);
+  if (prev != m->device) cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_err(e, "nt_source_from_sites");
+  m->last_launches = 1;
+  return NT_OK;
+}
+
 nt_status nt_instance_cells(const nt_model* m, int32_t* out, int64_t cap) {
   if (!m || !out) return err(NT_E_ARG, "nt_instance_cells: NULL argument");
   if (!m->finalized) return err(NT_E_ORDER, "nt_instance_cells: model not finalized");

@@ -41,6 +41,10 @@ cudaError_t launch_wq(const DevGeom& g, const KRun& R, bool trace, bool states, 
                       cudaStream_t stream, int* grid_out); \
 cudaError_t dp_init(const DevGeom& g, void* objs, void* tab, cudaStream_t stream); \
 size_t dp_object_bytes(); \
+cudaError_t bank_compact(const DevGeom& g, const double* bank, const uint8_t* bank_n, uint64_t n, double* sites, \
+                         unsigned long long* M_host, cudaStream_t stream); \
+cudaError_t source_from_sites(const double* sites, unsigned long long M, uint64_t seed, uint32_t cycle, \
+                              uint64_t j_begin, uint64_t n_next, double* states, cudaStream_t stream); \
 cudaError_t fission_source(const DevGeom& g, const double* bank, const uint8_t* bank_n, uint64_t n_prev, \
                            uint64_t seed, uint32_t cycle, uint64_t n_next, double* states, \
                            unsigned long long* M_host, cudaStream_t stream); \

@@ -730,25 +730,62 @@ __global__ void __launch_bounds__(kScanB) k_bank_prefix(const uint8_t* bn, uint6
   if (i < n) prefix[i] = offs[blockIdx.x] + sh[w] + (x - v);
 }
 
-__global__ void k_fission_source(const DevGeom g, const double* bank, const uint8_t* bn,
-                                 const unsigned long long* prefix, uint64_t n_prev, unsigned long long M,
-                                 uint64_t seed, uint32_t cycle, uint64_t n_next, double* st) {
+// flat (history, site)-ordered site list: sites[(prefix[i] + k) * 3 + a]
+__global__ void k_bank_compact(const double* bank, const uint8_t* bn, const unsigned long long* prefix, uint64_t n,
+                               int ms, double* sites) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const int c = bn[i];
+    for (int k = 0; k < c; ++k)
+      for (int a = 0; a < 3; ++a) sites[(prefix[i] + k) * 3 + a] = bank[(i * ms + k) * 3 + a];
+  }
+}
+
+// source particle J = j_begin + j: site floor(u_J * M) of the flat list, isotropic direction
+__global__ void k_source_from_sites(const double* sites, unsigned long long M, uint64_t seed, uint32_t cycle,
+                                    uint64_t j_begin, uint64_t n_next, double* st) {
   for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n_next; j += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t J = j_begin + j;
     double u, unused, xmu, xphi, ox, oy, oz;
-    draw2(seed, j, cycle, 0xF155u, u, unused);
+    draw2(seed, J, cycle, 0xF155u, u, unused);
     const unsigned long long t = static_cast<unsigned long long>(floor(u * static_cast<double>(M)));
-    uint64_t lo = 0, hi = n_prev;                     // last h with prefix[h] <= t
-    while (hi - lo > 1) {
-      const uint64_t mid = (lo + hi) >> 1;
-      if (prefix[mid] <= t) lo = mid; else hi = mid;
-    }
-    const double* p = bank + (lo * static_cast<uint64_t>(g.max_sites) + (t - prefix[lo])) * 3;
-    draw2(seed, j, cycle, 0xF156u, xmu, xphi);
+    const double* p = sites + t * 3;
+    draw2(seed, J, cycle, 0xF156u, xmu, xphi);
     isotropic(xmu, xphi, ox, oy, oz);
     st[j] = p[0]; st[n_next + j] = p[1]; st[2 * n_next + j] = p[2];
     st[3 * n_next + j] = ox; st[4 * n_next + j] = oy; st[5 * n_next + j] = oz;
-    (void)bn;
   }
+}
+
+static unsigned grid_for(uint64_t n) {
+  uint64_t grid = (n + 255) / 256;
+  if (grid > 148 * 16) grid = 148 * 16;
+  return (unsigned)(grid ? grid : 1);
+}
+
+cudaError_t bank_compact(const DevGeom& g, const double* bank, const uint8_t* bank_n, uint64_t n, double* sites,
+                         unsigned long long* M_host, cudaStream_t stream) {
+  *M_host = 0;
+  if (n == 0) return cudaSuccess;
+  const uint64_t nb = (n + kScanB - 1) / kScanB;
+  unsigned long long* scratch = nullptr;             // sums[nb] | total | prefix[n]
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (nb + 1 + n) * sizeof(unsigned long long), stream);
+  if (e != cudaSuccess) return e;
+  unsigned long long *sums = scratch, *total = scratch + nb, *prefix = scratch + nb + 1;
+  k_bank_block_sums<<<(unsigned)nb, kScanB, 0, stream>>>(bank_n, n, sums);
+  k_bank_scan_sums<<<1, 32, 0, stream>>>(sums, nb, total);
+  k_bank_prefix<<<(unsigned)nb, kScanB, 0, stream>>>(bank_n, n, sums, prefix);
+  k_bank_compact<<<grid_for(n), 256, 0, stream>>>(bank, bank_n, prefix, n, g.max_sites, sites);
+  e = cudaMemcpyAsync(M_host, total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
+  const cudaError_t e2 = cudaFreeAsync(scratch, stream);
+  return e != cudaSuccess ? e : e2;
+}
+
+cudaError_t source_from_sites(const double* sites, unsigned long long M, uint64_t seed, uint32_t cycle,
+                              uint64_t j_begin, uint64_t n_next, double* states, cudaStream_t stream) {
+  if (M == 0 || n_next == 0) return cudaSuccess;
+  k_source_from_sites<<<grid_for(n_next), 256, 0, stream>>>(sites, M, seed, cycle, j_begin, n_next, states);
+  return cudaGetLastError();
 }
 
 cudaError_t fission_source(const DevGeom& g, const double* bank, const uint8_t* bank_n, uint64_t n_prev,
@@ -756,24 +793,12 @@ cudaError_t fission_source(const DevGeom& g, const double* bank, const uint8_t* 
                            unsigned long long* M_host, cudaStream_t stream) {
   *M_host = 0;
   if (n_prev == 0) return cudaSuccess;
-  const uint64_t nb = (n_prev + kScanB - 1) / kScanB;
-  unsigned long long* scratch = nullptr;             // sums[nb] | total | prefix[n_prev]
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (nb + 1 + n_prev) * sizeof(unsigned long long), stream);
+  double* sites = nullptr;
+  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sites), n_prev * (uint64_t)g.max_sites * 3 * sizeof(double), stream);
   if (e != cudaSuccess) return e;
-  unsigned long long *sums = scratch, *total = scratch + nb, *prefix = scratch + nb + 1;
-  k_bank_block_sums<<<(unsigned)nb, kScanB, 0, stream>>>(bank_n, n_prev, sums);
-  k_bank_scan_sums<<<1, 32, 0, stream>>>(sums, nb, total);
-  k_bank_prefix<<<(unsigned)nb, kScanB, 0, stream>>>(bank_n, n_prev, sums, prefix);
-  e = cudaMemcpyAsync(M_host, total, sizeof(unsigned long long), cudaMemcpyDeviceToHost, stream);
-  if (e == cudaSuccess) e = cudaStreamSynchronize(stream);
-  if (e == cudaSuccess && *M_host > 0 && n_next > 0) {
-    uint64_t grid = (n_next + 255) / 256;
-    if (grid > 148 * 16) grid = 148 * 16;
-    k_fission_source<<<(unsigned)grid, 256, 0, stream>>>(g, bank, bank_n, prefix, n_prev, *M_host, seed, cycle,
-                                                          n_next, states);
-    e = cudaGetLastError();
-  }
-  const cudaError_t e2 = cudaFreeAsync(scratch, stream);
+  e = bank_compact(g, bank, bank_n, n_prev, sites, M_host, stream);
+  if (e == cudaSuccess) e = source_from_sites(sites, *M_host, seed, cycle, 0, n_next, states, stream);
+  const cudaError_t e2 = cudaFreeAsync(sites, stream);
   return e != cudaSuccess ? e : e2;
 }
 

@@ -67,3 +67,39 @@ def test_shard_function():
             shards = [nt.shard(N, g, G) for g in range(G)]
             assert sum(k for _, k in shards) == N
             assert all(shards[g][0] + shards[g][1] == (shards[g + 1][0] if g + 1 < G else N) for g in range(G))
+
+
+def _pi_worker(rank, world, port, n, cycles, outdir):
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import oracle
+    import paper_2406_13849_b200 as nt
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    om = oracle.OracleModel.from_spec(workloads.infinite_medium(1.0, 0.25, 0.55))
+
+    def track(nn, pid0, states, cycle):
+        res = om.run(nn, seed=21, pid_begin=pid0, bank=True, threads=1,
+                     states=None if states is None else states.numpy())
+        sites = om.bank_sites(res["bank"], res["bank_n"])
+        return torch.from_numpy(sites.copy()), len(sites)
+
+    def sample(sites, M, cycle, j0, nn):
+        return torch.from_numpy(om.source_from_sites(sites.numpy(), 21, cycle, j0, nn).copy())
+
+    ks = nt.power_iteration_distributed(None, n, cycles, seed=21, track_fn=track, sample_fn=sample)
+    np.save(os.path.join(outdir, f"ks_{rank}.npy"), np.array(ks))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_power_iteration_allgather(tmp_path, oracle_mod):
+    """Multi-rank power iteration (F1): the all-gathered fission bank makes 2 ranks x n histories
+    reproduce one process tracking 2n histories, cycle by cycle (k exact)."""
+    port = _free_port()
+    n, cycles = 300, 3
+    mp.spawn(_pi_worker, args=(2, port, n, cycles, str(tmp_path)), nprocs=2, join=True)
+    k0, k1 = np.load(tmp_path / "ks_0.npy"), np.load(tmp_path / "ks_1.npy")
+    assert np.array_equal(k0, k1)
+    om = oracle_mod.OracleModel.from_spec(workloads.infinite_medium(1.0, 0.25, 0.55))
+    ref = om.power_iteration(2 * n, cycles, seed=21)
+    assert np.array_equal(k0, np.array(ref))

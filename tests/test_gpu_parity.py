@@ -465,3 +465,13 @@ def test_fast_division_sqrt_are_ieee(nt):
     """The kernels' slow-path-free division / sqrt return the IEEE results bit for bit on 2^26
     random operands spanning (and exceeding) the walk's ranges."""
     assert nt.selftest_arith(1 << 26, 3) == (0, 0)
+
+
+def test_power_iteration_distributed_single_rank(nt, orc):
+    """The multi-GPU driver's device path (nt_bank_compact + nt_source_from_sites) at one rank
+    equals the single-GPU power iteration and the oracle's, cycle by cycle."""
+    spec = FISSILE["c1"]()
+    m = nt.Model.from_spec(spec, device=0)
+    om = orc.OracleModel.from_spec(spec)
+    ks = nt.power_iteration_distributed(m, 1000, 3, seed=8)
+    assert ks == m.power_iteration(1000, cycles=3, seed=8) == om.power_iteration(1000, cycles=3, seed=8)
