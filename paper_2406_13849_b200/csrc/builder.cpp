@@ -704,6 +704,35 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
     }
     for (int a = 0; a < 3; ++a) F.cell_tr.push_back(c.tr[a]);
   }
+  // Across-surface neighbours, a search shortcut for CSG crossings (Alg. 8): for half-space entry h
+  // of cell c (surface s, sense t), the cells of c's universe that hold s with the other sense.
+  // Lists longer than kNbMax stay empty (the BIH search is used); the containing cell is unique,
+  // so testing these first changes nothing but the search time.
+  {
+    constexpr int kNbMax = 4;
+    F.hs_nb_off.assign(1, 0);
+    F.nb_cells.clear();
+    std::map<std::pair<int, int>, std::vector<int>> by_side;    // (surface, sense) -> cells, per universe
+    std::vector<int> uni_of(C.size(), -1);
+    for (int u = 0; u < (int)U.size(); ++u)
+      if (U[u].kind == U_CSG) for (int c : U[u].cells) uni_of[c] = u;
+    std::vector<std::map<std::pair<int, int>, std::vector<int>>> side(U.size());
+    for (int i = 0; i < (int)C.size(); ++i)
+      if (uni_of[i] >= 0)
+        for (size_t k = 0; k < C[i].sid.size(); ++k) side[uni_of[i]][{C[i].sid[k], C[i].sense[k]}].push_back(i);
+    for (int i = 0; i < (int)C.size(); ++i) {
+      for (int h = F.cell_hs[i]; h < F.cell_hs[i + 1]; ++h) {
+        const int e = F.hs[h], s = e >> 4, t = e & 1;
+        if (uni_of[i] >= 0) {
+          auto it = side[uni_of[i]].find({s, t ^ 1});
+          if (it != side[uni_of[i]].end() && (int)it->second.size() <= kNbMax)
+            for (int c2 : it->second) F.nb_cells.push_back(c2);
+        }
+        F.hs_nb_off.push_back((int32_t)F.nb_cells.size());
+      }
+    }
+    if (F.nb_cells.empty()) F.nb_cells.push_back(0);
+  }
   // cell AABBs by truncation of the universe box, padded
   std::vector<Aabb> cb(C.size(), Aabb::empty());
   for (int u = 0; u < (int)U.size(); ++u)

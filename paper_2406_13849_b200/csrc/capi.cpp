@@ -297,7 +297,8 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
                o_leaf = place(blob, F.bih_leaf), o_fills = place(blob, F.fills), o_st = place(blob, F.mc_st),
                o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell), o_nut = place(blob, F.mc_nut),
                o_edges = place(blob, F.edges), o_uinst = place(blob, F.univ_inst),
-               o_ioff = place(blob, F.inst_off), o_cpos = place(blob, F.cell_pos);
+               o_ioff = place(blob, F.inst_off), o_cpos = place(blob, F.cell_pos),
+               o_nboff = place(blob, F.hs_nb_off), o_nbc = place(blob, F.nb_cells);
   const size_t o_pou = place(blob, F.r_pin_of_univ), o_poff = place(blob, F.r_pin_off),
                o_psid = place(blob, F.r_pin_sid), o_pmc = place(blob, F.r_pin_mc);
   m->blob_bytes = blob.size();
@@ -339,6 +340,8 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     g.univ_inst = (const int32_t*)(b + o_uinst);
     g.inst_off = (const int32_t*)(b + o_ioff);
     g.cell_pos = (const int32_t*)(b + o_cpos);
+    g.hs_nb_off = (const int32_t*)(b + o_nboff);
+    g.nb_cells = (const int32_t*)(b + o_nbc);
     m->rg = F.rg;
     m->rg.pin_of_univ = (const int32_t*)(b + o_pou);
     m->rg.pin_off = (const int32_t*)(b + o_poff);

@@ -213,6 +213,22 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
           if (pos >= 0) Q(wr, qq)[pos] = static_cast<QIdx>(slot);
         }
       };
+      // ASYNC: append every lane's slot to its target ring in one pass (lanes grouped by target
+      // with match.any; one tail atomic per target; -1 = no target)
+      auto push_all = [&](int qq) {
+        if (!__any_sync(0xffffffffu, qq >= 0)) return;
+        const unsigned grp = __match_any_sync(0xffffffffu, qq);
+        const int leader = __ffs(grp) - 1;
+        uint32_t base2 = 0;
+        if (qq >= 0 && lane == leader) base2 = atomicAdd(a_tail + qq, static_cast<uint32_t>(__popc(grp)));
+        base2 = __shfl_sync(0xffffffffu, base2, leader);
+        if (qq >= 0) {
+          __threadfence_block();                                   // slot state before the entry
+          uint32_t* e = ring + qq * B + ((base2 + __popc(grp & ((1u << lane) - 1u))) & (B - 1));
+          while (vload(e) != 0u) {}                                // previous lap consumed
+          vstore(e, static_cast<uint32_t>(slot) + 1u);
+        }
+      };
       // ---------------- EVENT: change_direction / descent / birth of this chunk's slots
         // births: claim pids for this warp's birth lanes (warp-aggregated)
         const unsigned bm = __ballot_sync(0xffffffffu, kind == 2);
@@ -346,7 +362,8 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
           if (!ok) finalize(slot, NT_T_LOST);
         }
       const bool ready = kind == 5 || (done && ok) || scat;
-      push(Q_F, (done && !ok) || absorbed);
+      const bool ended_at_event = (done && !ok) || absorbed;
+      if (!ASYNC) push(Q_F, ended_at_event);
       // ---------------- MOVE the same slots (no barrier between a slot's event and its move)
       {
         // outcome: 0 none, 1 reflect (-> M), 2 collide, 3 CSG descent, 4 array descent, 5 ended
@@ -447,15 +464,19 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
           if (outc == 5) finalize(slot, term);
         }
         // per-event counters (one shared atomic per warp and counter)
-        warp_count(outc == 1, s_cnt + C_REFL, lane);
-        warp_count(outc == 2, s_cnt + C_COLL, lane);
+        warp_count(outc == 1, s_cnt + C_REFL, lane);   // collisions = segments - crossings - reflections (flush)
         if (lcross >= 0) atomicAdd(s_cnt + C_CBL0 + lcross, 1u);   // crossings = leaks + sum over levels (flush)
         // enqueue for the next event
-        push(Q_M, outc == 1);
-        push(Q_C, outc == 2);
-        push(Q_DC, outc == 3);
-        push(Q_DA, outc == 4);
-        push(Q_F, outc == 5);
+        if constexpr (ASYNC) {
+          push_all(ended_at_event || outc == 5 ? Q_F : outc == 1 ? Q_M : outc == 2 ? Q_C : outc == 3 ? Q_DC
+                   : outc == 4 ? Q_DA : -1);
+        } else {
+          push(Q_M, outc == 1);
+          push(Q_C, outc == 2);
+          push(Q_DC, outc == 3);
+          push(Q_DA, outc == 4);
+          push(Q_F, outc == 5);
+        }
       }
       if (ASYNC) base -= B;                       // ASYNC: keep claiming until the block is done
     }
@@ -471,6 +492,7 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
     unsigned int c = s_cnt[C_LEAK];
     for (int lv = 0; lv < kMaxDepth; ++lv) c += s_cnt[C_CBL0 + lv];
     s_cnt[C_CROSS] = c;
+    s_cnt[C_COLL] = s_cnt[C_SEG] - c - s_cnt[C_REFL];  // every segment ends in one of the three
   }
   __syncthreads();
   flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);

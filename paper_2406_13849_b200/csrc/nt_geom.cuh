@@ -209,10 +209,18 @@ struct Best {
   __device__ __forceinline__ int l() const { return key & 15; }
   __device__ __forceinline__ int sense() const { return (key >> 4) & 1; }
   __device__ __forceinline__ int j() const { return key >> 5; }
+  // p ? a : b as one predicated select (keeps the candidate loop branch-free)
+  static __device__ __forceinline__ double selp(double a, double b, bool p) {
+    double r;
+    asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+        : "=d"(r) : "d"(a), "d"(b), "r"(static_cast<unsigned>(p)));
+    return r;
+  }
   __device__ __forceinline__ void consider(double dd, int ll, int jj, int ss) {
-    const bool lt = dd < d;                       // branch-free select form
-    d2 = lt ? d : (dd < d2 ? dd : d2);
-    d = lt ? dd : d;
+    const bool lt = dd < d;                       // min / second-min, branch-free
+    const double hi = selp(d, dd, lt);            // the larger of (d, dd)
+    d = selp(dd, d, lt);
+    d2 = selp(hi, d2, hi < d2);
     key = lt ? (ll | (ss << 4) | (jj << 5)) : key;
   }
 };

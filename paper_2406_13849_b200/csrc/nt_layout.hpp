@@ -89,6 +89,8 @@ struct DevGeom {
   const int32_t* univ_inst;   // per-instance tallies (D1): per universe, base into inst_off
   const int32_t* inst_off;    //   instances before child k of the universe
   const int32_t* cell_pos;    //   per cell: its position in its universe
+  const int32_t* hs_nb_off;   // per half-space entry: [off, off+1) into nb_cells (CSG crossing shortcut)
+  const int32_t* nb_cells;
   int32_t root, n_mc, max_depth, n_univ;
   int32_t n_cells, n_surf, root_kind, features;   // features: F_* bits present in the model
   const void* const* trk;     // DP dispatch only: per-universe tracker object pointers (dp_tracker.cuh)

@@ -61,6 +61,7 @@ struct Flat {
   std::vector<double> edges;        // non-uniform rect edges (N1)
   // per-instance tallies (D1): instance = sum over levels of inst_off[univ_inst[u] + child]
   std::vector<int32_t> univ_inst, inst_off, cell_pos, inst_mc;
+  std::vector<int32_t> hs_nb_off, nb_cells;   // across-surface neighbours per half-space entry
   int64_t n_inst = 0;               // 0: not available (pseudo-array builds)
   std::vector<int32_t> bih_depth;   // per universe (CSG), host info
   int root = -1, max_depth = 0, n_mc = 0, features = 0;

@@ -89,7 +89,23 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
     double tx, ty, tz;
     int dau;
     if (kind == U_CSG) {
-      const int cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags);
+      int cell = -1;
+      if (l == l0 && fsid >= 0) {
+        // crossing: first the cells across the crossed half-space of the cell just left
+        const int prev = st.a(l0);
+        const int h0 = ld(g.cell_hs + prev), h1 = ld(g.cell_hs + prev + 1);
+        int h = h0;
+        while (h < h1 && hs_sid(ld(g.hs + h)) != fsid) ++h;
+        if (h < h1) {
+          const int k1 = ld(g.hs_nb_off + h + 1);
+          for (int k = ld(g.hs_nb_off + h); k < k1; ++k) {
+            const int c = ld(g.nb_cells + k);
+            uint32_t nb = 0;
+            if (cell_contains(g, c, x, y, z, fsid, fsense, nb)) { cell = c; flags |= nb; break; }
+          }
+        }
+      }
+      if (cell < 0) cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags);
       if (cell < 0) return false;
       st.a(l) = cell;
       const int f = ld(g.cell_fill + cell);

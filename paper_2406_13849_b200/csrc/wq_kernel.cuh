@@ -355,7 +355,6 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
         if (outc == 5) finalize(slot, term);
       }
       warp_count(outc == 1, s_cnt + C_REFL, lane);
-      warp_count(outc == 2, s_cnt + C_COLL, lane);
       if (lcross >= 0) atomicAdd(s_cnt + C_CBL0 + lcross, 1u);   // crossings = leaks + sum over levels (flush)
       mM &= ~warp_or64(valid, slot);
       mM |= warp_or64(outc == 1, slot);
@@ -403,6 +402,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
     unsigned int c = s_cnt[C_LEAK];
     for (int lv = 0; lv < kMaxDepth; ++lv) c += s_cnt[C_CBL0 + lv];
     s_cnt[C_CROSS] = c;
+    s_cnt[C_COLL] = s_cnt[C_SEG] - c - s_cnt[C_REFL];  // every segment ends in one of the three
   }
   __syncthreads();
   flush_tallies(R, gl, s_exit, s_cnt, nmc, tid, B);
