@@ -500,8 +500,9 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   if (run->max_segments > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": max_segments >= 2^32");
   const int block = run->block_dim > 0 ? run->block_dim : 256;
   if (block % 32 || block > 256) return err(NT_E_ARG, std::string(who) + ": block_dim must be a multiple of 32, <= 256");
-  if (run->tracker == NT_TRACKER_GENERIC && !(run->flags & (NT_WARPQ | NT_HISTORY)) && block != 128 && block != 256)
-    return err(NT_E_ARG, std::string(who) + ": the event scheduler needs block_dim 128 or 256");
+  if (run->tracker == NT_TRACKER_GENERIC && !(run->flags & (NT_WARPQ | NT_HISTORY)) && block != 128 && block != 256 &&
+      !(block == 192 && !(run->flags & (NT_ROUNDS | NT_DP))))
+    return err(NT_E_ARG, std::string(who) + ": the event scheduler needs block_dim 128 or 256 (192: ring queues, SP only)");
   if (run->n > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": at most 2^32-1 histories per call");
   if (trace && o->mesh && m->mesh_on)
     return err(NT_E_UNSUPPORTED, std::string(who) + ": the mesh tally cannot be combined with NT_TRACE");
@@ -511,7 +512,7 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   const bool dp = (run->flags & NT_DP) != 0;
   // block queues: ring queues without rounds (default, block 256) or rounds + barrier (NT_ROUNDS,
   // also every block_dim 128 run)
-  const bool async = !(run->flags & NT_ROUNDS) && block == 256;
+  const bool async = !(run->flags & NT_ROUNDS) && (block == 256 || block == 192);
   if (dp && (run->tracker != NT_TRACKER_GENERIC || (run->flags & (NT_WARPQ | NT_HISTORY)) || block != 256))
     return err(NT_E_ARG, std::string(who) + ": NT_DP needs the generic tracker, block queues and block_dim 256");
   m->last_launches = 0;

@@ -161,9 +161,9 @@ __device__ __forceinline__ bool descend_dp(const DevGeom& g, Stack& st, int l0, 
   for (int l = l0; l < kMaxDepth; ++l) {
     st.u(l) = u;
     if (STORE_T) {
-      st.T(l, 0) = Tx;
-      st.T(l, 1) = Ty;
-      st.T(l, 2) = Tz;
+      st.setT(l, 0, Tx);
+      st.setT(l, 1, Ty);
+      st.setT(l, 2, Tz);
     }
     int ia = 0, ib = 0, ic = 0;
     double tx = 0.0, ty = 0.0, tz = 0.0;

@@ -41,21 +41,27 @@ __device__ __forceinline__ void warp_count(bool pred, unsigned int* counter, int
   if (lane == 0 && m) atomicAdd(counter, (unsigned)__popc(m));
 }
 
+// ring capacity: the power of two >= the slot count (a slot is in at most one ring at a time)
+__host__ __device__ constexpr int ring_size(int B) { return B <= 128 ? 128 : 256; }
+
 size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false) {
   const size_t nmc = g.n_mc, d = g.max_depth;
   size_t s = 0;
-  s += (7 + 3 * d + (trace ? 1 : 0)) * 8 * (size_t)B;                 // doubles
+  s += (7 + 3 * (d - 1) + (trace ? 1 : 0)) * 8 * (size_t)B;           // doubles (T from level 1)
   s += (6 + 4 * d + (trace ? 2 : 0)) * 4 * (size_t)B;                 // ints
   s += (3 + (trace ? 1 : 0)) * (size_t)B;                             // bytes
   s = (s + 15) & ~size_t(15);
-  if (async) s += NQ * sizeof(uint32_t) * (size_t)B;                  // ring queues
+  if (async) s += NQ * sizeof(uint16_t) * (size_t)ring_size(B);        // ring queues
   else s += 3 * NQ * sizeof(QIdx) * (size_t)B;                        // queues (triple-buffered)
   s += (nmc + kNC + 3 * NQ + 4) * 4;                                    // exits, counters, queue counts
   return (s + 15) & ~size_t(15);
 }
 
 __device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpret_cast<const volatile uint32_t*>(p); }
-__device__ __forceinline__ void vstore(uint32_t* p, uint32_t v) { *reinterpret_cast<volatile uint32_t*>(p) = v; }
+__device__ __forceinline__ uint32_t vload(const uint16_t* p) { return *reinterpret_cast<const volatile uint16_t*>(p); }
+__device__ __forceinline__ void vstore(uint16_t* p, uint32_t v) {
+  *reinterpret_cast<volatile uint16_t*>(p) = static_cast<uint16_t>(v);
+}
 
 // DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh).
 // TALLY: bit 0 mesh tally (M1), bit 1 per-instance tally (D1); separate instantiations.
@@ -65,7 +71,7 @@ __device__ __forceinline__ void vstore(uint32_t* p, uint32_t v) { *reinterpret_c
 // event (warp-aggregated atomic on the tail, entry published after a block fence).  The block
 // ends when the pids are exhausted and no history is live.
 template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false>
-__global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRun R) {
+__global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGeom g, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmc = g.n_mc, maxd = g.max_depth;
@@ -73,8 +79,8 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
   double* sx = reinterpret_cast<double*>(smem);
   double* sy = sx + B; double* sz = sy + B; double* su = sz + B; double* sv = su + B; double* sw = sv + B;
   double* stau = sw + B;
-  double* sTb = stau + B;                           // [maxd][3][B]
-  double* sps = sTb + 3 * maxd * B;                 // TRACE: pending segment length
+  double* sTb = stau + B;                           // [maxd-1][3][B] (T_0 = 0)
+  double* sps = sTb + 3 * (maxd - 1) * B;           // TRACE: pending segment length
   uint32_t* sidx = reinterpret_cast<uint32_t*>(sps + (TRACE ? B : 0));
   uint32_t* sepoch = sidx + B; uint32_t* snseg = sepoch + B;
   int32_t* smc = reinterpret_cast<int32_t*>(snseg + B);
@@ -90,8 +96,9 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
   size_t off = (size_t)(reinterpret_cast<unsigned char*>(spl + (TRACE ? B : 0)) - smem);
   off = (off + 15) & ~size_t(15);
   QIdx* sq = reinterpret_cast<QIdx*>(smem + off);            // [3][NQ][B]        (rounds)
-  uint32_t* ring = reinterpret_cast<uint32_t*>(smem + off);  // [NQ][B] slot + 1, 0 = empty (ASYNC)
-  unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NQ * B)
+  constexpr int RB = ring_size(B);
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + off);  // [NQ][RB] slot + 1, 0 = empty (ASYNC)
+  unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NQ * RB)
                                : reinterpret_cast<unsigned int*>(sq + 3 * NQ * B);
   unsigned int* s_cnt = s_exit + nmc;
   int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [3][NQ]
@@ -104,9 +111,9 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
   if (tid < 3 * NQ) s_qn[tid] = 0;
   if (ASYNC) {
-    for (int i = tid; i < NQ * B; i += B) ring[i] = 0u;
+    for (int i = tid; i < NQ * RB; i += B) ring[i] = 0u;
     __syncthreads();
-    for (int i = tid; i < B; i += B) ring[Q_F * B + i] = static_cast<uint32_t>(i) + 1u;   // all slots free
+    for (int i = tid; i < B; i += B) ring[Q_F * RB + i] = static_cast<uint16_t>(i + 1);    // all slots free
     if (tid == 0) { a_tail[Q_F] = B; s_flag[0] = 0; s_flag[1] = 0; }
   } else {
     if (tid == 0) { s_flag[0] = 0; s_qn[0 * NQ + Q_F] = B; }
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
         take = __shfl_sync(0xffffffffu, take, 0);
         valid = static_cast<uint32_t>(lane) < take;
         if (valid) {
-          uint32_t* e = ring + q * B + ((h + lane) & (B - 1));
+          uint16_t* e = ring + q * RB + ((h + lane) & (RB - 1));
           uint32_t v;
           while ((v = vload(e)) == 0u) {}
           vstore(e, 0u);
@@ -203,7 +210,7 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
             base2 = __shfl_sync(0xffffffffu, base2, leader);
             if (pred) {
               __threadfence_block();                               // slot state before the entry
-              uint32_t* e = ring + qq * B + ((base2 + __popc(m & ((1u << lane) - 1u))) & (B - 1));
+              uint16_t* e = ring + qq * RB + ((base2 + __popc(m & ((1u << lane) - 1u))) & (RB - 1));
               while (vload(e) != 0u) {}                            // previous lap consumed
               vstore(e, static_cast<uint32_t>(slot) + 1u);
             }
@@ -224,7 +231,7 @@ __global__ void __launch_bounds__(B, 3) k_track_event(const DevGeom g, const KRu
         base2 = __shfl_sync(0xffffffffu, base2, leader);
         if (qq >= 0) {
           __threadfence_block();                                   // slot state before the entry
-          uint32_t* e = ring + qq * B + ((base2 + __popc(grp & ((1u << lane) - 1u))) & (B - 1));
+          uint16_t* e = ring + qq * RB + ((base2 + __popc(grp & ((1u << lane) - 1u))) & (RB - 1));
           while (vload(e) != 0u) {}                                // previous lap consumed
           vstore(e, static_cast<uint32_t>(slot) + 1u);
         }

@@ -30,15 +30,17 @@ NT_DEV_BEGIN
 
 // per-thread universe stack in shared memory, level-major: [level][field][B] so that one
 // level's fields sit at fixed offsets from one per-level base (conflict-free across a warp)
+// The root frame is the global frame (T_0 = 0 always), so translations are stored from level 1.
 struct Stack {
   int* si;      // [maxd][4][B]: u, a, b, c   (thread-offset already applied)
-  double* sT;   // [maxd][3][B]               (thread-offset already applied)
+  double* sT;   // [maxd-1][3][B]: T of levels 1 .. maxd-1 (thread-offset already applied)
   int B;
   __device__ __forceinline__ int& u(int l) { return si[(4 * l + 0) * B]; }
   __device__ __forceinline__ int& a(int l) { return si[(4 * l + 1) * B]; }
   __device__ __forceinline__ int& b(int l) { return si[(4 * l + 2) * B]; }
   __device__ __forceinline__ int& c(int l) { return si[(4 * l + 3) * B]; }
-  __device__ __forceinline__ double& T(int l, int k) { return sT[(3 * l + k) * B]; }
+  __device__ __forceinline__ double T(int l, int k) const { return l ? sT[(3 * (l - 1) + k) * B] : 0.0; }
+  __device__ __forceinline__ void setT(int l, int k, double v) { if (l) sT[(3 * (l - 1) + k) * B] = v; }
 };
 
 // D1: instance of the material cell at the bottom of the stack (levels 0 .. L-1): the sum over the
@@ -79,9 +81,9 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
   for (int l = l0; l < kMaxDepth; ++l) {
     st.u(l) = u;
     if (STORE_T) {
-      st.T(l, 0) = Tx;
-      st.T(l, 1) = Ty;
-      st.T(l, 2) = Tz;
+      st.setT(l, 0, Tx);
+      st.setT(l, 1, Ty);
+      st.setT(l, 2, Tz);
     }
     const double x = rx - Tx, y = ry - Ty, z = rz - Tz;
     const DUniv* U = g.univ + u;
@@ -229,12 +231,12 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
   const int nmc = g.n_mc;
   double* sT = reinterpret_cast<double*>(smem);
-  unsigned int* s_cnt = reinterpret_cast<unsigned int*>(sT + 3 * g.max_depth * B + 4 * g.max_depth * B / 2);
+  unsigned int* s_cnt = reinterpret_cast<unsigned int*>(sT + 3 * (g.max_depth - 1) * B + 4 * g.max_depth * B / 2);
   unsigned int* s_exit = s_cnt + kNC;
   double* gl = R.slices + (size_t)blockIdx.x * nmc;   // per-block track-length tally (global)
   Stack st;
   st.sT = sT + tid;
-  st.si = reinterpret_cast<int*>(sT + 3 * g.max_depth * B) + tid;
+  st.si = reinterpret_cast<int*>(sT + 3 * (g.max_depth - 1) * B) + tid;
   st.B = B;
   for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
@@ -452,7 +454,7 @@ __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const doubl
   const int B = blockDim.x;
   Stack st;
   st.sT = reinterpret_cast<double*>(smem) + threadIdx.x;
-  st.si = reinterpret_cast<int*>(reinterpret_cast<double*>(smem) + 3 * g.max_depth * B) + threadIdx.x;
+  st.si = reinterpret_cast<int*>(reinterpret_cast<double*>(smem) + 3 * (g.max_depth - 1) * B) + threadIdx.x;
   st.B = B;
   for (uint64_t i = blockIdx.x * (uint64_t)B + threadIdx.x; i < n; i += (uint64_t)gridDim.x * B) {
     int L = 0, mc = 0;
@@ -465,7 +467,7 @@ __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const doubl
 
 // ---------------------------------------------------------------- host launchers
 size_t generic_smem_bytes(const DevGeom& g, int block) {
-  return (size_t)g.max_depth * block * (3 * 8 + 4 * 4) + (kNC + (size_t)g.n_mc) * 4;
+  return (size_t)block * ((g.max_depth - 1) * 3 * 8 + g.max_depth * 4 * 4) + (kNC + (size_t)g.n_mc) * 4;
 }
 
 // per-launch scratch: per-block track-length slices (stream-ordered allocation, zeroed)
@@ -596,6 +598,11 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
   };
   const int tally = (R.mesh ? 1 : 0) | (R.inst ? 2 : 0);
   if (tally && trace) return cudaErrorNotSupported;
+  if (async && block == 192) {     // ring queues, 6 warps per block (more blocks per SM)
+    if (g.trk || tally) return cudaErrorNotSupported;
+    if (trace) return states ? go(k_track_event<192, true, true, false, 0, true>) : go(k_track_event<192, true, false, false, 0, true>);
+    return states ? go(k_track_event<192, false, true, false, 0, true>) : go(k_track_event<192, false, false, false, 0, true>);
+  }
   if (async) {                     // barrier-free ring queues (block 256), SP or DP dispatch
     if (block != 256) return cudaErrorInvalidValue;
     auto pick = [&](auto dp) -> cudaError_t {
@@ -836,7 +843,7 @@ cudaError_t selftest_arith(uint64_t n, uint64_t seed, unsigned long long* d_bad)
 cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, int32_t* cell,
                               uint8_t* flag, cudaStream_t stream) {
   const int block = 256;
-  const size_t smem = (size_t)g.max_depth * block * (3 * 8 + 4 * 4);
+  const size_t smem = (size_t)block * ((g.max_depth - 1) * 3 * 8 + g.max_depth * 4 * 4);
   cudaError_t e = cudaFuncSetAttribute(k_find_cells, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   uint64_t grid = (n + block - 1) / block;

@@ -78,6 +78,13 @@ def test_config_trace_parity(nt, orc, cfg, sched):
     assert g["counters"]["lost"] == 0 and g["counters"]["capped"] == 0
 
 
+@pytest.mark.parametrize("cfg", ["c3", "c4", "c5m"])
+def test_config_trace_parity_block192(nt, orc, cfg):
+    """Ring-queue scheduler with 192-slot blocks (6 warps, more blocks per SM): traces bit-exact."""
+    spec, _ = workloads.config(cfg)
+    _compare(nt, orc, spec, CONFIG_N[cfg], seed=1, block_dim=192)
+
+
 @pytest.mark.parametrize("seed", workloads.PARITY_SEEDS)
 def test_c3_parity_seeds(nt, orc, seed):
     spec, _ = workloads.config("c3")
@@ -283,7 +290,7 @@ def test_dp_dispatch_rejects_other_schedulers(nt):
     assert m.L.nt_track(m.h, nt.C.byref(run), nt.C.byref(o), None) == -1
 
 
-@pytest.mark.parametrize("block", [128, 256])
+@pytest.mark.parametrize("block", [128, 192, 256])
 @pytest.mark.parametrize("n", [1, 31, 257, 1000])
 def test_ragged_batches_and_large_pids(nt, orc, n, block):
     """Ragged batch sizes (partial warps / blocks) and pids above 2^32 (counter hi word)."""
