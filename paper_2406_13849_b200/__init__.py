@@ -170,6 +170,10 @@ class Model:
         _check(self.L.nt_add_material(self.h, sigma_t, sigma_a, C.byref(i)))
         return i.value
 
+    def set_fission(self, mat: int, nu_sigma_f: float):
+        """One-group nu Sigma_f of material `mat` (reading F1; validated at finalize)."""
+        _check(self.L.nt_set_fission(self.h, mat, nu_sigma_f))
+
     def add_csg_universe(self) -> int:
         i = C.c_int32()
         _check(self.L.nt_add_csg_universe(self.h, C.byref(i)))
@@ -250,7 +254,7 @@ class Model:
         for mt in spec["materials"]:
             k = m.add_material(mt["sigma_t"], mt["sigma_a"])
             if mt.get("nu_sigma_f", 0.0):
-                _check(m.L.nt_set_fission(m.h, k, mt["nu_sigma_f"]))
+                m.set_fission(k, mt["nu_sigma_f"])
         for u in spec["universes"]:
             if u["kind"] == "csg":
                 uid = m.add_csg_universe()
