@@ -289,10 +289,13 @@ def main():
             return ss / tt, ss
         rg, sg = timed(kw)
         rr, sr = timed(dict(kw, tracker="rect", scheduler="history"))
+        rh, sh = timed(dict(kw, scheduler="history"))
         ratio = {"generic_over_rect": rg / rr, "generic_segments_per_s": rg, "rect_segments_per_s": rr,
-                 "segments_equal": sg == sr, "generic_scheduler": kw["scheduler"],
+                 "segments_equal": sg == sr == sh, "generic_scheduler": kw["scheduler"],
+                 "generic_history_over_rect": rh / rr, "generic_history_segments_per_s": rh,
                  "note": "this rank, identical seeds/pids, no all-reduce; rect = Alg. 9-10 specialised "
-                         "tracker (history scheduler); target >= 0.85 (north star)"}
+                         "tracker, history-based; generic_history_over_rect compares the two trackers "
+                         "under the same (history) scheduling; target >= 0.85 (north star)"}
 
     e2e = None
     if not a.no_e2e and mbuf is not None:
