@@ -740,7 +740,14 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
       for (int c : U[u].cells) {
         Aabb a = ubox[u].valid() ? polytope_box(S, C[c], truncate(S, C[c], ubox[u]))
                                  : Aabb{{-kBig, -kBig, -kBig}, {kBig, kBig, kBig}};
-        if (!a.valid()) a = ubox[u].valid() ? ubox[u] : Aabb{{0, 0, 0}, {0, 0, 0}};
+        if (!a.valid()) {
+          // the cell does not meet the universe box (e.g. pseudo-array tiles beyond it): no point
+          // the walk can reach lies in it.  Give it its own box outside, so that the BIH keeps it
+          // away from every query (a universe-sized box would put it in every search).
+          const Aabb big{{-kBig, -kBig, -kBig}, {kBig, kBig, kBig}};
+          a = polytope_box(S, C[c], truncate(S, C[c], big));
+          if (!a.valid()) a = ubox[u].valid() ? ubox[u] : Aabb{{0, 0, 0}, {0, 0, 0}};
+        }
         cb[c] = pad(a);
       }
   if (!opts.pseudo) build_instance_tables(C, U, root, F);

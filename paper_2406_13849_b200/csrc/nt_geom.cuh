@@ -132,7 +132,14 @@ struct BihStack {
 };
 
 #ifdef NT_BIH_STATS
-__device__ unsigned long long g_bih_stats[4];   // calls, node visits, cell tests, root-leaf calls
+// calls, node visits, cell tests, -, max cells / call, max nodes / call, [6..15] log2 histogram of cells / call
+__device__ unsigned long long g_bih_stats[16];
+__device__ __forceinline__ void bih_stats_done(unsigned cells, unsigned nodes) {
+  atomicMax(&g_bih_stats[4], (unsigned long long)cells);
+  atomicMax(&g_bih_stats[5], (unsigned long long)nodes);
+  const int b = cells ? min(9, 32 - __clz(cells)) : 0;
+  atomicAdd(&g_bih_stats[6 + b], 1ull);
+}
 #endif
 __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, double y, double z,
                                         int fsid, int fsense, uint32_t& flags) {
@@ -141,6 +148,12 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
 #endif
   BihStack stk;
   int node = 0;                                          // relative to root
+#ifdef NT_BIH_STATS
+  unsigned st_cells = 0, st_nodes = 0;
+#define NT_BIH_RET(v) do { bih_stats_done(st_cells, st_nodes); return (v); } while (0)
+#else
+#define NT_BIH_RET(v) return (v)
+#endif
   for (;;) {
     int meta, a;
     for (;;) {                                           // internal nodes down to a leaf
@@ -149,6 +162,7 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
       a = ld(&n->a);
 #ifdef NT_BIH_STATS
       atomicAdd(&g_bih_stats[1], 1ull);
+      ++st_nodes;
 #endif
       if (meta < 0) break;
       const double c = sel3(meta, x, y, z);
@@ -159,7 +173,7 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
       else if (gr) node = left + 1;
       else {
         node = stk.pop();
-        if (node < 0) return -1;
+        if (node < 0) NT_BIH_RET(-1);
       }
     }
     const int cnt = -meta - 1;                           // leaf: test its cells
@@ -168,15 +182,17 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
       uint32_t nb = 0;
 #ifdef NT_BIH_STATS
       atomicAdd(&g_bih_stats[2], 1ull);
+      ++st_cells;
 #endif
       if (cell_contains(g, cell, x, y, z, fsid, fsense, nb)) {
         flags |= nb;
-        return cell;
+        NT_BIH_RET(cell);
       }
     }
     node = stk.pop();
-    if (node < 0) return -1;
+    if (node < 0) NT_BIH_RET(-1);
   }
+#undef NT_BIH_RET
 }
 
 // forward wall of a rect tile along one axis (O11 RECT walls): (e(i+1) - x)/u or (e(i) - x)/u

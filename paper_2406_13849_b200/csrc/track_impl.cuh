@@ -827,8 +827,8 @@ cudaError_t fission_source(const DevGeom& g, const double* bank, const uint8_t* 
 
 cudaError_t bih_stats(unsigned long long* host4, bool reset) {
 #ifdef NT_BIH_STATS
-  if (reset) { unsigned long long z[4] = {0, 0, 0, 0}; return cudaMemcpyToSymbol(g_bih_stats, z, sizeof z); }
-  return cudaMemcpyFromSymbol(host4, g_bih_stats, 4 * sizeof(unsigned long long));
+  if (reset) { unsigned long long z[16] = {}; return cudaMemcpyToSymbol(g_bih_stats, z, sizeof z); }
+  return cudaMemcpyFromSymbol(host4, g_bih_stats, 16 * sizeof(unsigned long long));
 #else
   (void)host4; (void)reset;
   return cudaErrorNotSupported;
