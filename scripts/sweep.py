@@ -33,8 +33,9 @@ for cfg in a.configs.split(","):
     n = int(min(n_cfg, a.max_particles))
     if cfg == "c1":
         n = max(n, 1_000_000)          # C1's 1e4 histories take < 1 ms; time a larger batch
-    variants = [("generic", "block", False), ("generic", "warp", False), ("generic", "history", False),
-                ("generic", "block", True), ("rect", "history", False)]
+    variants = [("generic", "block", False), ("generic", "rounds", False), ("generic", "warp", False),
+                ("generic", "history", False), ("generic", "dp", False), ("generic", "block", True),
+                ("rect", "history", False)]
     for tracker, sched, pseudo in variants:
         m = nt.Model.from_spec(spec, device=0, pseudo_array=pseudo)
         if tracker == "rect" and not m.info["rect_specialisable"]:
