@@ -203,6 +203,22 @@ def test_instance_tally_parity(nt, orc, cfg, sched):
     assert np.all(np.abs(gi - ref) <= 1e-9 * np.abs(ref) + 1e-12 * ref.max())
 
 
+@pytest.mark.parametrize("name", ["nonuniform_slabs", "gap_lattice", "hex_pins_small_flat", "rect3d_small"])
+def test_instance_tally_test_models(nt, orc, name):
+    """Instance numbering through non-uniform rect, 3-D rect and hex arrays (with outer tiles)."""
+    M = workloads.models
+    spec = {"nonuniform_slabs": M.nonuniform_slabs, "gap_lattice": lambda: M.gap_lattice(True),
+            "hex_pins_small_flat": lambda: M.hex_pins_small("flat"), "rect3d_small": M.rect3d_small}[name]()
+    m = nt.Model.from_spec(spec, device=0)
+    om = orc.OracleModel.from_spec(spec)
+    assert np.array_equal(m.instance_cells(), om.instance_cells())
+    res = m.track(500, seed=13, instances=True)
+    torch.cuda.synchronize()
+    o = om.run(500, seed=13, instances=True)
+    gi, ref = res["inst"].cpu().numpy()[:om.n_instances()], o["inst"]
+    assert np.all(np.abs(gi - ref) <= 1e-9 * np.abs(ref) + 1e-12 * ref.max())
+
+
 def test_mesh_and_instance_tallies_together(nt, orc):
     """Both extra tallies in one run (separate kernel instantiation) on the full-core model."""
     spec = MESHED["c3"]()
