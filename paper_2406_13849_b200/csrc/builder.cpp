@@ -145,7 +145,7 @@ Aabb truncate(const std::vector<HSurf>& S, const HCell& c, const Aabb& start) {
 // universe): the box of the polytope {truncated box} ∩ {plane half-spaces}, from its vertices.
 // Quadrics are only used through truncate(), so the result still contains the cell.  Falls
 // back to the truncated box when the enumeration finds nothing (empty or degenerate cell).
-Aabb polytope_box(const std::vector<HSurf>& S, const HCell& c, const Aabb& b) {
+Aabb polytope_box(const std::vector<HSurf>& S, const HCell& c, const Aabb& b, bool empty_if_none = false) {
   struct H { double n[3], d; };             // n.x <= d
   std::vector<H> hs;
   bool general = false;
@@ -190,7 +190,7 @@ Aabb polytope_box(const std::vector<HSurf>& S, const HCell& c, const Aabb& b) {
         }
         if (in) r.grow(Aabb{{p[0], p[1], p[2]}, {p[0], p[1], p[2]}});
       }
-  if (!r.valid()) return b;
+  if (!r.valid()) return empty_if_none ? Aabb::empty() : b;
   for (int a = 0; a < 3; ++a) {          // never looser than the truncated box
     r.lo[a] = std::max(r.lo[a], b.lo[a]);
     r.hi[a] = std::min(r.hi[a], b.hi[a]);
@@ -738,7 +738,9 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
   for (int u = 0; u < (int)U.size(); ++u)
     if (U[u].kind == U_CSG)
       for (int c : U[u].cells) {
-        Aabb a = ubox[u].valid() ? polytope_box(S, C[c], truncate(S, C[c], ubox[u]))
+        // empty_if_none: a plane-bounded cell whose polytope misses the universe box is detected
+        // here and gets its own (natural) box below, which always contains the cell
+        Aabb a = ubox[u].valid() ? polytope_box(S, C[c], truncate(S, C[c], ubox[u]), true)
                                  : Aabb{{-kBig, -kBig, -kBig}, {kBig, kBig, kBig}};
         if (!a.valid()) {
           // the cell does not meet the universe box (e.g. pseudo-array tiles beyond it): no point

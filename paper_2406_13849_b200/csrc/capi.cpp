@@ -654,6 +654,30 @@ extern "C" nt_status nt_debug_bih_stats(int32_t fset, uint64_t* out4, int32_t re
   return NT_OK;
 }
 
+// debug: the BIH nodes of CSG universe uid (lmax, rmin, meta, a per node, relative to the root node)
+extern "C" nt_status nt_debug_bih_nodes(const nt_model* m, int32_t uid, double* lmax, double* rmin, int32_t* meta,
+                                        int32_t* a, int32_t cap, int32_t* n_nodes) {
+  if (!m || !m->finalized || uid < 0 || uid >= (int)m->F.univ.size() || m->F.univ[uid].kind != U_CSG)
+    return err(NT_E_ARG, "nt_debug_bih_nodes: bad model / universe");
+  const int root = m->F.univ[uid].i0;
+  int n = 0;
+  std::vector<int> todo{root};
+  int hi = root;
+  while (!todo.empty()) {                      // nodes of this universe: contiguous from root
+    const int k = todo.back();
+    todo.pop_back();
+    hi = std::max(hi, k);
+    if (m->F.bih[k].meta >= 0) { todo.push_back(m->F.bih[k].a); todo.push_back(m->F.bih[k].a + 1); }
+  }
+  for (int k = root; k <= hi; ++k, ++n)
+    if (n < cap) {
+      const BihNode& b = m->F.bih[k];
+      lmax[n] = b.lmax; rmin[n] = b.rmin; meta[n] = b.meta; a[n] = b.meta >= 0 ? b.a - root : b.a;
+    }
+  *n_nodes = n;
+  return NT_OK;
+}
+
 nt_status nt_selftest_arith(uint64_t n, uint64_t seed, uint64_t* mismatches) {
   if (!mismatches) return err(NT_E_ARG, "nt_selftest_arith: mismatches is NULL");
   unsigned long long* d = nullptr;
