@@ -688,7 +688,14 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
     std::vector<int> o(c.sid.size());
     std::iota(o.begin(), o.end(), 0);
     std::sort(o.begin(), o.end(), [&](int a, int b) { return c.sid[a] < c.sid[b]; });
-    for (int k : o) F.hs.push_back(hs_pack(c.sid[k], S[c.sid[k]].kind, c.sense[k]));
+    for (int k : o) {
+      F.hs.push_back(hs_pack(c.sid[k], S[c.sid[k]].kind, c.sense[k]));
+      DHs r{};
+      for (int q = 0; q < 4; ++q) r.c[q] = F.surf[c.sid[k]].c[q];
+      r.e = F.hs.back();
+      r.tol = F.surf_tol[c.sid[k]];
+      F.hsr.push_back(r);
+    }
     F.cell_hs.push_back((int32_t)F.hs.size());
     if (c.fill_kind == 0) {
       F.cell_fill.push_back(F.n_mc++);
@@ -818,6 +825,7 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
   if (F.inst_off.empty()) F.inst_off.push_back(0);
   if (F.cell_pos.empty()) F.cell_pos.push_back(0);
   if (F.hs.empty()) F.hs.push_back(0);
+  if (F.hsr.empty()) F.hsr.push_back(DHs{});
   if (F.mc_st.empty()) fail("model has no material cells");
 }
 

@@ -298,7 +298,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
                o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell), o_nut = place(blob, F.mc_nut),
                o_edges = place(blob, F.edges), o_uinst = place(blob, F.univ_inst),
                o_ioff = place(blob, F.inst_off), o_cpos = place(blob, F.cell_pos),
-               o_nboff = place(blob, F.hs_nb_off), o_nbc = place(blob, F.nb_cells);
+               o_nboff = place(blob, F.hs_nb_off), o_nbc = place(blob, F.nb_cells), o_hsr = place(blob, F.hsr);
   const size_t o_pou = place(blob, F.r_pin_of_univ), o_poff = place(blob, F.r_pin_off),
                o_psid = place(blob, F.r_pin_sid), o_pmc = place(blob, F.r_pin_mc);
   m->blob_bytes = blob.size();
@@ -325,6 +325,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     g.surf_tol = (const double*)(b + o_tol);
     g.surf_meta = (const uint8_t*)(b + o_meta);
     g.hs = (const int32_t*)(b + o_hs);
+    g.hsr = (const DHs*)(b + o_hsr);
     g.cell_hs = (const int32_t*)(b + o_chs);
     g.cell_fill = (const int32_t*)(b + o_cf);
     g.cell_tr = (const double*)(b + o_ctr);

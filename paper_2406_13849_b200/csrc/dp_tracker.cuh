@@ -56,7 +56,7 @@ struct CsgTracker final : UnivTracker {
     for (int h = h0; h < h1; ++h) {
       const int e = ld(g.hs + h);
       const int sid = hs_sid(e);
-      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, g.surf + sid, x, y, z, u, v, w);
+      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, g.surf[sid].c, x, y, z, u, v, w);
       b.consider(d, l, sid, hs_sense(e));
     }
   }
@@ -159,7 +159,7 @@ __device__ __forceinline__ bool descend_dp(const DevGeom& g, Stack& st, int l0, 
                                            int& L, int& mc, uint32_t& flags) {
 #pragma unroll 1
   for (int l = l0; l < kMaxDepth; ++l) {
-    st.u(l) = u;
+    st.set_u(l, u, ld(&g.univ[u].kind));
     if (STORE_T) {
       st.setT(l, 0, Tx);
       st.setT(l, 1, Ty);

@@ -256,6 +256,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           }
         }
         bool ok = false, done = false, scat = false, absorbed = false;
+        int iso_ep = -2;      // >= 0: isotropic direction from (epoch iso_ep, block 1) and tau; -1: tau only
+        double xtau = 0.0;
         if (kind == 4) {
           // ---- change_direction (O14, O15)
           const uint64_t pid = R.pid0 + sidx[slot];
@@ -271,11 +273,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             if (TRACE) emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_ABSORBED, sflags[slot]);
             finalize(slot, NT_T_ABSORBED);
           } else {
-            double xmu, xphi, u, v, w;
-            draw2(R.seed, pid, epoch, 1, xmu, xphi);
-            isotropic(xmu, xphi, u, v, w);
-            su[slot] = u; sv[slot] = v; sw[slot] = w;
-            stau[slot] = -spec_log(xb);
+            iso_ep = static_cast<int>(epoch);      // direction and tau: shared tail below
+            xtau = xb;
             scat = true;
             if (TRACE) emit<TRACE>(R, pid, snseg[slot] - 1, NT_EV_COLLIDE, -1, -1, cb, cb, sps[slot], NT_T_NONE, sflags[slot]);
           }
@@ -291,26 +290,23 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           double Tx = 0.0, Ty = 0.0, Tz = 0.0;
           if (born) {
             const uint64_t pid = R.pid0 + sidx[slot];
-            double xa, xb;
-            draw2(R.seed, pid, 0, 0, xa, xb);
-            double u, v, w;
+            double xa;
+            draw2(R.seed, pid, 0, 0, xa, xtau);
             if (STATES) {
               const uint64_t id = sidx[slot];
               rx = R.states[id]; ry = R.states[R.n + id]; rz = R.states[2 * R.n + id];
-              u = R.states[3 * R.n + id]; v = R.states[4 * R.n + id]; w = R.states[5 * R.n + id];
+              su[slot] = R.states[3 * R.n + id]; sv[slot] = R.states[4 * R.n + id]; sw[slot] = R.states[5 * R.n + id];
+              iso_ep = -1;                         // tau only
             } else {
-              double xmu, xphi, xx, xy, xz, unused;
-              draw2(R.seed, pid, 0, 1, xmu, xphi);
+              double xx, xy, xz, unused;
               draw2(R.seed, pid, 0, 2, xx, xy);
               draw2(R.seed, pid, 0, 3, xz, unused);
               rx = R.lo[0] + R.w[0] * xx;
               ry = R.lo[1] + R.w[1] * xy;
               rz = R.lo[2] + R.w[2] * xz;
-              isotropic(xmu, xphi, u, v, w);
+              iso_ep = 0;                          // epoch-0 direction (block 1) in the shared tail
             }
             sx[slot] = rx; sy[slot] = ry; sz[slot] = rz;
-            su[slot] = u; sv[slot] = v; sw[slot] = w;
-            stau[slot] = -spec_log(xb);
             sepoch[slot] = 0; snseg[slot] = 0; sos[slot] = -1; sosl[slot] = -1;
             if (TRACE) spl[slot] = -2;
           } else {
@@ -331,7 +327,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
                 du = get_tracker(g, st.u(l0))->next_tile(g, j, ta, tb, tc, tx, ty, tz);
               } else {
                 const DUniv* U = g.univ + st.u(l0);
-                const int uk = ld(&U->kind);
+                const int uk = st.ukind(l0);
                 if (!kHex || uk == U_RECT) {
                   const int dir = (j & 1) ? 1 : -1, ax = j >> 1;
                   if (ax == 0) ta += dir; else if (ax == 1) tb += dir; else tc += dir;
@@ -368,6 +364,16 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           }
           if (!ok) finalize(slot, NT_T_LOST);
         }
+      // one direction / tau site for births and scatters (O15, O12): keeps the kernel's code small
+      if (iso_ep > -2) {
+        if (iso_ep >= 0) {
+          double xmu, xphi, u, v, w;
+          draw2(R.seed, R.pid0 + sidx[slot], static_cast<uint32_t>(iso_ep), 1, xmu, xphi);
+          isotropic(xmu, xphi, u, v, w);
+          su[slot] = u; sv[slot] = v; sw[slot] = w;
+        }
+        stau[slot] = -spec_log(xtau);
+      }
       const bool ready = kind == 5 || (done && ok) || scat;
       const bool ended_at_event = (done && !ok) || absorbed;
       if (!ASYNC) push(Q_F, ended_at_event);
@@ -443,7 +449,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
                 } else {
                   atomicAdd(s_exit + mc, 1u);
                   lcross = l;
-                  const int uk = ld(&g.univ[st.u(l)].kind);
+                  const int uk = st.ukind(l);
                   if (uk == U_CSG) {
                     sdesc[slot] = l | ((b.sense() ^ 1) << 4) | ((j + 1) << 5);
                     os_l = l; os_s = j;

@@ -21,16 +21,23 @@ constexpr bool kRectNU = (NT_FEAT & F_RECTNU) != 0;
 template <class T>
 __device__ __forceinline__ T ld(const T* p) { return __ldg(p); }
 
-__device__ __forceinline__ double clamp0(double d) { return d > 0.0 ? d : 0.0; }
+// d > 0 ? d : 0 as one compare and one select (nvcc otherwise emits a NaN-propagating max sequence;
+// the result is the same for every input, NaN -> 0 included)
+__device__ __forceinline__ double clamp0(double d) {
+  double r;
+  asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, 0d0000000000000000;\n\tselp.f64 %0, %1, 0d0000000000000000, p;\n\t}"
+      : "=d"(r) : "d"(d));
+  return r;
+}
 
 __device__ __forceinline__ double sel3(int a, double x, double y, double z) {
   return a == 0 ? x : (a == 1 ? y : z);
 }
 
 // f(r) of a surface (O3), evaluation order exactly as documented
-__device__ __forceinline__ double surf_f(int kind, const DSurf* sp, double x, double y, double z) {
-  if (kind <= S_PZ) return sel3(kind, x, y, z) - ld(&sp->c[0]);
-  const double c0 = ld(&sp->c[0]), c1 = ld(&sp->c[1]), c2 = ld(&sp->c[2]), c3 = ld(&sp->c[3]);
+__device__ __forceinline__ double surf_f(int kind, const double* sp, double x, double y, double z) {
+  if (kind <= S_PZ) return sel3(kind, x, y, z) - ld(&sp[0]);
+  const double c0 = ld(&sp[0]), c1 = ld(&sp[1]), c2 = ld(&sp[2]), c3 = ld(&sp[3]);
   if (kPlane && kind == S_PLANE) return ((c0 * x + c1 * y) + c2 * z) - c3;
   const double dx = x - c0, dy = y - c1;
   if (!kSphere || kind == S_CZ) return (dx * dx + dy * dy) - c2;
@@ -42,16 +49,16 @@ __device__ __forceinline__ double surf_f(int kind, const DSurf* sp, double x, do
 // os: particle logically on this surface (quadric c := 0).  Returns +inf when no exit.
 // Written with ONE division and ONE square root per call (selected operands) to keep the
 // code small; the selected operands are exactly those of the case formulas in DESIGN.md O11.
-__device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const DSurf* sp, double x,
+__device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const double* sp, double x,
                                             double y, double z, double u, double v, double w) {
   double num, den;
   bool ok;
   if (kind <= S_PZ) {
     den = sel3(kind, u, v, w);
     ok = sense ? den < 0.0 : den > 0.0;                      // also excludes den == 0
-    num = ld(&sp->c[0]) - sel3(kind, x, y, z);
+    num = ld(&sp[0]) - sel3(kind, x, y, z);
   } else {
-    const double c0 = ld(&sp->c[0]), c1 = ld(&sp->c[1]), c2 = ld(&sp->c[2]), c3 = ld(&sp->c[3]);
+    const double c0 = ld(&sp[0]), c1 = ld(&sp[1]), c2 = ld(&sp[2]), c3 = ld(&sp[3]);
     if (kPlane && kind == S_PLANE) {
       den = (c0 * u + c1 * v) + c2 * w;
       ok = sense ? den < 0.0 : den > 0.0;
@@ -71,7 +78,7 @@ __device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const 
         c = os ? 0.0 : ((dx * dx + dy * dy) + dz * dz) - c3;
         q = k * k - c;
       }
-      const double sq = fsqrt(q > 0.0 ? q : 0.0);                 // q < 0: max(q,0) inside, miss outside
+      const double sq = fsqrt(clamp0(q));                 // q < 0: max(q,0) inside, miss outside
       if (!sense) {             // inside (negative side): far root
         ok = a != 0.0;
         if (k <= 0.0) { num = -k + sq; den = a; } else { num = -c; den = k + sq; }
@@ -92,15 +99,16 @@ __device__ __forceinline__ bool cell_contains(const DevGeom& g, int cell, double
   const int h0 = ld(g.cell_hs + cell), h1 = ld(g.cell_hs + cell + 1);
   uint32_t nb = 0;
   for (int h = h0; h < h1; ++h) {
-    const int e = ld(g.hs + h);
+    const DHs* r = g.hsr + h;
+    const int e = ld(&r->e);
     const int sid = hs_sid(e);
     int s;
     if (sid == fsid) {
       s = fsense;
     } else {
-      const double f = surf_f(hs_kind(e), g.surf + sid, x, y, z);
+      const double f = surf_f(hs_kind(e), r->c, x, y, z);
       s = f >= 0.0;
-      if (fabs(f) <= ld(g.surf_tol + sid)) nb = 1u;
+      if (fabs(f) <= ld(&r->tol)) nb = 1u;
     }
     if (s != hs_sense(e)) return false;
   }
@@ -141,13 +149,19 @@ __device__ __forceinline__ void bih_stats_done(unsigned cells, unsigned nodes) {
   atomicAdd(&g_bih_stats[6 + b], 1ull);
 }
 #endif
+// `first` / `nfirst`: an optional list of cells tested before the search (the crossing shortcut's
+// neighbours across the crossed half-space).  It is run as a leaf whose continuation is the root, so
+// the kernel holds one copy of the containment test.
 __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, double y, double z,
-                                        int fsid, int fsense, uint32_t& flags) {
+                                        int fsid, int fsense, uint32_t& flags, const int32_t* first = nullptr,
+                                        int nfirst = 0) {
 #ifdef NT_BIH_STATS
   atomicAdd(&g_bih_stats[0], 1ull);
 #endif
   BihStack stk;
   int node = 0;                                          // relative to root
+  bool pre = nfirst > 0;
+  if (pre) stk.push(1u);                                 // after the list: the root (stored +1)
 #ifdef NT_BIH_STATS
   unsigned st_cells = 0, st_nodes = 0;
 #define NT_BIH_RET(v) do { bih_stats_done(st_cells, st_nodes); return (v); } while (0)
@@ -155,8 +169,9 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
 #define NT_BIH_RET(v) return (v)
 #endif
   for (;;) {
-    int meta, a;
-    for (;;) {                                           // internal nodes down to a leaf
+    int meta = 0, a = 0;
+    const int32_t* leaf = first;
+    for (; !pre;) {                                      // internal nodes down to a leaf
       const BihNode* n = g.bih + root + node;
       meta = ld(&n->meta);
       a = ld(&n->a);
@@ -176,9 +191,11 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
         if (node < 0) NT_BIH_RET(-1);
       }
     }
-    const int cnt = -meta - 1;                           // leaf: test its cells
+    int cnt = nfirst;
+    if (!pre) { leaf = g.bih_leaf + a; cnt = -meta - 1; }   // leaf: test its cells
+    pre = false;
     for (int q = 0; q < cnt; ++q) {
-      const int cell = ld(g.bih_leaf + a + q);
+      const int cell = ld(leaf + q);
       uint32_t nb = 0;
 #ifdef NT_BIH_STATS
       atomicAdd(&g_bih_stats[2], 1ull);

@@ -41,6 +41,11 @@ enum UnivKind : int { U_CSG = 0, U_RECT = 1, U_HEX = 2 };
 // CZ: x0, y0, R*R (c3 unused).  SPHERE: x0, y0, z0, R*R.
 struct alignas(16) DSurf { double c[4]; };
 
+// Half-space record (48 bytes): the cell's packed entry with its surface's coefficients and O16
+// tolerance copied in, so that a distance or containment test loads everything from one index
+// (no dependent hs -> surface load).  hsr[h] mirrors hs[h].
+struct alignas(16) DHs { double c[4]; int32_t e, pad; double tol; };
+
 // Half-space entry of a cell: (sid << 4) | (kind << 1) | sense  (sense 1 = positive side).
 NT_HD int hs_sid(int h) { return h >> 4; }
 NT_HD int hs_kind(int h) { return (h >> 1) & 7; }
@@ -74,6 +79,7 @@ struct DevGeom {
   const double* surf_tol;     // O16 proximity tolerance per surface
   const uint8_t* surf_meta;   // per surface: kind | (nt_bc << 4)
   const int32_t* hs;          // packed half-spaces, per cell sorted by surface id (O13)
+  const DHs* hsr;             // per half-space entry: packed entry + surface coefficients + tolerance
   const int32_t* cell_hs;     // [n_cells+1] CSR offsets into hs
   const int32_t* cell_fill;   // >= 0: material-cell index (tally bin); < 0: -1 - daughter uid
   const double* cell_tr;      // [3*n_cells] fill translation

@@ -51,6 +51,7 @@ struct Flat {
   std::vector<double> surf_tol;
   std::vector<uint8_t> surf_meta;
   std::vector<int32_t> hs, cell_hs, cell_fill;
+  std::vector<DHs> hsr;             // hs[h] with its surface's coefficients and tolerance
   std::vector<double> cell_tr;
   std::vector<DUniv> univ;
   std::vector<BihNode> bih;

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
             if (sid == fsid) {
               s = fsense;
             } else {
-              const double f = surf_f(k >> 1, g.surf + sid, rx, ry, rz);
+              const double f = surf_f(k >> 1, g.surf[sid].c, rx, ry, rz);
               s = f >= 0.0;
               if (fabs(f) <= ld(g.surf_tol + sid)) nb = 1u;
             }
@@ -97,12 +97,12 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
           {
             const int sid = rg.zsid[0];
             if (sid == fsid) szl = fsense;
-            else { const double f = surf_f(S_PZ, g.surf + sid, rx, ry, rz); szl = f >= 0.0; if (fabs(f) <= ld(g.surf_tol + sid)) nb = 1u; }
+            else { const double f = surf_f(S_PZ, g.surf[sid].c, rx, ry, rz); szl = f >= 0.0; if (fabs(f) <= ld(g.surf_tol + sid)) nb = 1u; }
           }
           {
             const int sid = rg.zsid[1];
             if (sid == fsid) szh = fsense;
-            else { const double f = surf_f(S_PZ, g.surf + sid, rx, ry, rz); szh = f >= 0.0; if (fabs(f) <= ld(g.surf_tol + sid)) nb = 1u; }
+            else { const double f = surf_f(S_PZ, g.surf[sid].c, rx, ry, rz); szh = f >= 0.0; if (fabs(f) <= ld(g.surf_tol + sid)) nb = 1u; }
           }
           ok = szl == 1 && szh == 0;
           // annulus: first k with (k == 0 or inner sense POS) and outer sense NEG
@@ -113,7 +113,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
             int s;
             uint32_t nbk = 0;
             if (sid == fsid) s = fsense;
-            else { const double f = surf_f(S_CZ, g.surf + sid, rx, ry, rz); s = f >= 0.0; nbk = fabs(f) <= ld(g.surf_tol + sid); }
+            else { const double f = surf_f(S_CZ, g.surf[sid].c, rx, ry, rz); s = f >= 0.0; nbk = fabs(f) <= ld(g.surf_tol + sid); }
             if (prev_pos && s == 0) { found = k; nb_in = nb_prev | nbk; }
             prev_pos = s;
             nb_prev = nbk;
@@ -169,7 +169,7 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
           int s;
           uint32_t nbk = 0;
           if (sid == fsid) s = fsense;
-          else { const double f = surf_f(S_CZ, g.surf + sid, x, y, z); s = f >= 0.0; nbk = fabs(f) <= ld(g.surf_tol + sid); }
+          else { const double f = surf_f(S_CZ, g.surf[sid].c, x, y, z); s = f >= 0.0; nbk = fabs(f) <= ld(g.surf_tol + sid); }
           if (prev_pos && s == 0) { a = k; nb_in = nb_prev | nbk; break; }
           prev_pos = s;
           nb_prev = nbk;
@@ -204,28 +204,28 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
 #pragma unroll
           for (int k = 0; k < 6; ++k) {
             const int sid = rg.box_sid[k];
-            const double d = surf_dist(k >> 1, (k & 1) ? 0 : 1, false, g.surf + sid, rx, ry, rz, u, v, w);
+            const double d = surf_dist(k >> 1, (k & 1) ? 0 : 1, false, g.surf[sid].c, rx, ry, rz, u, v, w);
             b.consider(d, 0, sid, (k & 1) ? 0 : 1);
           }
         } else {
           {
             const int sid = rg.zsid[0];
-            const double d = surf_dist(S_PZ, 1, false, g.surf + sid, rx, ry, rz, u, v, w);
+            const double d = surf_dist(S_PZ, 1, false, g.surf[sid].c, rx, ry, rz, u, v, w);
             b.consider(d, 0, sid, 1);
           }
           {
             const int sid = rg.zsid[1];
-            const double d = surf_dist(S_PZ, 0, false, g.surf + sid, rx, ry, rz, u, v, w);
+            const double d = surf_dist(S_PZ, 0, false, g.surf[sid].c, rx, ry, rz, u, v, w);
             b.consider(d, 0, sid, 0);
           }
           if (ann > 0) {
             const int sid = rg.root_sid[ann - 1];
-            const double d = surf_dist(S_CZ, 1, os_l == 0 && os_s == sid, g.surf + sid, rx, ry, rz, u, v, w);
+            const double d = surf_dist(S_CZ, 1, os_l == 0 && os_s == sid, g.surf[sid].c, rx, ry, rz, u, v, w);
             b.consider(d, 0, sid, 1);
           }
           {
             const int sid = rg.root_sid[ann];
-            const double d = surf_dist(S_CZ, 0, os_l == 0 && os_s == sid, g.surf + sid, rx, ry, rz, u, v, w);
+            const double d = surf_dist(S_CZ, 0, os_l == 0 && os_s == sid, g.surf[sid].c, rx, ry, rz, u, v, w);
             b.consider(d, 0, sid, 0);
           }
         }
@@ -246,12 +246,12 @@ __global__ void __launch_bounds__(256) k_track_rect(const DevGeom g, const RectG
           const double x = rx - Tx[K], y = ry - Ty[K], z = rz - Tz[K];
           if (pa > 0) {
             const int sid = ld(rg.pin_sid + off + pa - 1);
-            const double d = surf_dist(S_CZ, 1, os_l == KP && os_s == sid, g.surf + sid, x, y, z, u, v, w);
+            const double d = surf_dist(S_CZ, 1, os_l == KP && os_s == sid, g.surf[sid].c, x, y, z, u, v, w);
             b.consider(d, KP, sid, 1);
           }
           if (pa < ncz) {
             const int sid = ld(rg.pin_sid + off + pa);
-            const double d = surf_dist(S_CZ, 0, os_l == KP && os_s == sid, g.surf + sid, x, y, z, u, v, w);
+            const double d = surf_dist(S_CZ, 0, os_l == KP && os_s == sid, g.surf[sid].c, x, y, z, u, v, w);
             b.consider(d, KP, sid, 0);
           }
         }

@@ -32,10 +32,13 @@ NT_DEV_BEGIN
 // level's fields sit at fixed offsets from one per-level base (conflict-free across a warp)
 // The root frame is the global frame (T_0 = 0 always), so translations are stored from level 1.
 struct Stack {
-  int* si;      // [maxd][4][B]: u, a, b, c   (thread-offset already applied)
+  int* si;      // [maxd][4][B]: u | kind << 28, a, b, c   (thread-offset already applied)
   double* sT;   // [maxd-1][3][B]: T of levels 1 .. maxd-1 (thread-offset already applied)
   int B;
-  __device__ __forceinline__ int& u(int l) { return si[(4 * l + 0) * B]; }
+  // the universe's kind travels with its id, so distance and crossing code need no universe load
+  __device__ __forceinline__ int u(int l) const { return si[(4 * l + 0) * B] & 0x0FFFFFFF; }
+  __device__ __forceinline__ int ukind(int l) const { return static_cast<int>(static_cast<unsigned>(si[(4 * l + 0) * B]) >> 28); }
+  __device__ __forceinline__ void set_u(int l, int u, int kind) { si[(4 * l + 0) * B] = u | (kind << 28); }
   __device__ __forceinline__ int& a(int l) { return si[(4 * l + 1) * B]; }
   __device__ __forceinline__ int& b(int l) { return si[(4 * l + 2) * B]; }
   __device__ __forceinline__ int& c(int l) { return si[(4 * l + 3) * B]; }
@@ -51,7 +54,7 @@ __device__ __forceinline__ int instance_of(const DevGeom& g, Stack& st, int L) {
   for (int l = 0; l < L; ++l) {
     const int u = st.u(l);
     const DUniv* U = g.univ + u;
-    const int kind = ld(&U->kind);
+    const int kind = st.ukind(l);
     int k;
     if (kind == U_CSG) {
       k = ld(g.cell_pos + st.a(l));
@@ -79,19 +82,20 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
                                      int& L, int& mc, uint32_t& flags) {
 #pragma unroll 1
   for (int l = l0; l < kMaxDepth; ++l) {
-    st.u(l) = u;
+    const DUniv* U = g.univ + u;
+    const int kind = ld(&U->kind);
+    st.set_u(l, u, kind);
     if (STORE_T) {
       st.setT(l, 0, Tx);
       st.setT(l, 1, Ty);
       st.setT(l, 2, Tz);
     }
     const double x = rx - Tx, y = ry - Ty, z = rz - Tz;
-    const DUniv* U = g.univ + u;
-    const int kind = ld(&U->kind);
     double tx, ty, tz;
     int dau;
     if (kind == U_CSG) {
-      int cell = -1;
+      const int32_t* nbl = nullptr;
+      int nnb = 0;
       if (l == l0 && fsid >= 0) {
         // crossing: first the cells across the crossed half-space of the cell just left
         const int prev = st.a(l0);
@@ -99,15 +103,12 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
         int h = h0;
         while (h < h1 && hs_sid(ld(g.hs + h)) != fsid) ++h;
         if (h < h1) {
-          const int k1 = ld(g.hs_nb_off + h + 1);
-          for (int k = ld(g.hs_nb_off + h); k < k1; ++k) {
-            const int c = ld(g.nb_cells + k);
-            uint32_t nb = 0;
-            if (cell_contains(g, c, x, y, z, fsid, fsense, nb)) { cell = c; flags |= nb; break; }
-          }
+          const int k0 = ld(g.hs_nb_off + h);
+          nbl = g.nb_cells + k0;
+          nnb = ld(g.hs_nb_off + h + 1) - k0;
         }
       }
-      if (cell < 0) cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags);
+      const int cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags, nbl, nnb);
       if (cell < 0) return false;
       st.a(l) = cell;
       const int f = ld(g.cell_fill + cell);
@@ -150,10 +151,10 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
     const int h0 = ld(g.cell_hs + cell), h1 = ld(g.cell_hs + cell + 1);
 #pragma unroll 1
     for (int h = h0; h < h1; ++h) {
-      const int e = ld(g.hs + h);
+      const DHs* r = g.hsr + h;
+      const int e = ld(&r->e);
       const int sid = hs_sid(e);
-      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, g.surf + sid, x, y, z, u,
-                                 v, w);
+      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, r->c, x, y, z, u, v, w);
       b.consider(d, l, sid, hs_sense(e));        // +inf (no hit) is a no-op
     }
   } else if (!kHex || kind == U_RECT) {
@@ -182,8 +183,7 @@ __device__ __forceinline__ void level_distances(const DevGeom& g, Stack& st, int
                                                 double rz, double u, double v, double w, int os_l,
                                                 int os_s, Best& b) {
   const double x = rx - st.T(l, 0), y = ry - st.T(l, 1), z = rz - st.T(l, 2);
-  const DUniv* U = g.univ + st.u(l);
-  level_candidates(g, U, ld(&U->kind), st.a(l), st.b(l), st.c(l), l, x, y, z, u, v, w, os_l, os_s, b);
+  level_candidates(g, g.univ + st.u(l), st.ukind(l), st.a(l), st.b(l), st.c(l), l, x, y, z, u, v, w, os_l, os_s, b);
 }
 
 // translation from the frame of level l to the frame of level l+1 (same arithmetic as descend)
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
             atomicAdd(s_cnt + C_CBL0 + l, 1u);
             const int ul = st.u(l);
             const DUniv* U = g.univ + ul;
-            const int kind = ld(&U->kind);
+            const int kind = st.ukind(l);
             p_l = l; p_j = j; p_cb = cell_before; p_s = s;
             if (kind == U_CSG) {   // O9': far side of surface j in universe(l)
               d_l0 = l; d_u = ul; d_Tx = st.T(l, 0); d_Ty = st.T(l, 1); d_Tz = st.T(l, 2);
