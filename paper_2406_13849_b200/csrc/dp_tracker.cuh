@@ -54,10 +54,11 @@ struct CsgTracker final : UnivTracker {
                            double v, double w, int os_l, int os_s, Best& b) const override {
     const int h0 = ld(g.cell_hs + ia), h1 = ld(g.cell_hs + ia + 1);
     for (int h = h0; h < h1; ++h) {
-      const int e = ld(g.hs + h);
+      const DHs* r = g.hsr + h;
+      const int e = ld(&r->e);
       const int sid = hs_sid(e);
-      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, g.surf[sid].c, x, y, z, u, v, w);
-      b.consider(d, l, sid, hs_sense(e));
+      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, r->c, x, y, z, u, v, w);
+      b.consider(d, l, h, hs_sense(e));
     }
   }
   __device__ int next_tile(const DevGeom&, int, int&, int&, int&, double&, double&, double&) const override {

@@ -85,7 +85,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
   uint32_t* sepoch = sidx + B; uint32_t* snseg = sepoch + B;
   int32_t* smc = reinterpret_cast<int32_t*>(snseg + B);
   int32_t* sos = smc + B;                           // on-surface sid (-1 none)
-  int32_t* sdesc = sos + B;                         // pending descent: l0 | fsense<<4 | (fsid+1)<<5
+  int32_t* sdesc = sos + B;                         // pending descent: l0 | fsense<<4 | (fh+1)<<5 (CSG: half-space, array: face)
   int32_t* sib = sdesc + B;                         // [maxd][4][B]
   int32_t* spj = sib + 4 * maxd * B;                // TRACE: pending j, cell_before
   int32_t* spcb = spj + (TRACE ? B : 0);
@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           double rx = 0, ry = 0, rz = 0;
           uint32_t flags = 0;
           int L = 0, mc = 0;
-          int l0 = 0, du = g.root, fsid = -1, fsense = 0;
+          int l0 = 0, du = g.root, fh = -1, fsense = 0;
           double Tx = 0.0, Ty = 0.0, Tz = 0.0;
           if (born) {
             const uint64_t pid = R.pid0 + sidx[slot];
@@ -315,12 +315,12 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             const int dsc = sdesc[slot];
             l0 = dsc & 15;
             fsense = (dsc >> 4) & 1;
-            fsid = (dsc >> 5) - 1;
+            fh = (dsc >> 5) - 1;
             if (kind == 0) {
               du = st.u(l0);
               Tx = st.T(l0, 0); Ty = st.T(l0, 1); Tz = st.T(l0, 2);
             } else {                                     // Alg. 6: tile +- 1 at level l0, then daughter
-              const int j = fsid;
+              const int j = fh;
               int ta = st.a(l0), tb = st.b(l0), tc = st.c(l0);
               double tx, ty, tz;
               if constexpr (DP) {
@@ -342,12 +342,13 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
               st.a(l0) = ta; st.b(l0) = tb; st.c(l0) = tc;
               Tx = st.T(l0, 0) + tx; Ty = st.T(l0, 1) + ty; Tz = st.T(l0, 2) + tz;
               l0 = l0 + 1;
-              fsid = -1;
+              fh = -1;
               fsense = 0;
             }
           }
-          if constexpr (DP) ok = du >= 0 && descend_dp(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
-          else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
+          if constexpr (DP) ok = du >= 0 && descend_dp(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh >= 0 ? hs_sid(ld(&g.hsr[fh].e)) : -1,
+                                                       fsense, L, mc, flags);
+          else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh, fsense, L, mc, flags);
           done = true;
           if (!ok) flags |= NT_F3;
           sflags[slot] = static_cast<uint8_t>(flags);
@@ -430,9 +431,11 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
               if (cross) {
                 const double tt = tau - sig * s;
                 tau = tt > 0.0 ? tt : 0.0;
-                const int l = b.l(), j = b.j();
-                const int meta = (l == 0 && g.root_kind == U_CSG) ? ld(g.surf_meta + j) : 0;
-                const int bc = meta >> 4;
+                const int l = b.l(), jb = b.j();
+                const int uk = st.ukind(l);
+                int meta;
+                const int j = winner_surface(g, uk == U_CSG, jb, meta);
+                const int bc = l == 0 ? meta >> 4 : 0;
                 if (bc == NT_BC_VACUUM) {
                   atomicAdd(s_exit + mc, 1u);
                   term = NT_T_LEAKED;
@@ -449,9 +452,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
                 } else {
                   atomicAdd(s_exit + mc, 1u);
                   lcross = l;
-                  const int uk = st.ukind(l);
                   if (uk == U_CSG) {
-                    sdesc[slot] = l | ((b.sense() ^ 1) << 4) | ((j + 1) << 5);
+                    sdesc[slot] = l | ((b.sense() ^ 1) << 4) | ((jb + 1) << 5);
                     os_l = l; os_s = j;
                     outc = 3;
                   } else {

@@ -41,10 +41,12 @@ enum UnivKind : int { U_CSG = 0, U_RECT = 1, U_HEX = 2 };
 // CZ: x0, y0, R*R (c3 unused).  SPHERE: x0, y0, z0, R*R.
 struct alignas(16) DSurf { double c[4]; };
 
-// Half-space record (48 bytes): the cell's packed entry with its surface's coefficients and O16
-// tolerance copied in, so that a distance or containment test loads everything from one index
-// (no dependent hs -> surface load).  hsr[h] mirrors hs[h].
-struct alignas(16) DHs { double c[4]; int32_t e, pad; double tol; };
+// Half-space record (48 bytes): the cell's packed entry with its surface's coefficients, O16
+// tolerance and surf_meta (kind | bc << 4) copied in, so that a distance, containment or crossing
+// step loads everything from one index (no dependent hs -> surface load).  hsr[h] mirrors hs[h].
+// A CSG distance winner is identified by its half-space index h (Best::j), which also names the
+// crossed surface's neighbour list (hs_nb_off[h]) for the descent.
+struct alignas(16) DHs { double c[4]; int32_t e, meta; double tol; };
 
 // Half-space entry of a cell: (sid << 4) | (kind << 1) | sense  (sense 1 = positive side).
 NT_HD int hs_sid(int h) { return h >> 4; }

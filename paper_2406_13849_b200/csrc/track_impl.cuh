@@ -74,12 +74,33 @@ __device__ __forceinline__ int instance_of(const DevGeom& g, Stack& st, int L) {
   return inst;
 }
 
-// Alg. 7 descent from level l0 in universe u with frame translation T; forced sense applies
-// at level l0 only (CSG cross_surface).  Returns false when a level has no cell (LOST).
+// The distance winner's surface: for a CSG level the key holds the half-space index h; its surface
+// id and surf_meta (BC) come from the record.  Array levels: the key is the wall / face number.
+__device__ __forceinline__ int winner_surface(const DevGeom& g, bool csg, int jb, int& meta) {
+  meta = 0;
+  if (!csg) return jb;
+  const DHs* r = g.hsr + jb;
+  meta = ld(&r->meta);
+  return hs_sid(ld(&r->e));
+}
+
+// Alg. 7 descent from level l0 in universe u with frame translation T.  fh >= 0: a CSG crossing
+// out of the cell at level l0 through half-space entry fh; the crossed surface's sense is forced to
+// fsense at level l0 (O9') and the cells across it (hs_nb_off[fh]) are tested first.  Returns false
+// when a level has no cell (LOST).
 template <bool STORE_T = true>
 __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int u, double Tx, double Ty,
-                                     double Tz, double rx, double ry, double rz, int fsid, int fsense,
+                                     double Tz, double rx, double ry, double rz, int fh, int fsense,
                                      int& L, int& mc, uint32_t& flags) {
+  int fsid = -1;
+  const int32_t* nbl = nullptr;
+  int nnb = 0;
+  if (fh >= 0) {
+    fsid = hs_sid(ld(&g.hsr[fh].e));
+    const int k0 = ld(g.hs_nb_off + fh);
+    nbl = g.nb_cells + k0;
+    nnb = ld(g.hs_nb_off + fh + 1) - k0;
+  }
 #pragma unroll 1
   for (int l = l0; l < kMaxDepth; ++l) {
     const DUniv* U = g.univ + u;
@@ -94,21 +115,9 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
     double tx, ty, tz;
     int dau;
     if (kind == U_CSG) {
-      const int32_t* nbl = nullptr;
-      int nnb = 0;
-      if (l == l0 && fsid >= 0) {
-        // crossing: first the cells across the crossed half-space of the cell just left
-        const int prev = st.a(l0);
-        const int h0 = ld(g.cell_hs + prev), h1 = ld(g.cell_hs + prev + 1);
-        int h = h0;
-        while (h < h1 && hs_sid(ld(g.hs + h)) != fsid) ++h;
-        if (h < h1) {
-          const int k0 = ld(g.hs_nb_off + h);
-          nbl = g.nb_cells + k0;
-          nnb = ld(g.hs_nb_off + h + 1) - k0;
-        }
-      }
-      const int cell = csg_find(g, ld(&U->i0), x, y, z, l == l0 ? fsid : -1, fsense, flags, nbl, nnb);
+      const bool first = l == l0;
+      const int cell = csg_find(g, ld(&U->i0), x, y, z, first ? fsid : -1, fsense, flags, first ? nbl : nullptr,
+                                first ? nnb : 0);
       if (cell < 0) return false;
       st.a(l) = cell;
       const int f = ld(g.cell_fill + cell);
@@ -155,7 +164,7 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
       const int e = ld(&r->e);
       const int sid = hs_sid(e);
       const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, r->c, x, y, z, u, v, w);
-      b.consider(d, l, sid, hs_sense(e));        // +inf (no hit) is a no-op
+      b.consider(d, l, h, hs_sense(e));          // +inf (no hit) is a no-op; CSG key = half-space index
     }
   } else if (!kHex || kind == U_RECT) {
     rect_candidates(g, U, ia, ib, ic, l, x, y, z, u, v, w, b);
@@ -250,7 +259,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
   // phase: 0 = needs a history, 1 = needs a descent, 2 = moving
   int phase = 0;
   // pending descent
-  int d_l0 = 0, d_u = 0, d_fsid = -1, d_fsense = 0;
+  int d_l0 = 0, d_u = 0, d_fh = -1, d_fsense = 0;
   double d_Tx = 0, d_Ty = 0, d_Tz = 0;
   // pending crossing record (trace only)
   int p_l = -1, p_j = -1, p_cb = -1;
@@ -288,13 +297,13 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
       }
       tau = -spec_log(xi_tau);
       epoch = 0; flags = 0; nseg = 0; ncross = 0; ncoll = 0; os_l = -1; os_s = -1;
-      d_l0 = 0; d_u = g.root; d_Tx = d_Ty = d_Tz = 0.0; d_fsid = -1; d_fsense = 0;
+      d_l0 = 0; d_u = g.root; d_Tx = d_Ty = d_Tz = 0.0; d_fh = -1; d_fsense = 0;
       p_l = -2;   // no pending crossing record: a failure here is a birth loss
       phase = 1;
     }
     if (phase == 1) {
       // ---- Alg. 7 / Alg. 8 descent (single call site for birth and every crossing)
-      const bool ok = descend(g, st, d_l0, d_u, d_Tx, d_Ty, d_Tz, rx, ry, rz, d_fsid, d_fsense, L, mc, flags);
+      const bool ok = descend(g, st, d_l0, d_u, d_Tx, d_Ty, d_Tz, rx, ry, rz, d_fh, d_fsense, L, mc, flags);
       if (!ok) {
         flags |= NT_F3;
         term = NT_T_LOST;
@@ -337,9 +346,11 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
           const double tt = tau - sig * s;
           tau = tt > 0.0 ? tt : 0.0;
           ++nseg;
-          const int l = b.l(), j = b.j();
-          const int meta = (l == 0 && g.root_kind == U_CSG) ? ld(g.surf_meta + j) : 0;
-          const int bc = meta >> 4;
+          const int l = b.l(), jb = b.j();
+          const int kind_l = st.ukind(l);
+          int meta;
+          const int j = winner_surface(g, kind_l == U_CSG, jb, meta);
+          const int bc = l == 0 ? meta >> 4 : 0;
           if (bc == NT_BC_VACUUM) {
             atomicAdd(s_exit + mc, 1u);
             ++ncross;
@@ -356,11 +367,11 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
             atomicAdd(s_cnt + C_CBL0 + l, 1u);
             const int ul = st.u(l);
             const DUniv* U = g.univ + ul;
-            const int kind = st.ukind(l);
+            const int kind = kind_l;
             p_l = l; p_j = j; p_cb = cell_before; p_s = s;
             if (kind == U_CSG) {   // O9': far side of surface j in universe(l)
               d_l0 = l; d_u = ul; d_Tx = st.T(l, 0); d_Ty = st.T(l, 1); d_Tz = st.T(l, 2);
-              d_fsid = j; d_fsense = b.sense() ^ 1;
+              d_fh = jb; d_fsense = b.sense() ^ 1;
               os_l = l; os_s = j;
               phase = 1;
             } else {               // Alg. 6: tile +- 1, then the new tile's daughter
@@ -385,7 +396,7 @@ __global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KR
               } else {
                 d_l0 = l + 1; d_u = dau;
                 d_Tx = st.T(l, 0) + tx; d_Ty = st.T(l, 1) + ty; d_Tz = st.T(l, 2) + tz;
-                d_fsid = -1; d_fsense = 0;
+                d_fh = -1; d_fsense = 0;
                 phase = 1;
               }
             }

@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
   uint32_t* sepoch = sidx + S; uint32_t* snseg = sepoch + S;
   int32_t* smc = reinterpret_cast<int32_t*>(snseg + S);
   int32_t* sos = smc + S;
-  int32_t* sdesc = sos + S;                             // pending descent: l0 | fsense<<4 | (fsid+1)<<5
+  int32_t* sdesc = sos + S;                             // pending descent: l0 | fsense<<4 | (fh+1)<<5
   int32_t* spj = sdesc + S;                             // TRACE only
   int32_t* spcb = spj + (TRACE ? S : 0);
   int32_t* sib = spcb + (TRACE ? S : 0);                // [maxd][4][S]
@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
         double rx, ry, rz;
         uint32_t flags = 0;
         int L = 0, mc = 0;
-        int l0 = 0, du = g.root, fsid = -1, fsense = 0;
+        int l0 = 0, du = g.root, fh = -1, fsense = 0;
         double Tx = 0.0, Ty = 0.0, Tz = 0.0;
         if (born) {
           const uint64_t pid = R.pid0 + sidx[slot];
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
           const int dsc = sdesc[slot];
           l0 = dsc & 15;
           fsense = (dsc >> 4) & 1;
-          fsid = (dsc >> 5) - 1;
+          fh = (dsc >> 5) - 1;
           // frame of level l0, recomputed top-down with the descent's arithmetic
           for (int l = 0; l < l0; ++l) {
             const DUniv* U = g.univ + st.u(l);
@@ -201,7 +201,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
           }
           du = st.u(l0);
           if (kind == 1) {                                  // Alg. 6: tile +- 1, then the daughter
-            const int j = fsid;
+            const int j = fh;
             const DUniv* U = g.univ + du;
             const int uk = ld(&U->kind);
             int ta = st.a(l0), tb = st.b(l0), tc = st.c(l0);
@@ -219,11 +219,11 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
             du = array_daughter(g, U, uk, ta, tb, tc, tx, ty, tz);
             Tx = Tx + tx; Ty = Ty + ty; Tz = Tz + tz;
             l0 = l0 + 1;
-            fsid = -1;
+            fh = -1;
             fsense = 0;
           }
         }
-        ok = du >= 0 && descend<false>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fsid, fsense, L, mc, flags);
+        ok = du >= 0 && descend<false>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh, fsense, L, mc, flags);
         done = true;
         if (!ok) flags |= NT_F3;
         sflags[slot] = static_cast<uint8_t>(flags);
@@ -309,9 +309,10 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
             if (cross) {
               const double tt = tau - sig * s;
               tau = tt > 0.0 ? tt : 0.0;
-              const int l = b.l(), j = b.j();
-              const int meta = (l == 0 && g.root_kind == U_CSG) ? ld(g.surf_meta + j) : 0;
-              const int bc = meta >> 4;
+              const int l = b.l(), jb = b.j();
+              int meta;
+              const int j = winner_surface(g, kind_l == U_CSG, jb, meta);
+              const int bc = l == 0 ? meta >> 4 : 0;
               if (bc == NT_BC_VACUUM) {
                 atomicAdd(s_exit + mc, 1u);
                 term = NT_T_LEAKED;
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(kWqWarps * 32) k_track_wq(const DevGeom g, con
                 atomicAdd(s_exit + mc, 1u);
                 lcross = l;
                 if (kind_l == U_CSG) {
-                  sdesc[slot] = l | ((b.sense() ^ 1) << 4) | ((j + 1) << 5);
+                  sdesc[slot] = l | ((b.sense() ^ 1) << 4) | ((jb + 1) << 5);
                   os_l = l; os_s = j;
                   outc = 3;
                 } else {
