@@ -156,32 +156,28 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
       bool valid = i < total;
       if constexpr (ASYNC) {
         // ---- claim up to 32 entries of the fullest queue (lane 0), or finish
+        // lane k < NQ reads queue k; the fullest queue (lowest index on ties) wins a warp max-reduction
         int q = -1;
         uint32_t h = 0, take = 0;
-        if (lane == 0) {
-          for (;;) {
-            int best = -1;
-            uint32_t bh = 0, bav = 0;
-            const bool births = vload(reinterpret_cast<uint32_t*>(s_flag)) == 0u;
-#pragma unroll
-            for (int k = 0; k < NQ; ++k) {
-              if (k == Q_F && !births) continue;
-              const uint32_t hk = vload(a_head + k), av = vload(a_tail + k) - hk;
-              if (av > bav) { bav = av; best = k; bh = hk; }
-            }
-            if (best >= 0) {
-              const uint32_t tk = bav < 32u ? bav : 32u;
-              if (atomicCAS(a_head + best, bh, bh + tk) == bh) { q = best; h = bh; take = tk; break; }
-              continue;
-            }
-            if (!births && vload(reinterpret_cast<uint32_t*>(s_flag + 1)) == 0u) break;   // all done
-            __nanosleep(64);
+        for (;;) {
+          const bool births = vload(reinterpret_cast<uint32_t*>(s_flag)) == 0u;
+          uint32_t hk = 0, av = 0;
+          if (lane < NQ && (lane != Q_F || births)) { hk = vload(a_head + lane); av = vload(a_tail + lane) - hk; }
+          const uint32_t mx = __reduce_max_sync(0xffffffffu, (av << 8) | static_cast<uint32_t>(255 - lane));
+          const uint32_t bav = mx >> 8;                  // av <= ring size (256)
+          if (bav > 0u) {
+            const int best = 255 - static_cast<int>(mx & 255u);
+            const uint32_t bh = __shfl_sync(0xffffffffu, hk, best);
+            const uint32_t tk = bav < 32u ? bav : 32u;
+            int won = 0;
+            if (lane == 0) won = atomicCAS(a_head + best, bh, bh + tk) == bh;
+            if (__shfl_sync(0xffffffffu, won, 0)) { q = best; h = bh; take = tk; break; }
+            continue;
           }
+          if (!births && vload(reinterpret_cast<uint32_t*>(s_flag + 1)) == 0u) break;   // all done
+          __nanosleep(64);
         }
-        q = __shfl_sync(0xffffffffu, q, 0);
         if (q < 0) break;
-        h = __shfl_sync(0xffffffffu, h, 0);
-        take = __shfl_sync(0xffffffffu, take, 0);
         valid = static_cast<uint32_t>(lane) < take;
         if (valid) {
           uint16_t* e = ring + q * RB + ((h + lane) & (RB - 1));
@@ -470,7 +466,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             }
           }
           sx[slot] = rx; sy[slot] = ry; sz[slot] = rz;
-          su[slot] = u; sv[slot] = v; sw[slot] = w;
+          if (outc == 1) { su[slot] = u; sv[slot] = v; sw[slot] = w; }   // only a reflection turns the flight
           stau[slot] = tau;
           sflags[slot] = static_cast<uint8_t>(flags);
           snseg[slot] = nseg;
