@@ -289,16 +289,27 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     return err(NT_E_NOMEM, "nt_finalize: out of host memory");
   }
   const Flat& F = m->F;
+  // leaf and neighbour lists as cell references (cell, fill, half-space range)
+  auto cref = [&F](const std::vector<int32_t>& ids) {
+    std::vector<CRef> r(ids.size());
+    for (size_t i = 0; i < ids.size(); ++i) {
+      const int c = ids[i];
+      const bool ok = c >= 0 && c < (int)F.cell_fill.size();
+      r[i] = ok ? CRef{c, F.cell_fill[c], F.cell_hs[c], F.cell_hs[c + 1]} : CRef{c, 0, 0, 0};
+    }
+    return r;
+  };
+  const std::vector<CRef> leaf_refs = cref(F.bih_leaf), nb_refs = cref(F.nb_cells);
   // one contiguous blob of 256-byte aligned arrays
   std::vector<char> blob;
   const size_t o_surf = place(blob, F.surf), o_tol = place(blob, F.surf_tol), o_meta = place(blob, F.surf_meta),
                o_hs = place(blob, F.hs), o_chs = place(blob, F.cell_hs), o_cf = place(blob, F.cell_fill),
                o_ctr = place(blob, F.cell_tr), o_univ = place(blob, F.univ), o_bih = place(blob, F.bih),
-               o_leaf = place(blob, F.bih_leaf), o_fills = place(blob, F.fills), o_st = place(blob, F.mc_st),
+               o_leaf = place(blob, leaf_refs), o_fills = place(blob, F.fills), o_st = place(blob, F.mc_st),
                o_pabs = place(blob, F.mc_pabs), o_mcc = place(blob, F.mc_cell), o_nut = place(blob, F.mc_nut),
                o_edges = place(blob, F.edges), o_uinst = place(blob, F.univ_inst),
                o_ioff = place(blob, F.inst_off), o_cpos = place(blob, F.cell_pos),
-               o_nboff = place(blob, F.hs_nb_off), o_nbc = place(blob, F.nb_cells), o_hsr = place(blob, F.hsr);
+               o_nboff = place(blob, F.hs_nb_off), o_nbc = place(blob, nb_refs), o_hsr = place(blob, F.hsr);
   const size_t o_pou = place(blob, F.r_pin_of_univ), o_poff = place(blob, F.r_pin_off),
                o_psid = place(blob, F.r_pin_sid), o_pmc = place(blob, F.r_pin_mc);
   m->blob_bytes = blob.size();
@@ -331,7 +342,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     g.cell_tr = (const double*)(b + o_ctr);
     g.univ = (const DUniv*)(b + o_univ);
     g.bih = (const BihNode*)(b + o_bih);
-    g.bih_leaf = (const int32_t*)(b + o_leaf);
+    g.bih_leaf = (const CRef*)(b + o_leaf);
     g.fills = (const int32_t*)(b + o_fills);
     g.mc_st = (const double*)(b + o_st);
     g.mc_pabs = (const double*)(b + o_pabs);
@@ -342,7 +353,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     g.inst_off = (const int32_t*)(b + o_ioff);
     g.cell_pos = (const int32_t*)(b + o_cpos);
     g.hs_nb_off = (const int32_t*)(b + o_nboff);
-    g.nb_cells = (const int32_t*)(b + o_nbc);
+    g.nb_cells = (const CRef*)(b + o_nbc);
     m->rg = F.rg;
     m->rg.pin_of_univ = (const int32_t*)(b + o_pou);
     m->rg.pin_off = (const int32_t*)(b + o_poff);

@@ -40,10 +40,10 @@ struct CsgTracker final : UnivTracker {
   __device__ int find_cell(const DevGeom& g, double x, double y, double z, int fsid, int fsense, int& ia,
                            int& ib, int& ic, double& tx, double& ty, double& tz,
                            uint32_t& flags) const override {
-    const int cell = csg_find(g, ld(&U->i0), x, y, z, fsid, fsense, flags);
+    int f = 0;
+    const int cell = csg_find(g, ld(&U->i0), x, y, z, fsid, fsense, flags, f);
     if (cell < 0) return -1;
     ia = cell; ib = 0; ic = 0;
-    const int f = ld(g.cell_fill + cell);
     if (f >= 0) return -2 - f;
     tx = ld(g.cell_tr + 3 * cell);
     ty = ld(g.cell_tr + 3 * cell + 1);

@@ -30,8 +30,15 @@ __device__ __forceinline__ double clamp0(double d) {
   return r;
 }
 
+// p ? a : b as one predicated select (no branch)
+__device__ __forceinline__ double dsel(bool p, double a, double b) {
+  double r;
+  asm("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %3, 0;\n\tselp.f64 %0, %1, %2, q;\n\t}"
+      : "=d"(r) : "d"(a), "d"(b), "r"(static_cast<unsigned>(p)));
+  return r;
+}
 __device__ __forceinline__ double sel3(int a, double x, double y, double z) {
-  return a == 0 ? x : (a == 1 ? y : z);
+  return dsel(a == 0, x, dsel(a == 1, y, z));
 }
 
 // f(r) of a surface (O3), evaluation order exactly as documented
@@ -89,14 +96,15 @@ __device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const 
       }
     }
   }
-  return ok ? clamp0(fdiv(num, den)) : NT_INF;
+  // the division runs on every lane (a lane without a forward exit would idle beside the others
+  // anyway); its result is discarded by the select
+  return dsel(ok, clamp0(fdiv(num, den)), NT_INF);
 }
 
 // Alg. 3 "cell contains pos" with an optional logically forced sense (O9'); on success the
 // O16 F1 proximity bit of the accepted cell is returned in `near`.
-__device__ __forceinline__ bool cell_contains(const DevGeom& g, int cell, double x, double y, double z,
+__device__ __forceinline__ bool cell_contains(const DevGeom& g, int h0, int h1, double x, double y, double z,
                                               int fsid, int fsense, uint32_t& near) {
-  const int h0 = ld(g.cell_hs + cell), h1 = ld(g.cell_hs + cell + 1);
   uint32_t nb = 0;
   for (int h = h0; h < h1; ++h) {
     const DHs* r = g.hsr + h;
@@ -152,8 +160,9 @@ __device__ __forceinline__ void bih_stats_done(unsigned cells, unsigned nodes) {
 // `first` / `nfirst`: an optional list of cells tested before the search (the crossing shortcut's
 // neighbours across the crossed half-space).  It is run as a leaf whose continuation is the root, so
 // the kernel holds one copy of the containment test.
+// Returns the cell (or -1) and its fill in `fill`.
 __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, double y, double z,
-                                        int fsid, int fsense, uint32_t& flags, const int32_t* first = nullptr,
+                                        int fsid, int fsense, uint32_t& flags, int& fill, const CRef* first = nullptr,
                                         int nfirst = 0) {
 #ifdef NT_BIH_STATS
   atomicAdd(&g_bih_stats[0], 1ull);
@@ -170,7 +179,7 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
 #endif
   for (;;) {
     int meta = 0, a = 0;
-    const int32_t* leaf = first;
+    const CRef* leaf = first;
     for (; !pre;) {                                      // internal nodes down to a leaf
       const BihNode* n = g.bih + root + node;
       meta = ld(&n->meta);
@@ -195,15 +204,16 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
     if (!pre) { leaf = g.bih_leaf + a; cnt = -meta - 1; }   // leaf: test its cells
     pre = false;
     for (int q = 0; q < cnt; ++q) {
-      const int cell = ld(leaf + q);
+      const int4 cr = __ldg(reinterpret_cast<const int4*>(leaf + q));   // cell, fill, h0, h1
       uint32_t nb = 0;
 #ifdef NT_BIH_STATS
       atomicAdd(&g_bih_stats[2], 1ull);
       ++st_cells;
 #endif
-      if (cell_contains(g, cell, x, y, z, fsid, fsense, nb)) {
+      if (cell_contains(g, cr.z, cr.w, x, y, z, fsid, fsense, nb)) {
         flags |= nb;
-        NT_BIH_RET(cell);
+        fill = cr.y;
+        NT_BIH_RET(cr.x);
       }
     }
     node = stk.pop();

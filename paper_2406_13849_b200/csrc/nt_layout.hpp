@@ -69,6 +69,11 @@ struct alignas(16) DUniv {
   double d[16];
 };
 
+// Cell reference (16 bytes) as listed by BIH leaves and crossing-neighbour lists: the cell id with its
+// fill (material-cell bin >= 0, or -1 - daughter uid) and its half-space range [h0, h1), so that a
+// point-location step reads everything about a candidate cell with one 16-byte load.
+struct alignas(16) CRef { int32_t cell, fill, h0, h1; };
+
 // Bounding-interval-hierarchy node (24 bytes): two planes per node.
 //  meta >= 0: internal, split axis = meta, children a and a+1;
 //             left child covers x[axis] <= lmax, right child x[axis] >= rmin (may overlap).
@@ -87,7 +92,7 @@ struct DevGeom {
   const double* cell_tr;      // [3*n_cells] fill translation
   const DUniv* univ;
   const BihNode* bih;
-  const int32_t* bih_leaf;
+  const CRef* bih_leaf;       // leaf cell lists (cell references)
   const int32_t* fills;
   const double* mc_st;        // per material cell: sigma_t
   const double* mc_pabs;      // per material cell: sigma_a / sigma_t (O14)
@@ -98,7 +103,7 @@ struct DevGeom {
   const int32_t* inst_off;    //   instances before child k of the universe
   const int32_t* cell_pos;    //   per cell: its position in its universe
   const int32_t* hs_nb_off;   // per half-space entry: [off, off+1) into nb_cells (CSG crossing shortcut)
-  const int32_t* nb_cells;
+  const CRef* nb_cells;       // cell references
   int32_t root, n_mc, max_depth, n_univ;
   int32_t n_cells, n_surf, root_kind, features;   // features: F_* bits present in the model
   const void* const* trk;     // DP dispatch only: per-universe tracker object pointers (dp_tracker.cuh)

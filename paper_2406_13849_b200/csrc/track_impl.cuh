@@ -93,7 +93,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
                                      double Tz, double rx, double ry, double rz, int fh, int fsense,
                                      int& L, int& mc, uint32_t& flags) {
   int fsid = -1;
-  const int32_t* nbl = nullptr;
+  const CRef* nbl = nullptr;
   int nnb = 0;
   if (fh >= 0) {
     fsid = hs_sid(ld(&g.hsr[fh].e));
@@ -116,11 +116,11 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
     int dau;
     if (kind == U_CSG) {
       const bool first = l == l0;
-      const int cell = csg_find(g, ld(&U->i0), x, y, z, first ? fsid : -1, fsense, flags, first ? nbl : nullptr,
+      int f = 0;
+      const int cell = csg_find(g, ld(&U->i0), x, y, z, first ? fsid : -1, fsense, flags, f, first ? nbl : nullptr,
                                 first ? nnb : 0);
       if (cell < 0) return false;
       st.a(l) = cell;
-      const int f = ld(g.cell_fill + cell);
       if (f >= 0) { L = l + 1; mc = f; return true; }
       dau = -1 - f;
       tx = ld(g.cell_tr + 3 * cell);
