@@ -86,14 +86,13 @@ __device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const 
         q = k * k - c;
       }
       const double sq = fsqrt(clamp0(q));                 // q < 0: max(q,0) inside, miss outside
-      if (!sense) {             // inside (negative side): far root
-        ok = a != 0.0;
-        if (k <= 0.0) { num = -k + sq; den = a; } else { num = -c; den = k + sq; }
-      } else {                  // outside: moving away or missing -> no exit
-        ok = a != 0.0 && k < 0.0 && q >= 0.0;
-        num = c;
-        den = -k + sq;
-      }
+      // inside (negative side), far root: k <= 0 -> (-k + sq) / a, else -c / (k + sq);
+      // outside: c / (-k + sq), no exit when moving away or missing.  Operands by selects.
+      const bool far = !sense && k <= 0.0;
+      const double mk = dsel(sense, -k, k);                // den = mk + sq unless `far`
+      num = dsel(far, -k + sq, dsel(sense, c, -c));
+      den = dsel(far, a, mk + sq);
+      ok = a != 0.0 && (!sense || (k < 0.0 && q >= 0.0));
     }
   }
   // the division runs on every lane (a lane without a forward exit would idle beside the others
@@ -419,9 +418,11 @@ __device__ __forceinline__ void rect_candidates(const DevGeom& g, const DUniv* U
       return;
     }
   }
-  if (u != 0.0) b.consider(rect_wall(ld(&U->d[0]), ld(&U->d[3]), ia, x, u), l, u > 0.0 ? 1 : 0, 0);
-  if (v != 0.0) b.consider(rect_wall(ld(&U->d[1]), ld(&U->d[4]), ib, y, v), l, v > 0.0 ? 3 : 2, 0);
-  if (!ld(&U->is2d) && w != 0.0) b.consider(rect_wall(ld(&U->d[2]), ld(&U->d[5]), ic, z, w), l, w > 0.0 ? 5 : 4, 0);
+  // an axis with a zero direction cosine has no wall: +inf (a no-op for consider), selected, no branch
+  b.consider(dsel(u != 0.0, rect_wall(ld(&U->d[0]), ld(&U->d[3]), ia, x, u), NT_INF), l, u > 0.0 ? 1 : 0, 0);
+  b.consider(dsel(v != 0.0, rect_wall(ld(&U->d[1]), ld(&U->d[4]), ib, y, v), NT_INF), l, v > 0.0 ? 3 : 2, 0);
+  if (!ld(&U->is2d))
+    b.consider(dsel(w != 0.0, rect_wall(ld(&U->d[2]), ld(&U->d[5]), ic, z, w), NT_INF), l, w > 0.0 ? 5 : 4, 0);
 }
 
 // tile centre of an array (the daughter translation, readings O8/O9/N1).  rect (i,j,k), hex (q,r,kz).
