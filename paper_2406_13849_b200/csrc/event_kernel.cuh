@@ -42,7 +42,7 @@ __device__ __forceinline__ void warp_count(bool pred, unsigned int* counter, int
 }
 
 // ring capacity: the power of two >= the slot count (a slot is in at most one ring at a time)
-__host__ __device__ constexpr int ring_size(int B) { return B <= 128 ? 128 : 256; }
+__host__ __device__ constexpr int ring_size(int S) { return S <= 128 ? 128 : S <= 256 ? 256 : 512; }
 
 size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false) {
   const size_t nmc = g.n_mc, d = g.max_depth;
@@ -70,36 +70,39 @@ __device__ __forceinline__ void vstore(uint16_t* p, uint32_t v) {
 // the head), runs that EVENT and MOVE on them, and appends every slot to the ring of its next
 // event (warp-aggregated atomic on the tail, entry published after a block fence).  The block
 // ends when the pids are exhausted and no history is live.
-template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false>
+// S = particle slots per block (ASYNC only: S may exceed B, so that a warp finishing its chunk finds
+// other slots queued instead of waiting for the chunks other warps hold; rounds need S == B).
+template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false, int S = B>
 __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGeom g, const KRun R) {
+  static_assert(ASYNC || S == B, "round-based queues need one slot per thread");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmc = g.n_mc, maxd = g.max_depth;
   // ---- carve shared memory (see event_smem_bytes)
   double* sx = reinterpret_cast<double*>(smem);
-  double* sy = sx + B; double* sz = sy + B; double* su = sz + B; double* sv = su + B; double* sw = sv + B;
-  double* stau = sw + B;
-  double* sTb = stau + B;                           // [maxd-1][3][B] (T_0 = 0)
-  double* sps = sTb + 3 * (maxd - 1) * B;           // TRACE: pending segment length
-  uint32_t* sidx = reinterpret_cast<uint32_t*>(sps + (TRACE ? B : 0));
-  uint32_t* sepoch = sidx + B; uint32_t* snseg = sepoch + B;
-  int32_t* smc = reinterpret_cast<int32_t*>(snseg + B);
-  int32_t* sos = smc + B;                           // on-surface sid (-1 none)
-  int32_t* sdesc = sos + B;                         // pending descent: l0 | fsense<<4 | (fh+1)<<5 (CSG: half-space, array: face)
-  int32_t* sib = sdesc + B;                         // [maxd][4][B]
-  int32_t* spj = sib + 4 * maxd * B;                // TRACE: pending j, cell_before
-  int32_t* spcb = spj + (TRACE ? B : 0);
-  uint8_t* sflags = reinterpret_cast<uint8_t*>(spcb + (TRACE ? B : 0));
-  uint8_t* sL = sflags + B;
-  int8_t* sosl = reinterpret_cast<int8_t*>(sL + B);
-  int8_t* spl = sosl + B;                           // TRACE: pending level
-  size_t off = (size_t)(reinterpret_cast<unsigned char*>(spl + (TRACE ? B : 0)) - smem);
+  double* sy = sx + S; double* sz = sy + S; double* su = sz + S; double* sv = su + S; double* sw = sv + S;
+  double* stau = sw + S;
+  double* sTb = stau + S;                           // [maxd-1][3][S] (T_0 = 0)
+  double* sps = sTb + 3 * (maxd - 1) * S;           // TRACE: pending segment length
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(sps + (TRACE ? S : 0));
+  uint32_t* sepoch = sidx + S; uint32_t* snseg = sepoch + S;
+  int32_t* smc = reinterpret_cast<int32_t*>(snseg + S);
+  int32_t* sos = smc + S;                           // on-surface sid (-1 none)
+  int32_t* sdesc = sos + S;                         // pending descent: l0 | fsense<<4 | (fh+1)<<5 (CSG: half-space, array: face)
+  int32_t* sib = sdesc + S;                         // [maxd][4][S]
+  int32_t* spj = sib + 4 * maxd * S;                // TRACE: pending j, cell_before
+  int32_t* spcb = spj + (TRACE ? S : 0);
+  uint8_t* sflags = reinterpret_cast<uint8_t*>(spcb + (TRACE ? S : 0));
+  uint8_t* sL = sflags + S;
+  int8_t* sosl = reinterpret_cast<int8_t*>(sL + S);
+  int8_t* spl = sosl + S;                           // TRACE: pending level
+  size_t off = (size_t)(reinterpret_cast<unsigned char*>(spl + (TRACE ? S : 0)) - smem);
   off = (off + 15) & ~size_t(15);
-  QIdx* sq = reinterpret_cast<QIdx*>(smem + off);            // [3][NQ][B]        (rounds)
-  constexpr int RB = ring_size(B);
+  QIdx* sq = reinterpret_cast<QIdx*>(smem + off);            // [3][NQ][S]        (rounds)
+  constexpr int RB = ring_size(S);
   uint16_t* ring = reinterpret_cast<uint16_t*>(smem + off);  // [NQ][RB] slot + 1, 0 = empty (ASYNC)
   unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NQ * RB)
-                               : reinterpret_cast<unsigned int*>(sq + 3 * NQ * B);
+                               : reinterpret_cast<unsigned int*>(sq + 3 * NQ * S);
   unsigned int* s_cnt = s_exit + nmc;
   int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [3][NQ]
   int* s_flag = s_qn + 3 * NQ;                              // [0] = pids exhausted, [1] live (ASYNC)
@@ -113,8 +116,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
   if (ASYNC) {
     for (int i = tid; i < NQ * RB; i += B) ring[i] = 0u;
     __syncthreads();
-    for (int i = tid; i < B; i += B) ring[Q_F * RB + i] = static_cast<uint16_t>(i + 1);    // all slots free
-    if (tid == 0) { a_tail[Q_F] = B; s_flag[0] = 0; s_flag[1] = 0; }
+    for (int i = tid; i < S; i += B) ring[Q_F * RB + i] = static_cast<uint16_t>(i + 1);    // all slots free
+    if (tid == 0) { a_tail[Q_F] = S; s_flag[0] = 0; s_flag[1] = 0; }
   } else {
     if (tid == 0) { s_flag[0] = 0; s_qn[0 * NQ + Q_F] = B; }
     for (int i = tid; i < B; i += B) sq[(0 * NQ + Q_F) * B + i] = static_cast<QIdx>(i);   // round 0 reads set 0: all slots free
@@ -278,7 +281,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           Stack st;
           st.si = sib + slot;
           st.sT = sTb + slot;
-          st.B = B;
+          st.B = S;
           double rx = 0, ry = 0, rz = 0;
           uint32_t flags = 0;
           int L = 0, mc = 0;
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           Stack st;
           st.si = sib + slot;
           st.sT = sTb + slot;
-          st.B = B;
+          st.B = S;
           double rx = sx[slot], ry = sy[slot], rz = sz[slot];
           double u = su[slot], v = sv[slot], w = sw[slot];
           double tau = stau[slot];

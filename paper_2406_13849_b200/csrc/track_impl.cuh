@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <type_traits>
 
 #include "../../include/nestrack.h"
@@ -586,9 +587,22 @@ cudaError_t launch_rect(const DevGeom&, const RectGeom&, const KRun&, bool, bool
 }
 #endif
 
+// Slots per block of the ring scheduler (block 256, SP): 320 when three such blocks still fit an SM
+// (a warp that finishes its chunk then finds queued slots instead of waiting for the chunks the
+// other seven warps hold), else 256.  NESTRACK_SLOTS=256|320 overrides (tuning).
+static int ring_slots(const DevGeom& g, bool trace) {
+  static const int env = [] { const char* e = getenv("NESTRACK_SLOTS"); return e ? atoi(e) : 0; }();
+  if (env == 256 || env == 320) return env;
+  int dev = 0, smem_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  const size_t need = 3 * (event_smem_bytes(g, 320, trace, true) + 1024);
+  return need <= (size_t)smem_sm ? 320 : 256;
+}
+
 cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
                          int blocks_per_sm, cudaStream_t stream, int* grid_out, bool async) {
-  const size_t smem = event_smem_bytes(g, block, trace, async);
+  size_t smem = event_smem_bytes(g, block, trace, async);
   auto go = [&](auto kern) -> cudaError_t {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -621,6 +635,11 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
       if (tally == 1) return states ? go(k_track_event<256, false, true, D, 1, true>) : go(k_track_event<256, false, false, D, 1, true>);
       if (tally == 2) return states ? go(k_track_event<256, false, true, D, 2, true>) : go(k_track_event<256, false, false, D, 2, true>);
       if (tally == 3) return states ? go(k_track_event<256, false, true, D, 3, true>) : go(k_track_event<256, false, false, D, 3, true>);
+      if (!D && ring_slots(g, trace) == 320) {
+        smem = event_smem_bytes(g, 320, trace, true);
+        if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 320>) : go(k_track_event<256, true, false, false, 0, true, 320>);
+        return states ? go(k_track_event<256, false, true, false, 0, true, 320>) : go(k_track_event<256, false, false, false, 0, true, 320>);
+      }
       if (trace) return states ? go(k_track_event<256, true, true, D, 0, true>) : go(k_track_event<256, true, false, D, 0, true>);
       return states ? go(k_track_event<256, false, true, D, 0, true>) : go(k_track_event<256, false, false, D, 0, true>);
     };
