@@ -268,36 +268,9 @@ def main():
             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz (DESIGN.md)",
             "falg_flops_per_segment": falg, "kernel_ms_per_launch": 1e3 * kernel_s}
 
-    # the metric's second half: generic tree tracker vs the rect-specialised tracker, same histories
-    ratio = None
-    if not a.no_ratio and a.tracker == "generic" and model.info["rect_specialisable"]:
-        def timed(kk):
-            o2 = torch.zeros_like(out)
-            model.track(n, seed=seed0 + 20_000, pid_begin=rank * n, out=o2, stream=stream, mesh=mbuf, **kk)
-            torch.cuda.synchronize()
-            tt, ss = 0.0, 0
-            for s in range(a.steps):
-                o2.zero_()
-                flush.max()
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                model.track(n, seed=seed0 + s, pid_begin=rank * n, out=o2, stream=stream, mesh=mbuf, **kk)
-                e1.record(stream)
-                torch.cuda.synchronize()
-                tt += e0.elapsed_time(e1) / 1e3
-                ss += model.unpack(o2)["counters"]["segments"]
-            return ss / tt, ss
-        rg, sg = timed(kw)
-        rr, sr = timed(dict(kw, tracker="rect", scheduler="history"))
-        rh, sh = timed(dict(kw, scheduler="history"))
-        ratio = {"generic_over_rect": rg / rr, "generic_segments_per_s": rg, "rect_segments_per_s": rr,
-                 "segments_equal": sg == sr == sh, "generic_scheduler": kw["scheduler"],
-                 "generic_history_over_rect": rh / rr, "generic_history_segments_per_s": rh,
-                 "note": "this rank, identical seeds/pids, no all-reduce; rect = Alg. 9-10 specialised "
-                         "tracker, history-based; generic_history_over_rect compares the two trackers "
-                         "under the same (history) scheduling; target >= 0.85 (north star)"}
-
+    # end to end right after the device-timed steps, under the same clocks (sampled here too)
     e2e = None
+    ck_e2e = ClockSampler(local).start() if not a.no_e2e else None
     if not a.no_e2e and mbuf is not None:
         # mesh runs: the public Python call + D2H of the packed tallies and the mesh (pinned host)
         hout = torch.empty(model.out_len, dtype=torch.float64).pin_memory()
@@ -346,6 +319,39 @@ def main():
         e2e = {"value": esegs / te, "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": int(model.out_len * 8),
                "api": "nt_track_host (host output buffer; births generated on device from seed/pid)"}
+    if ck_e2e is not None:
+        ce = ck_e2e.stop()
+        if e2e is not None:
+            e2e["clocks"] = ce
+
+    # the metric's second half: generic tree tracker vs the rect-specialised tracker, same histories
+    ratio = None
+    if not a.no_ratio and a.tracker == "generic" and model.info["rect_specialisable"]:
+        def timed(kk):
+            o2 = torch.zeros_like(out)
+            model.track(n, seed=seed0 + 20_000, pid_begin=rank * n, out=o2, stream=stream, mesh=mbuf, **kk)
+            torch.cuda.synchronize()
+            tt, ss = 0.0, 0
+            for s in range(a.steps):
+                o2.zero_()
+                flush.max()
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                model.track(n, seed=seed0 + s, pid_begin=rank * n, out=o2, stream=stream, mesh=mbuf, **kk)
+                e1.record(stream)
+                torch.cuda.synchronize()
+                tt += e0.elapsed_time(e1) / 1e3
+                ss += model.unpack(o2)["counters"]["segments"]
+            return ss / tt, ss
+        rg, sg = timed(kw)
+        rr, sr = timed(dict(kw, tracker="rect", scheduler="history"))
+        rh, sh = timed(dict(kw, scheduler="history"))
+        ratio = {"generic_over_rect": rg / rr, "generic_segments_per_s": rg, "rect_segments_per_s": rr,
+                 "segments_equal": sg == sr == sh, "generic_scheduler": kw["scheduler"],
+                 "generic_history_over_rect": rh / rr, "generic_history_segments_per_s": rh,
+                 "note": "this rank, identical seeds/pids, no all-reduce; rect = Alg. 9-10 specialised "
+                         "tracker, history-based; generic_history_over_rect compares the two trackers "
+                         "under the same (history) scheduling; target >= 0.85 (north star)"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,

@@ -236,7 +236,7 @@ __device__ __forceinline__ void flush_tallies(const KRun& R, double* gl, const u
 enum { C_PART = 0, C_SEG, C_CROSS, C_REFL, C_LEAK, C_COLL, C_ABS, C_LOST, C_CAP, C_FLAG, C_CBL0 };
 
 template <bool TRACE, bool STATES, int TALLY = 0>
-__global__ void __launch_bounds__(256) k_track_generic(const DevGeom g, const KRun R) {
+__global__ void __launch_bounds__(256, 3) k_track_generic(const DevGeom g, const KRun R) {
   extern __shared__ __align__(16) unsigned char smem[];
   const int B = blockDim.x, tid = threadIdx.x, lane = tid & 31;
   const int nmc = g.n_mc;
