@@ -91,6 +91,14 @@ def test_c3_parity_seeds(nt, orc, seed):
     _compare(nt, orc, spec, 1000, seed=seed, pid_begin=12345, trace=False)
 
 
+@pytest.mark.parametrize("cfg", ["c1", "c2", "c4"])
+def test_config_parity_untraced(nt, orc, cfg):
+    """Untraced runs take the ring scheduler's 320-slot kernel where it fits (a traced run needs more
+    shared memory per slot and keeps 256): counters, exits, lengths and flags against the oracle."""
+    spec, _ = workloads.config(cfg)
+    _compare(nt, orc, spec, 3000, seed=2, pid_begin=777, trace=False)
+
+
 @pytest.mark.parametrize("name", ["sphere_in_box", "hex_pins_small_pointy", "hex_pins_small_flat",
                                   "rect3d_small", "lattice3_nested", "lattice3_flat", "infinite_medium",
                                   "c1_void_vacuum"])
@@ -498,3 +506,43 @@ def test_power_iteration_distributed_single_rank(nt, orc):
     om = orc.OracleModel.from_spec(spec)
     ks = nt.power_iteration_distributed(m, 1000, 3, seed=8)
     assert ks == m.power_iteration(1000, cycles=3, seed=8) == om.power_iteration(1000, cycles=3, seed=8)
+
+
+_SLOTS_SCRIPT = r"""
+import sys, json, hashlib
+sys.path.insert(0, sys.argv[1])
+import torch, workloads, paper_2406_13849_b200 as nt
+m = nt.Model.from_spec(workloads.c3_full_core(), device=0)
+res = m.track(200000, seed=5, pid_begin=123456, pflags=True, per_history=True)
+torch.cuda.synchronize()
+g = m.unpack(res["out"])
+h = hashlib.sha256()
+for k in ("pflags", "pnseg", "pterm"):
+    h.update(res[k].cpu().numpy().tobytes())
+print(json.dumps({"counters": g["counters"], "exits": [int(x) for x in g["exits"]],
+                  "len": [float(x).hex() for x in g["len"]], "per_history": h.hexdigest()}))
+"""
+
+
+def test_ring_slot_counts_agree(nt):
+    """The ring scheduler's 320-slot and 256-slot kernels (NESTRACK_SLOTS, read once per process)
+    give the same walks: counters, exits and every history's segment count, terminal and flags
+    equal; lengths to summation order."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    outs = {}
+    for slots in ("256", "320"):
+        env = dict(os.environ, NESTRACK_SLOTS=slots)
+        p = subprocess.run([sys.executable, "-c", _SLOTS_SCRIPT, root], env=env, capture_output=True, text=True,
+                           timeout=600)
+        assert p.returncode == 0, p.stderr[-2000:]
+        outs[slots] = json.loads(p.stdout.strip().splitlines()[-1])
+    a, b = outs["256"], outs["320"]
+    assert a["counters"] == b["counters"] and a["exits"] == b["exits"]
+    assert a["per_history"] == b["per_history"]
+    la = np.array([float.fromhex(x) for x in a["len"]])
+    lb = np.array([float.fromhex(x) for x in b["len"]])
+    assert np.allclose(la, lb, rtol=1e-12, atol=0)
