@@ -41,7 +41,8 @@ struct CsgTracker final : UnivTracker {
                            int& ib, int& ic, double& tx, double& ty, double& tz,
                            uint32_t& flags) const override {
     int f = 0;
-    const int cell = csg_find(g, ld(&U->i0), x, y, z, fsid, fsense, flags, f);
+    int h0 = 0, h1 = 0;
+    const int cell = csg_find(g, ld(&U->i0), x, y, z, fsid, fsense, flags, f, h0, h1);
     if (cell < 0) return -1;
     ia = cell; ib = 0; ic = 0;
     if (f >= 0) return -2 - f;

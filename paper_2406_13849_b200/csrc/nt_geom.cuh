@@ -56,16 +56,18 @@ __device__ __forceinline__ double surf_f(int kind, const double* sp, double x, d
 // os: particle logically on this surface (quadric c := 0).  Returns +inf when no exit.
 // Written with ONE division and ONE square root per call (selected operands) to keep the
 // code small; the selected operands are exactly those of the case formulas in DESIGN.md O11.
-__device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const double* sp, double x,
-                                            double y, double z, double u, double v, double w) {
+// Coefficients are passed by value: the caller loads the whole record before the kind branch, so
+// the loads overlap (surf_dist(..., const double* sp, ...) below loads them for other callers).
+__device__ __forceinline__ double surf_dist(int kind, int sense, bool os, double c0, double c1, double c2,
+                                            double c3, double x, double y, double z, double u, double v,
+                                            double w) {
   double num, den;
   bool ok;
   if (kind <= S_PZ) {
     den = sel3(kind, u, v, w);
     ok = sense ? den < 0.0 : den > 0.0;                      // also excludes den == 0
-    num = ld(&sp[0]) - sel3(kind, x, y, z);
+    num = c0 - sel3(kind, x, y, z);
   } else {
-    const double c0 = ld(&sp[0]), c1 = ld(&sp[1]), c2 = ld(&sp[2]), c3 = ld(&sp[3]);
     if (kPlane && kind == S_PLANE) {
       den = (c0 * u + c1 * v) + c2 * w;
       ok = sense ? den < 0.0 : den > 0.0;
@@ -98,6 +100,10 @@ __device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const 
   // the division runs on every lane (a lane without a forward exit would idle beside the others
   // anyway); its result is discarded by the select
   return dsel(ok, clamp0(fdiv(num, den)), NT_INF);
+}
+__device__ __forceinline__ double surf_dist(int kind, int sense, bool os, const double* sp, double x,
+                                            double y, double z, double u, double v, double w) {
+  return surf_dist(kind, sense, os, ld(&sp[0]), ld(&sp[1]), ld(&sp[2]), ld(&sp[3]), x, y, z, u, v, w);
 }
 
 // Alg. 3 "cell contains pos" with an optional logically forced sense (O9'); on success the
@@ -161,8 +167,8 @@ __device__ __forceinline__ void bih_stats_done(unsigned cells, unsigned nodes) {
 // the kernel holds one copy of the containment test.
 // Returns the cell (or -1) and its fill in `fill`.
 __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, double y, double z,
-                                        int fsid, int fsense, uint32_t& flags, int& fill, const CRef* first = nullptr,
-                                        int nfirst = 0) {
+                                        int fsid, int fsense, uint32_t& flags, int& fill, int& h0, int& h1,
+                                        const CRef* first = nullptr, int nfirst = 0) {
 #ifdef NT_BIH_STATS
   atomicAdd(&g_bih_stats[0], 1ull);
 #endif
@@ -212,6 +218,8 @@ __device__ __forceinline__ int csg_find(const DevGeom& g, int root, double x, do
       if (cell_contains(g, cr.z, cr.w, x, y, z, fsid, fsense, nb)) {
         flags |= nb;
         fill = cr.y;
+        h0 = cr.z;
+        h1 = cr.w;
         NT_BIH_RET(cr.x);
       }
     }

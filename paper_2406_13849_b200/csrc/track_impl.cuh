@@ -117,11 +117,13 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
     int dau;
     if (kind == U_CSG) {
       const bool first = l == l0;
-      int f = 0;
-      const int cell = csg_find(g, ld(&U->i0), x, y, z, first ? fsid : -1, fsense, flags, f, first ? nbl : nullptr,
-                                first ? nnb : 0);
+      int f = 0, h0 = 0, h1 = 0;
+      const int cell = csg_find(g, ld(&U->i0), x, y, z, first ? fsid : -1, fsense, flags, f, h0, h1,
+                                first ? nbl : nullptr, first ? nnb : 0);
       if (cell < 0) return false;
       st.a(l) = cell;
+      st.b(l) = h0;                 // a CSG level keeps its cell's half-space range in b, c
+      st.c(l) = h1;
       if (f >= 0) { L = l + 1; mc = f; return true; }
       dau = -1 - f;
       tx = ld(g.cell_tr + 3 * cell);
@@ -157,14 +159,16 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
                                                  int ic, int l, double x, double y, double z, double u,
                                                  double v, double w, int os_l, int os_s, Best& b) {
   if (kind == U_CSG) {
-    const int cell = ia;
-    const int h0 = ld(g.cell_hs + cell), h1 = ld(g.cell_hs + cell + 1);
+    const int h0 = ib, h1 = ic;     // the cell's half-space range, kept in the stack by the descent
 #pragma unroll 1
     for (int h = h0; h < h1; ++h) {
       const DHs* r = g.hsr + h;
+      const double2 c01 = __ldg(reinterpret_cast<const double2*>(r->c));
+      const double2 c23 = __ldg(reinterpret_cast<const double2*>(r->c + 2));
       const int e = ld(&r->e);
       const int sid = hs_sid(e);
-      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, r->c, x, y, z, u, v, w);
+      const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, c01.x, c01.y, c23.x, c23.y,
+                                 x, y, z, u, v, w);
       b.consider(d, l, h, hs_sense(e));          // +inf (no hit) is a no-op; CSG key = half-space index
     }
   } else if (!kHex || kind == U_RECT) {
