@@ -636,6 +636,12 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
     if (block != 256) return cudaErrorInvalidValue;
     auto pick = [&](auto dp) -> cudaError_t {
       constexpr bool D = decltype(dp)::value;
+      if (!D && tally && ring_slots(g, false) == 320) {   // mesh / instance tallies: 320 slots as well
+        smem = event_smem_bytes(g, 320, false, true);
+        if (tally == 1) return states ? go(k_track_event<256, false, true, false, 1, true, 320>) : go(k_track_event<256, false, false, false, 1, true, 320>);
+        if (tally == 2) return states ? go(k_track_event<256, false, true, false, 2, true, 320>) : go(k_track_event<256, false, false, false, 2, true, 320>);
+        return states ? go(k_track_event<256, false, true, false, 3, true, 320>) : go(k_track_event<256, false, false, false, 3, true, 320>);
+      }
       if (tally == 1) return states ? go(k_track_event<256, false, true, D, 1, true>) : go(k_track_event<256, false, false, D, 1, true>);
       if (tally == 2) return states ? go(k_track_event<256, false, true, D, 2, true>) : go(k_track_event<256, false, false, D, 2, true>);
       if (tally == 3) return states ? go(k_track_event<256, false, true, D, 3, true>) : go(k_track_event<256, false, false, D, 3, true>);
