@@ -292,10 +292,10 @@ __device__ __forceinline__ void bank_sites(const DevGeom& g, double* bank, uint8
 // segment r + t om, t in [0, s].  The cut parameters are (E_a(i) - r_a) / om_a with
 // E_a(i) = lo_a + i d_a -- the oracle's -- so every scored piece is the oracle's piece.  Pieces
 // outside the mesh are skipped; the walk stops once the ray leaves the mesh on some axis.
-// Out of line: the branch that calls it is taken only by runs that pass a mesh buffer.
+// Inlined: only the mesh-tally kernel instantiations (TALLY & 1) contain the call.
 struct MeshGeom { double lo[3], d[3]; int n[3]; };
 
-__device__ __noinline__ void mesh_score_impl(const MeshGeom M, double* out, double x, double y, double z,
+__device__ __forceinline__ void mesh_score_impl(const MeshGeom M, double* out, double x, double y, double z,
                                              double u, double v, double w, double s) {
   if (!(s > 0.0)) return;
   const double r[3] = {x, y, z}, om[3] = {u, v, w};
