@@ -179,16 +179,16 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
     hex_m(ia, ib, m0, m1, m2);
     const double p = ld(&U->d[2]);
     const double tk[3] = {t0, t1, t2}, mk[3] = {m0, m1, m2};
-#pragma unroll 1
+    // unrolled (the t / m arrays stay in registers) and branch-free: a family with g_k = 0 has no
+    // forward face, +inf is a no-op for consider
+#pragma unroll
     for (int k = 0; k < 3; ++k) {
       const double gk = ld(&U->d[10 + 2 * k]) * u + ld(&U->d[11 + 2 * k]) * v;
-      if (gk != 0.0) {
-        const double bnd = gk > 0.0 ? mk[k] + 0.5 : mk[k] - 0.5;
-        b.consider(clamp0(fdiv(p * (bnd - tk[k]), gk)), l, gk > 0.0 ? k : k + 3, 0);
-      }
+      const double bnd = dsel(gk > 0.0, mk[k] + 0.5, mk[k] - 0.5);
+      b.consider(dsel(gk != 0.0, clamp0(fdiv(p * (bnd - tk[k]), gk)), NT_INF), l, gk > 0.0 ? k : k + 3, 0);
     }
-    if (ld(&U->i1) > 0 && w != 0.0)
-      b.consider(rect_wall(ld(&U->d[4]), ld(&U->d[5]), ic, z, w), l, w > 0.0 ? 7 : 6, 0);
+    if (ld(&U->i1) > 0)
+      b.consider(dsel(w != 0.0, rect_wall(ld(&U->d[4]), ld(&U->d[5]), ic, z, w), NT_INF), l, w > 0.0 ? 7 : 6, 0);
   }
 }
 
