@@ -297,16 +297,23 @@ def main():
         hout = None
         import numpy as np
         hout = np.zeros(model.out_len)
-        for w in range(1):
-            model.track_host(min(n, 100000), seed=seed0, out=hout, **kw)
+        for w in range(max(a.warmup, 1)):          # the same W full-size warm-up steps as the device timing
+            model.track_host(n, seed=seed0 + 400 + w, pid_begin=rank * n, out=hout, stream=stream, **kw)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         esegs = 0
         if dist is not None:
             dist.barrier()
         t0 = time.perf_counter()
         e0.record(stream)
+        step_ms, step_dev = [], []
         for s in range(a.steps):
+            ts = time.perf_counter()
+            d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            d0.record(stream)
             model.track_host(n, seed=seed0 + 500 + s, pid_begin=rank * n, out=hout, stream=stream, **kw)
+            d1.record(stream)
+            step_ms.append(1e3 * (time.perf_counter() - ts))
+            step_dev.append((d0, d1))
             esegs += int(hout[2 * model.n_mc + 1])
         e1.record(stream)
         torch.cuda.synchronize()
@@ -318,7 +325,9 @@ def main():
             te, esegs = float(tt[0]), int(tt[1])
         e2e = {"value": esegs / te, "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": int(model.out_len * 8),
-               "api": "nt_track_host (host output buffer; births generated on device from seed/pid)"}
+               "api": "nt_track_host (host output buffer; births generated on device from seed/pid)",
+               "step_ms": [round(x, 1) for x in step_ms],
+               "step_device_ms": [round(d0.elapsed_time(d1), 1) for d0, d1 in step_dev]}
     if ck_e2e is not None:
         ce = ck_e2e.stop()
         if e2e is not None:
