@@ -319,6 +319,14 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     cudaGetDevice(&prev);
     cudaError_t e = cudaSetDevice(o->device);
     if (e != cudaSuccess) return cuda_err(e, "nt_finalize: cudaSetDevice");
+    {   // per-launch scratch is stream-ordered (cudaMallocAsync); let the device's default pool keep up
+        // to 64 MB across synchronisations instead of unmapping and remapping it every launch
+      cudaMemPool_t pool;
+      if (cudaDeviceGetDefaultMemPool(&pool, o->device) == cudaSuccess) {
+        uint64_t keep = 64ull << 20;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      }
+    }
     e = cudaMalloc(&m->blob, blob.size());
     if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_err(e, "nt_finalize: cudaMalloc"); }
     e = cudaMemcpy(m->blob, blob.data(), blob.size(), cudaMemcpyHostToDevice);
