@@ -24,6 +24,9 @@ NT_DEV_BEGIN
 // Queue layout (uint8 slot indices), triple-buffered by round:
 //   Q_M[p] move-ready, Q_C[p] collide, Q_DC[p] CSG descents, Q_DA[p] array descents, Q_F[p] free
 enum { Q_M = 0, Q_C = 1, Q_DC = 2, Q_DA = 3, Q_F = 4, NQ = 5 };
+#ifndef NT_RING_SLEEP_NS
+#define NT_RING_SLEEP_NS 64     // back-off of a warp that found every ring empty
+#endif
 using QIdx = uint8_t;           // slot index in a queue (blocks own <= 256 slots)
 
 __device__ __forceinline__ int warp_append(bool pred, int* counter, int lane) {
@@ -178,7 +181,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             continue;
           }
           if (!births && vload(reinterpret_cast<uint32_t*>(s_flag + 1)) == 0u) break;   // all done
-          __nanosleep(64);
+          __nanosleep(NT_RING_SLEEP_NS);
         }
         if (q < 0) break;
         valid = static_cast<uint32_t>(lane) < take;
