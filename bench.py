@@ -113,6 +113,28 @@ def _load_json(name):
     return None
 
 
+def _measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return None
+
+
+def _traffic_key(name, a, mesh_shape):
+    """profiles/traffic.json holds one ncu capture per (workload, variant) that was profiled."""
+    k = name
+    if a.tracker != "generic":
+        k += ".rect"
+    elif a.scheduler != "block":
+        k += "." + a.scheduler
+    if a.pseudo_array:
+        k += ".pseudo"
+    if mesh_shape:
+        k += ".mesh" + "x".join(map(str, mesh_shape))
+    return k
+
+
 def fp64_peak_tflops(sm_max_mhz: float | None) -> float:
     """fp64 FMA peak derived from unit counts: 148 SMs x 64 FP64 lanes x
     2 flop/FMA x max SM clock (1965 MHz) = 37.2 TFLOP/s."""
@@ -135,9 +157,29 @@ def cpu_baseline(spec, seed: int, budget_s: float):
     r = om.run(n2, seed=seed, pid_begin=10_000_000, threads=cores)
     dt = time.perf_counter() - t
     seg = r["counters"]["segments"]
+    # the same oracle on one core, on a smaller sample (~budget/3 s)
+    n1 = int(max(200, n2 * (budget_s / 3.0) / max(dt * cores, 1e-3)))
+    t = time.perf_counter()
+    r1 = om.run(n1, seed=seed, pid_begin=20_000_000, threads=1)
+    dt1 = time.perf_counter() - t
+    seg1 = r1["counters"]["segments"]
     return {"value": seg / dt, "unit": UNIT, "cores": cores, "kind": "oracle",
             "sample": f"{n2} histories of {spec['name']} (pids 1e7..), {seg} segments, {dt:.1f} s",
+            "value_1core": seg1 / dt1,
+            "sample_1core": f"{n1} histories (pids 2e7..), {seg1} segments, {dt1:.1f} s, 1 thread",
+            "cpu_model": _cpu_model(),
             "falg_flops_per_segment": om.falg(r)}
+
+
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
 
 
 def run_reference(a, spec, rank, world):
@@ -152,7 +194,8 @@ def run_reference(a, spec, rank, world):
     t = time.perf_counter()
     om.run(n, seed=1, threads=cores)
     per = (time.perf_counter() - t) / n
-    n_step = int(max(1000, min(2_000_000, 8.0 / max(per, 1e-9))))   # ~8 s per step
+    step_s = min(8.0, a.cpu_seconds)
+    n_step = int(max(1000, min(2_000_000, step_s / max(per, 1e-9))))   # ~8 s per step
     for w in range(a.warmup):
         om.run(min(n_step, 20000), seed=100 + w, threads=cores)
     segs, tt = 0, 0.0
@@ -174,9 +217,29 @@ def run_reference(a, spec, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def _free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def _self_launch(a):
+    """`bench.py --gpus N` outside torchrun: re-exec as N ranks (one process per GPU) under
+    torch.distributed.run on 127.0.0.1, the launch the driver uses for N > 1."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={a.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    print(f"bench.py: launching {a.gpus} ranks: {' '.join(cmd)}", file=sys.stderr, flush=True)
+    os.execv(sys.executable, cmd)
+
+
 def main():
     a = _args()
+    if a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        _self_launch(a)
     rank, world, local = _dist_env()
+    if world != a.gpus:
+        raise SystemExit(f"bench.py: --gpus {a.gpus} but WORLD_SIZE={world}; launch one rank per GPU")
     import workloads
     spec, n_cfg = workloads.config(a.config)
     if a.impl == "reference":
@@ -185,11 +248,17 @@ def main():
 
     import torch
     import paper_2406_13849_b200 as nt
+    if not torch.cuda.is_available() or torch.cuda.device_count() <= local:
+        raise SystemExit(f"bench.py: rank {rank} needs cuda:{local}, "
+                         f"{torch.cuda.device_count()} CUDA device(s) visible")
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rank == 0:
+            print(f"bench.py: {world} ranks, NCCL {'.'.join(map(str, torch.cuda.nccl.version()))}",
+                  file=sys.stderr, flush=True)
     n = int(a.particles) if a.particles else n_cfg
     mesh_shape = None
     if a.mesh:
@@ -238,12 +307,14 @@ def main():
     if dist is not None:
         dist.barrier()
     ck = clocks.stop()
-    t_rank = sum(e0.elapsed_time(e1) for e0, e1 in ev) / 1e3
+    step_s = [e0.elapsed_time(e1) / 1e3 for e0, e1 in ev]
+    t_rank = sum(step_s)
     t_max = t_rank
     if dist is not None:
-        tt = torch.tensor([t_rank], dtype=torch.float64, device="cuda")
+        tt = torch.tensor([t_rank] + step_s, dtype=torch.float64, device="cuda")
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        t_max = float(tt)
+        t_max = float(tt[0])
+        step_s = [float(x) for x in tt[1:]]          # per step: max over ranks
     per_step = [model.unpack(o) for o in outs]
     res = per_step[-1]
     segs = sum(p["counters"]["segments"] for p in per_step)      # all ranks (post all-reduce)
@@ -262,11 +333,21 @@ def main():
     kernel_s = t_rank / a.steps
     achieved = (falg or 0.0) * (segs / (world * a.steps)) / kernel_s / 1e12 if falg else None
     traffic_doc = _load_json("traffic.json") or {}
-    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-            "frac": (achieved / peak) if achieved else None,
-            "traffic": traffic_doc.get(spec["name"]),
+    traffic = traffic_doc.get(_traffic_key(spec["name"], a, mesh_shape))
+    hbm_peak = (_measured_peaks() or {}).get("hbm_gbs")
+    hbm = None
+    if traffic is not None and hbm_peak:
+        gbs = traffic / kernel_s / 1e9
+        hbm = {"bytes_per_launch": traffic, "achieved": gbs, "peak": hbm_peak, "unit": "GB/s",
+               "frac": gbs / hbm_peak, "source": "ncu dram__bytes_read.sum + dram__bytes_write.sum of one "
+               "launch (profiles/traffic.json) / this run's kernel time; peak MEASURED_PEAKS.json hbm_gbs"}
+    frac = (achieved / peak) if achieved else None
+    roof = {"bound": "alu", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": frac,
+            "traffic": traffic,
             "peak_source": "derived: 148 SM x 64 FP64 FMA/clk x 2 x sm_max_mhz (DESIGN.md)",
-            "falg_flops_per_segment": falg, "kernel_ms_per_launch": 1e3 * kernel_s}
+            "falg_flops_per_segment": falg, "kernel_ms_per_launch": 1e3 * kernel_s,
+            "hbm": hbm,
+            "binding": ("hbm" if hbm and frac is not None and hbm["frac"] > frac else "alu (fp64)")}
 
     # end to end right after the device-timed steps, under the same clocks (sampled here too)
     e2e = None
@@ -326,6 +407,9 @@ def main():
         e2e = {"value": esegs / te, "unit": UNIT, "h2d_bytes_per_step": 0,
                "d2h_bytes_per_step": int(model.out_len * 8),
                "api": "nt_track_host (host output buffer; births generated on device from seed/pid)",
+               "note": "the method's per-step inputs are (seed, pid range): histories are born on the "
+                       "device from Philox(seed, pid) (SURVEY O17/O18), so there are no input bytes to "
+                       "copy; the D2H of the packed tallies is inside the timed region",
                "step_ms": [round(x, 1) for x in step_ms],
                "step_device_ms": [round(d0.elapsed_time(d1), 1) for d0, d1 in step_dev]}
     if ck_e2e is not None:
@@ -374,6 +458,10 @@ def main():
                            "l2": "256 MB buffer read between timed steps (L2 flushed)",
                            "mesh_tally": mesh_shape},
                 "particles_per_s": particles / t_max,
+                "step_ms": [round(1e3 * x, 3) for x in step_s],
+                "ms_per_step_median": 1e3 * _median(step_s),
+                "cv": _cv(step_s),
+                "segments_per_s_median_step": segs / a.steps / _median(step_s),
                 "segments_per_history": segs / particles,
                 "counters_last_step": res["counters"],
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "rect_ratio": ratio,
@@ -382,6 +470,20 @@ def main():
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()
+
+
+def _median(x):
+    y = sorted(x)
+    k = len(y)
+    return y[k // 2] if k % 2 else 0.5 * (y[k // 2 - 1] + y[k // 2])
+
+
+def _cv(x):
+    if len(x) < 2:
+        return None
+    m = sum(x) / len(x)
+    var = sum((v - m) ** 2 for v in x) / (len(x) - 1)
+    return var ** 0.5 / m
 
 
 if __name__ == "__main__":

@@ -463,8 +463,37 @@ def track_distributed(model: Model, n_total: int, seed: int, pid_begin: int = 0,
     else:
         out = tracker_fn(n, pid_begin + b)
     if world > 1:
-        dist.all_reduce(out, op=dist.ReduceOp.SUM, group=group)
+        _all_reduce_sum(out, group)
     return out
+
+
+def _host_staged(group) -> bool:
+    """gloo runs all_gather on host tensors only (and is the backend of the CPU / one-GPU
+    multi-rank tests); NCCL takes device tensors directly."""
+    import torch.distributed as dist
+    return dist.get_backend(group) == "gloo"
+
+
+def _all_reduce_sum(t, group=None):
+    import torch.distributed as dist
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        dist.all_reduce(h, op=dist.ReduceOp.SUM, group=group)
+        t.copy_(h)
+    else:
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=group)
+
+
+def _all_gather(t, world: int, group=None):
+    import torch.distributed as dist
+    if t.is_cuda and _host_staged(group):
+        h = t.cpu()
+        bufs = [h.new_zeros(h.shape) for _ in range(world)]
+        dist.all_gather(bufs, h, group=group)
+        return [b.to(t.device) for b in bufs]
+    bufs = [t.new_zeros(t.shape) for _ in range(world)]
+    dist.all_gather(bufs, t, group=group)
+    return bufs
 
 
 def power_iteration_distributed(model: Model, n: int, cycles: int, seed: int = 240613849, group=None,
@@ -490,28 +519,26 @@ def power_iteration_distributed(model: Model, n: int, cycles: int, seed: int = 2
             M = C.c_uint64()
             _check(model.L.nt_bank_compact(model.h, C.c_void_p(res["bank"].data_ptr()),
                                            C.c_void_p(res["bank_n"].data_ptr()), nn,
-                                           C.c_void_p(sites.data_ptr()), C.byref(M), None))
+                                           C.c_void_p(sites.data_ptr()), C.byref(M),
+                                           _stream_handle(None)))
             return sites[:3 * M.value].view(-1, 3), int(M.value)
     if sample_fn is None:
         def sample_fn(sites, M, cycle, j0, nn):
             st = torch.empty((6, max(nn, 1)), dtype=torch.float64, device=sites.device)
             sites = sites.contiguous()
             _check(model.L.nt_source_from_sites(model.h, C.c_void_p(sites.data_ptr()), M, seed, cycle, j0, nn,
-                                                C.c_void_p(st.data_ptr()), None))
+                                                C.c_void_p(st.data_ptr()), _stream_handle(None)))
             return st[:, :nn].contiguous()
     ks, states = [], None
     for c in range(cycles):
         sites, Mr = track_fn(n, (c << 32) + rank * n, states, c)
         if world > 1:
             cnt = torch.tensor([Mr], dtype=torch.int64, device=sites.device)
-            counts = [torch.zeros_like(cnt) for _ in range(world)]
-            dist.all_gather(counts, cnt, group=group)
-            counts = [int(x.item()) for x in counts]
+            counts = [int(x.item()) for x in _all_gather(cnt, world, group)]
             pad = max(max(counts), 1)
             buf = torch.zeros((pad, 3), dtype=torch.float64, device=sites.device)
             buf[:Mr] = sites
-            bufs = [torch.zeros_like(buf) for _ in range(world)]
-            dist.all_gather(bufs, buf, group=group)
+            bufs = _all_gather(buf, world, group)
             sites = torch.cat([bufs[r][:counts[r]] for r in range(world)])
             M = sum(counts)
         else:

@@ -103,3 +103,22 @@ def test_two_rank_power_iteration_allgather(tmp_path, oracle_mod):
     om = oracle_mod.OracleModel.from_spec(workloads.infinite_medium(1.0, 0.25, 0.55))
     ref = om.power_iteration(2 * n, cycles, seed=21)
     assert np.array_equal(k0, np.array(ref))
+
+
+def test_bench_gpus_flag_launches_ranks():
+    """`bench.py --gpus 2` outside torchrun re-launches itself as 2 ranks (reference arm: runs on
+    CPU here); rank 0 alone prints the one JSON line, with n_gpus = 2."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK")}
+    p = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--impl", "reference", "--gpus", "2",
+                        "--steps", "1", "--warmup", "0", "--config", "c1", "--cpu-seconds", "0.5"],
+                       capture_output=True, text=True, timeout=300, env=env, cwd=root)
+    assert p.returncode == 0, p.stderr[-3000:]
+    lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, p.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["impl"] == "reference"
+    assert "launching 2 ranks" in p.stderr
