@@ -66,8 +66,8 @@ def lib():
             getattr(L, f).argtypes = [vp]
         L.orc_material_cell_ids.argtypes = [vp, dp]
         L.orc_cell_material.argtypes = [vp, i32]
-        L.orc_run.argtypes = [vp, u64, u64, u64, dp, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp, dp, dp]
-        L.orc_run_states.argtypes = [vp, u64, u64, u64, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp, dp, dp]
+        L.orc_run.argtypes = [vp, u64, u64, u64, dp, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp, dp, dp, dp, dp]
+        L.orc_run_states.argtypes = [vp, u64, u64, u64, dp, u64, i32, dp, dp, dp, u64, dp, dp, dp, dp, dp, dp, dp, dp]
         L.orc_set_fission.argtypes = [vp, i32, C.c_double]
         L.orc_max_sites.argtypes = [vp]
         L.orc_fission_source.argtypes = [vp, dp, dp, u64, u64, C.c_uint32, u64, dp]
@@ -116,6 +116,15 @@ def u01(h: int, l: int) -> float:
 
 def log(x: float) -> float:
     return lib().orc_log(x)
+
+
+def iso(xmu: float, xphi: float) -> np.ndarray:
+    """O15 isotropic direction of one (xi_mu, xi_phi) draw pair."""
+    L = lib()
+    L.orc_iso.argtypes = [C.c_double, C.c_double, C.c_void_p]
+    om = np.zeros(3)
+    L.orc_iso(xmu, xphi, _p(om))
+    return om
 
 
 def sincos2pi(xi: float):
@@ -208,7 +217,7 @@ class OracleModel:
     def run(self, n: int, seed: int = 240613849, pid_begin: int = 0, lo=None, hi=None,
             max_segments: int = 1_000_000, threads: int | None = None, pflags: bool = False,
             trace_cap: int = 0, states: np.ndarray | None = None, mesh: bool = False,
-            instances: bool = False, bank: bool = False):
+            instances: bool = False, bank: bool = False, per_history: bool = False):
         """Track particles [pid_begin, pid_begin+n).  Returns dict with out, counters, ...
         mesh=True (model spec with a "mesh"): res["mesh"] = per-voxel track length, x fastest.
         instances=True: res["inst"] = track length per material-cell instance (reading D1).
@@ -229,6 +238,9 @@ class OracleModel:
         bk = np.zeros((max(n, 1), ms, 3)) if bank else None
         bn = np.zeros(max(n, 1), dtype=np.uint8) if bank else None
         bargs = (_p(bk), _p(bn)) if bank else (None, None)
+        hn = np.zeros(max(n, 1), dtype=np.uint32) if per_history else None
+        ht = np.zeros(max(n, 1), dtype=np.uint8) if per_history else None
+        bargs = bargs + ((_p(hn), _p(ht)) if per_history else (None, None))
         if states is None:
             src = self.spec["source"]
             lo = np.asarray(src["lo"] if lo is None else lo, dtype=np.float64)
@@ -257,6 +269,8 @@ class OracleModel:
             res["bank"], res["bank_n"] = bk[:n], bn[:n]
         if pf is not None:
             res["pflags"] = pf[:n]
+        if per_history:
+            res["pnseg"], res["pterm"] = hn[:n], ht[:n]
         if tr is not None:
             cnt = int(tcount[0])
             assert cnt <= trace_cap, f"trace overflow {cnt} > {trace_cap}"

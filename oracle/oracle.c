@@ -841,6 +841,8 @@ typedef struct {
     double *bank;            /* optional fission sites (F1): [n][max_sites][3] */
     uint8_t *bank_n;         /*   sites banked by each history */
     int max_sites;
+    uint32_t *pnseg;         /* optional per-history segment count */
+    uint8_t *pterm;          /* optional per-history terminal (T_*) */
 } RunCtx;
 
 static void emit(const RunCtx *R, uint64_t pid, uint32_t seg, int kind, int level, int j, int cb,
@@ -1004,6 +1006,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
         flags |= (uint32_t)fl | F3;
         A->cnt[C_LOST]++;
         emit(R, pid, 0, EV_CROSS, -1, -1, -1, -1, 0.0, T_LOST, flags);
+        terminal = T_LOST;
         goto done;
     }
     flags |= (uint32_t)fl;
@@ -1020,6 +1023,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
         if (ds == INFINITY && dc == INFINITY) {                   /* nothing ahead: lost */
             flags |= F3; A->cnt[C_LOST]++;
             emit(R, pid, (uint32_t)nseg, EV_CROSS, -1, -1, cell, -1, 0.0, T_LOST, flags);
+            terminal = T_LOST;
             goto done;
         }
         if (ds < dc) {                                            /* Alg. 2 "while d < tau/Sigma" */
@@ -1035,6 +1039,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
             if (l == 0 && m->u[S[0].u].kind == U_CSG && m->s[j].bc == BC_VACUUM) {
                 A->exits[mc]++; A->cnt[C_CROSSINGS]++; A->cnt[C_LEAKS]++;
                 emit(R, pid, (uint32_t)(nseg - 1), EV_LEAK, 0, j, cell, -1, s, T_LEAKED, flags);
+                terminal = T_LEAKED;
                 goto done;
             }
             if (l == 0 && m->u[S[0].u].kind == U_CSG && m->s[j].bc == BC_REFLECT) {
@@ -1095,6 +1100,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
                 if (!ok) {
                     flags |= F3; A->cnt[C_LOST]++;
                     emit(R, pid, (uint32_t)(nseg - 1), EV_CROSS, l, j, cell, -1, s, T_LOST, flags);
+                    terminal = T_LOST;
                     goto done;
                 }
                 emit(R, pid, (uint32_t)(nseg - 1), EV_CROSS, l, j, cell, S[depth - 1].cell, s, T_NONE, flags);
@@ -1120,6 +1126,7 @@ static void walk(const RunCtx *R, uint64_t idx, Acc *A) {
                     R->bank_n[idx] = (uint8_t)ns;
                 }
                 emit(R, pid, (uint32_t)(nseg - 1), EV_COLLIDE, -1, -1, cell, cell, s, T_ABSORBED, flags);
+                terminal = T_ABSORBED;
                 goto done;
             }
             double xt = xb, xmu, xphi;
@@ -1139,13 +1146,15 @@ done:
     A->cnt[C_SEGMENTS] += nseg;
     if (flags) A->cnt[C_FLAGGED]++;
     if (R->pflags) R->pflags[idx] = (uint8_t)flags;
+    if (R->pnseg) R->pnseg[idx] = (uint32_t)nseg;
+    if (R->pterm) R->pterm[idx] = (uint8_t)terminal;
 }
 
 static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *lo,
                       const double *hi, const double *states, uint64_t max_seg, int nthreads,
                       double *out, uint8_t *pflags, void *trace, uint64_t trace_cap,
                       uint64_t *trace_count, uint64_t *evals, double *mesh_out, double *inst_out,
-                      double *bank, uint8_t *bank_n) {
+                      double *bank, uint8_t *bank_n, uint32_t *pnseg, uint8_t *pterm) {
     Model *m = vm;
     if (!m->finalized) return -1;
     RunCtx R;
@@ -1156,6 +1165,7 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
     R.mesh_out = m->mesh_on ? mesh_out : NULL;
     R.inst_out = inst_out;
     R.bank = bank; R.bank_n = bank_n; R.max_sites = orc_max_sites(m);
+    R.pnseg = pnseg; R.pterm = pterm;
     if (bank_n) memset(bank_n, 0, (size_t)n);
     const size_t ninst = inst_out ? (size_t)m->leaves[m->root] : 0;
     const size_t nbins = m->mesh_on ? (size_t)m->mesh_n[0] * m->mesh_n[1] * m->mesh_n[2] : 0;
@@ -1216,17 +1226,17 @@ static int run_common(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const 
 int orc_run(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *lo, const double *hi,
             uint64_t max_seg, int nthreads, double *out, uint8_t *pflags, void *trace,
             uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out,
-            double *inst_out, double *bank, uint8_t *bank_n) {
+            double *inst_out, double *bank, uint8_t *bank_n, uint32_t *pnseg, uint8_t *pterm) {
     return run_common(vm, seed, pid0, n, lo, hi, NULL, max_seg, nthreads, out, pflags, trace,
-                      trace_cap, trace_count, evals, mesh_out, inst_out, bank, bank_n);
+                      trace_cap, trace_count, evals, mesh_out, inst_out, bank, bank_n, pnseg, pterm);
 }
 
 int orc_run_states(void *vm, uint64_t seed, uint64_t pid0, uint64_t n, const double *states,
                    uint64_t max_seg, int nthreads, double *out, uint8_t *pflags, void *trace,
                    uint64_t trace_cap, uint64_t *trace_count, uint64_t *evals, double *mesh_out,
-                   double *inst_out, double *bank, uint8_t *bank_n) {
+                   double *inst_out, double *bank, uint8_t *bank_n, uint32_t *pnseg, uint8_t *pterm) {
     return run_common(vm, seed, pid0, n, NULL, NULL, states, max_seg, nthreads, out, pflags, trace,
-                      trace_cap, trace_count, evals, mesh_out, inst_out, bank, bank_n);
+                      trace_cap, trace_count, evals, mesh_out, inst_out, bank, bank_n, pnseg, pterm);
 }
 
 /* F1: source particles J = j_begin .. j_begin + n_next - 1 drawn from a flat site list (the
@@ -1333,6 +1343,9 @@ int orc_hex_owns(void *vm, int uid, int q, int r, const double *rl) {
     hex_t(&m->u[uid], rl, t);
     return hex_owns(q, r, t);
 }
+
+/* O15 direction of a scatter / birth draw pair, exposed for its statistical pins */
+void orc_iso(double xmu, double xphi, double *om) { iso(xmu, xphi, om); }
 
 int orc_ncount(void) { return NCOUNT; }
 int orc_trace_rec_size(void) { return (int)sizeof(TraceRec); }

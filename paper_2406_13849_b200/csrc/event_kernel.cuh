@@ -2,21 +2,27 @@
 // for sm_100a).
 //
 // Shift's GPU transport runs every tracking operation as a kernel over a masked vector of
-// histories.  Here one persistent block owns B particle slots (state in shared memory, SoA).
-// Each round, every live slot takes one EVENT and one MOVE, taken from ONE queue that is sorted
-// by event type: reflected slots (no event), change_direction (absorption or isotropic scatter,
-// P:399-409), find_cell / cross_surface descents (Alg. 7-8) at CSG levels, then at array levels,
-// then births into free slots (pid claims with a warp-aggregated atomic on the global counter).
-// A warp takes a consecutive 32-slot chunk, so a chunk is (almost always) one event type; the
-// same warp then runs MOVE on those slots: distance_to_boundary over all levels + collide-or-cross
-// + move_within_cell + track-length tally (Table 1, Alg. 2).  Each slot is appended to
-// the next round's queue of its next event with a ballot / popc / one shared atomic per warp.
-// One block barrier per round separates the rounds (queues are triple-buffered).
+// histories.  Here one persistent block owns S particle slots (state in shared memory, SoA) and
+// keeps them in per-event queues: reflected slots (no event), change_direction (absorption or
+// isotropic scatter), find_cell / cross_surface descents (Alg. 7-8) at CSG levels, then
+// at array levels, and free slots (births: pid claims with a warp-aggregated atomic on the global
+// counter).  A warp takes up to 32 slots of ONE queue, so it runs one event type at a time, and
+// then runs MOVE on the same slots: distance_to_boundary over all levels + collide-or-cross +
+// move_within_cell + track-length tally (Table 1, Alg. 2).  Each slot is then appended
+// to the queue of its next event with match.any / ballot / popc and one shared atomic per target.
 //
-// Every warp therefore executes one event type on 32 slots at a time instead of a mix of
-// divergent branches.  The per-level universe stack of each slot stays in shared memory between
-// stages; nothing round-trips through HBM.  Arithmetic is exactly the generic tracker's
-// (nt_geom.cuh, descend(), level_distances()), so results are bit-identical to it and to the oracle.
+// Two forms of the queues:
+//  * ASYNC (the default, `NT_ROUNDS` unset): each queue is a ring in shared memory with a head and
+//    a tail counter and no block barrier.  A warp reads the five heads, claims up to 32 entries of
+//    the fullest ring (CAS on its head), and publishes every slot it appends to a ring entry after
+//    a block fence (ring_publish).  S may exceed the thread count (320 slots for 256 threads), so a
+//    warp that finishes its chunk finds queued slots instead of waiting for other warps' chunks.
+//  * rounds (`NT_ROUNDS`): one queue set per round sorted by event type, warps take consecutive
+//    32-slot chunks, one block barrier per round, triple-buffered uint8 queues (S == B <= 256).
+//
+// The per-level universe stack of each slot stays in shared memory between stages; nothing
+// round-trips through HBM.  Arithmetic is exactly the generic tracker's (nt_geom.cuh, descend(),
+// level_distances()), so results are bit-identical to it and to the oracle.
 #pragma once
 
 NT_DEV_BEGIN
@@ -27,7 +33,8 @@ enum { Q_M = 0, Q_C = 1, Q_DC = 2, Q_DA = 3, Q_F = 4, NQ = 5 };
 #ifndef NT_RING_SLEEP_NS
 #define NT_RING_SLEEP_NS 64     // back-off of a warp that found every ring empty
 #endif
-using QIdx = uint8_t;           // slot index in a queue (blocks own <= 256 slots)
+using QIdx = uint8_t;           // rounds form: slot index in a queue (S == B <= 256 slots); the
+                                // ASYNC rings hold slot + 1 in uint16 entries (S <= 512)
 
 __device__ __forceinline__ int warp_append(bool pred, int* counter, int lane) {
   const unsigned m = __ballot_sync(0xffffffffu, pred);
@@ -64,6 +71,13 @@ __device__ __forceinline__ uint32_t vload(const uint32_t* p) { return *reinterpr
 __device__ __forceinline__ uint32_t vload(const uint16_t* p) { return *reinterpret_cast<const volatile uint16_t*>(p); }
 __device__ __forceinline__ void vstore(uint16_t* p, uint32_t v) {
   *reinterpret_cast<volatile uint16_t*>(p) = static_cast<uint16_t>(v);
+}
+// Publish `slot` into ring entry e (ASYNC form).  The entry's previous lap may still be unread, and
+// two producers a full lap apart map to the same entry, so the empty check and the write are one
+// shared-memory CAS: a producer can never overwrite an entry another producer filled.
+__device__ __forceinline__ void ring_publish(uint16_t* e, int slot) {
+  const unsigned short v = static_cast<unsigned short>(slot + 1);
+  while (atomicCAS(reinterpret_cast<unsigned short*>(e), static_cast<unsigned short>(0), v) != 0) {}
 }
 
 // DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh).
@@ -170,7 +184,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           uint32_t hk = 0, av = 0;
           if (lane < NQ && (lane != Q_F || births)) { hk = vload(a_head + lane); av = vload(a_tail + lane) - hk; }
           const uint32_t mx = __reduce_max_sync(0xffffffffu, (av << 8) | static_cast<uint32_t>(255 - lane));
-          const uint32_t bav = mx >> 8;                  // av <= ring size (256)
+          const uint32_t bav = mx >> 8;                  // av <= S slots (< 2^24): fits above the lane byte
           if (bav > 0u) {
             const int best = 255 - static_cast<int>(mx & 255u);
             const uint32_t bh = __shfl_sync(0xffffffffu, hk, best);
@@ -212,9 +226,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             base2 = __shfl_sync(0xffffffffu, base2, leader);
             if (pred) {
               __threadfence_block();                               // slot state before the entry
-              uint16_t* e = ring + qq * RB + ((base2 + __popc(m & ((1u << lane) - 1u))) & (RB - 1));
-              while (vload(e) != 0u) {}                            // previous lap consumed
-              vstore(e, static_cast<uint32_t>(slot) + 1u);
+              ring_publish(ring + qq * RB + ((base2 + __popc(m & ((1u << lane) - 1u))) & (RB - 1)), slot);
             }
           }
         } else {
@@ -233,9 +245,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
         base2 = __shfl_sync(0xffffffffu, base2, leader);
         if (qq >= 0) {
           __threadfence_block();                                   // slot state before the entry
-          uint16_t* e = ring + qq * RB + ((base2 + __popc(grp & ((1u << lane) - 1u))) & (RB - 1));
-          while (vload(e) != 0u) {}                                // previous lap consumed
-          vstore(e, static_cast<uint32_t>(slot) + 1u);
+          ring_publish(ring + qq * RB + ((base2 + __popc(grp & ((1u << lane) - 1u))) & (RB - 1)), slot);
         }
       };
       // ---------------- EVENT: change_direction / descent / birth of this chunk's slots

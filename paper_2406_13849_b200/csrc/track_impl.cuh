@@ -10,8 +10,10 @@
 // P:424-434, re-designed as a persistent history-based kernel — DESIGN.md).
 //
 // The per-level universe stack lives in shared memory (one slot per thread per level,
-// stride = blockDim, conflict-free); tallies are privatised per block in shared memory and
-// flushed once with fp64 global atomics.
+// stride = blockDim, conflict-free).  Tallies: exits and counters are u32
+// shared-memory atomics per block; track lengths go to the block's own fp64 slice in global
+// memory (RED.F64 at L2: a shared-memory fp64 atomicAdd would be a CAS loop), and the slices
+// and shared counters are flushed once per block at the end (flush_tallies).
 #include <cuda_runtime.h>
 
 #include <cstdint>

@@ -45,7 +45,7 @@ def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, t
     torch.cuda.synchronize()
     g = m.unpack(res["out"])
     o = om.run(n, seed=seed, pid_begin=pid_begin, pflags=True, trace_cap=cap, max_segments=max_segments,
-               states=states)
+               states=states, per_history=True)
     assert g["counters"] == o["counters"]
     assert np.array_equal(g["exits"], o["exits"])
     assert np.allclose(g["len"], o["len"], rtol=1e-12, atol=1e-300)
@@ -58,10 +58,11 @@ def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, t
         # per-segment tolerance of the contract, then the stronger bit-identity we reach
         assert np.all(np.abs(gt["s"] - ot["s"]) <= 1e-12 * np.abs(ot["s"]) + 1e-13)
         assert np.array_equal(gt["s"], ot["s"])
-        # per-history summaries agree with the trace
-        nseg = res["pnseg"].cpu().numpy()[:n]
-        cnt = np.bincount((gt["pid"] - pid_begin).astype(np.int64)[gt["kind"] <= 3], minlength=n)
-        assert nseg.sum() == g["counters"]["segments"]
+    # per-history segment counts and terminals equal the oracle's, history by history
+    nseg = res["pnseg"].cpu().numpy()[:n]
+    assert np.array_equal(nseg, o["pnseg"].astype(np.int32))
+    assert np.array_equal(res["pterm"].cpu().numpy()[:n], o["pterm"])
+    assert nseg.sum() == g["counters"]["segments"]
     return m, g, o, res
 
 

@@ -91,3 +91,52 @@ def test_exponential_mean(oracle_mod):
     n = len(taus)
     assert abs(taus.mean() - 1.0) < 4.0 / math.sqrt(n)
     assert abs(taus.var() - 1.0) < 4.0 * math.sqrt(8.0 / n)
+
+
+def _iso_draws(oracle_mod, n, seed=17):
+    """(xi_mu, xi_phi) of epoch-0 block 1 (O17) for pids 0..n-1."""
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    out = np.zeros((n, 2))
+    for pid in range(n):
+        x = oracle_mod.philox([pid, 0, 0, 1], key)
+        out[pid] = (oracle_mod.u01(int(x[0]), int(x[1])), oracle_mod.u01(int(x[2]), int(x[3])))
+    return out
+
+
+def test_iso_worked_values(oracle_mod):
+    """O15 closed forms: mu = 2 xi_mu - 1, phi = 2 pi xi_phi, Omega = (s cos phi, s sin phi, mu),
+    s = sqrt(1 - mu^2).  A phi = pi xi (or a swapped sin / cos, or a dropped s) fails these."""
+    h = math.sqrt(0.75)
+    cases = [((0.5, 0.0), (1.0, 0.0, 0.0)),
+             ((0.5, 0.25), (0.0, 1.0, 0.0)),
+             ((0.5, 0.5), (-1.0, 0.0, 0.0)),
+             ((0.5, 0.75), (0.0, -1.0, 0.0)),
+             ((0.75, 0.125), (h / math.sqrt(2.0), h / math.sqrt(2.0), 0.5)),
+             ((0.25, 0.625), (-h / math.sqrt(2.0), -h / math.sqrt(2.0), -0.5)),
+             ((0.75, 1.0 / 6.0), (h * 0.5, h * h, 0.5)),
+             ((1.0, 0.3), (0.0, 0.0, 1.0))]
+    for (xm, xp), want in cases:
+        got = oracle_mod.iso(xm, xp)
+        assert np.allclose(got, want, rtol=0, atol=4e-16), ((xm, xp), got, want)
+
+
+def test_iso_statistics(oracle_mod):
+    """O15 pins on Philox-drawn directions: |Omega| = 1, E[Omega] = 0 and E[Omega_i^2] = 1/3
+    (4 sigma; Var Omega_i = 1/3, Var Omega_i^2 = 1/5 - 1/9 = 4/45 on the unit sphere), and
+    Kolmogorov-Smirnov: mu = Omega_z ~ U(-1, 1), azimuth atan2(Omega_y, Omega_x) ~ U(-pi, pi),
+    and the azimuth in every octant-pair of mu is uniform too (no mu-phi coupling)."""
+    from scipy import stats
+    n = 20000
+    xi = _iso_draws(oracle_mod, n)
+    om = np.array([oracle_mod.iso(a, b) for a, b in xi])
+    assert np.all(np.abs(np.linalg.norm(om, axis=1) - 1.0) <= 4e-16)
+    mean = om.mean(axis=0)
+    assert np.all(np.abs(mean) <= 4.0 * math.sqrt(1.0 / 3.0 / n)), mean
+    sq = (om ** 2).mean(axis=0)
+    assert np.all(np.abs(sq - 1.0 / 3.0) <= 4.0 * math.sqrt(4.0 / 45.0 / n)), sq
+    assert stats.kstest(om[:, 2], stats.uniform(loc=-1.0, scale=2.0).cdf).pvalue > 1e-3
+    phi = np.arctan2(om[:, 1], om[:, 0])
+    assert stats.kstest(phi, stats.uniform(loc=-math.pi, scale=2.0 * math.pi).cdf).pvalue > 1e-3
+    for lo, hi in ((-1.0, -0.5), (-0.5, 0.0), (0.0, 0.5), (0.5, 1.0)):
+        sel = (om[:, 2] >= lo) & (om[:, 2] < hi)
+        assert stats.kstest(phi[sel], stats.uniform(loc=-math.pi, scale=2.0 * math.pi).cdf).pvalue > 1e-4

@@ -196,3 +196,28 @@ def test_seed_changes_walks(oracle_mod):
     a = m.run(200, seed=1)
     b = m.run(200, seed=2)
     assert a["counters"]["segments"] != b["counters"]["segments"]
+
+
+@pytest.mark.parametrize("cfg", ["c1", "c3", "c4"])
+def test_per_history_outputs_match_trace(oracle_mod, cfg):
+    """The oracle's per-history segment count and terminal equal what its own trace records say
+    (last record's seg + 1; its terminal) and add up to the counters."""
+    spec, _ = workloads.config(cfg)
+    om = oracle_mod.OracleModel.from_spec(spec)
+    n = 400
+    r = om.run(n, seed=5, pid_begin=77, per_history=True, trace_cap=400 * n, max_segments=60)
+    tr = r["trace"]
+    idx = (tr["pid"] - 77).astype(np.int64)
+    last = np.zeros(n, dtype=np.int64)
+    term = np.zeros(n, dtype=np.int64)
+    last[idx] = tr["seg"]
+    term[idx] = tr["terminal"]
+    capped = term == 4
+    # a capped history's extra CAPPED record carries seg == nseg; every other last record is seg nseg-1
+    assert np.array_equal(r["pnseg"].astype(np.int64), np.where(capped, last, last + 1))
+    assert np.array_equal(r["pterm"].astype(np.int64), term)
+    c = r["counters"]
+    assert int(r["pnseg"].sum()) == c["segments"]
+    assert [int((r["pterm"] == t).sum()) for t in (1, 2, 3, 4)] == \
+        [c["absorptions"], c["leaks"], c["lost"], c["capped"]]
+    assert c["capped"] > 0 and np.all(r["pterm"] > 0)

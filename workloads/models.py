@@ -579,6 +579,74 @@ def rect3d_small() -> dict:
     return sp.to_dict()
 
 
+# ---------------------------------------------------------------------------
+# O13 / O16 test models: near-coincident surfaces (PAPER.md:554-556 removes coincident lower-level
+# surfaces in preprocessing; this build keeps them and flags histories that come within 1e-10 cm)
+# ---------------------------------------------------------------------------
+NEAR_GAP = 5e-11           # cm: second surface this far inside the first (O16 flags fire at <= 1e-10)
+NEAR_BODY = 0.3            # body radius / plane offset (cm); 2R != 1 so the 2R scale of the tolerance shows
+NEAR_PLANE_N = (1.0, 2.0, 2.0)   # |n| = 3: exercises the 1e-10 |n| tolerance of an unnormalised PLANE
+
+
+def near_coincident(kind: str = "CZ", gap: float = NEAR_GAP, void: bool = False,
+                    body=(0.5, 0.05), outside=(0.3, 0.03)) -> dict:
+    """A body bounded by surface S inside a vacuum box [-1, 1]^3; the outside cell also carries a
+    second surface S' lying `gap` cm inside S (a redundant half-space: outside S implies outside
+    S').  Leaving the body through S lands `gap` from S' (O16 F1 on the new cell); entering it
+    meets S and then S' about `gap` further on (F2).  kind: CZ (R = 0.3 about the z axis), SPHERE
+    (R = 0.3 about the origin) or PLANE (n = (1, 2, 2), n.r = 0.9: the body is n.r < 0.9).
+    void=True: both materials void (deterministic rays)."""
+    sp = Spec(f"near_{kind.lower()}" + ("_void" if void else "") + ("" if gap == NEAR_GAP else f"_{gap:g}"))
+    root = sp.csg("root")
+    box = _box(sp, (-1.0, -1.0, -1.0), (1.0, 1.0, 1.0), "vacuum")
+    R = NEAR_BODY
+    if kind == "CZ":
+        s0 = sp.surf("CZ", [0.0, 0.0, R])
+        s1 = sp.surf("CZ", [0.0, 0.0, R - gap])
+    elif kind == "SPHERE":
+        s0 = sp.surf("SPHERE", [0.0, 0.0, 0.0, R])
+        s1 = sp.surf("SPHERE", [0.0, 0.0, 0.0, R - gap])
+    else:
+        nn = NEAR_PLANE_N
+        norm = math.sqrt(sum(v * v for v in nn))
+        s0 = sp.surf("PLANE", [nn[0], nn[1], nn[2], norm * R])
+        s1 = sp.surf("PLANE", [nn[0], nn[1], nn[2], norm * (R - gap)])
+    if void:
+        body, outside = (0.0, 0.0), (0.0, 0.0)
+    mb = sp.mat("body", *body)
+    mo = sp.mat("outside", *outside)
+    sp.cell(root, box + [-(s0 + 1)], material=mb)
+    sp.cell(root, box + [s0 + 1, s1 + 1], material=mo)
+    sp.root = root
+    sp.source = {"lo": [-1.0, -1.0, -1.0], "hi": [1.0, 1.0, 1.0]}
+    return sp.to_dict()
+
+
+def grazing_lattice(gap: float = NEAR_GAP, void: bool = False) -> dict:
+    """3x3 pin lattice (pitch 1.25, reflective box on the lattice edges) whose pin universe splits
+    the moderator with a PX plane `gap` cm inside the tile's +x wall: a CSG surface grazing a lattice
+    wall one level up.  Moving +x in the moderator, the plane and the wall are `gap`/u apart (F2
+    across levels); entering a tile through its +x wall descends `gap` from the plane (F1)."""
+    sp = Spec("grazing_lattice" + ("_void" if void else "") + ("" if gap == NEAR_GAP else f"_{gap:g}"))
+    root = sp.csg("root")
+    p = 1.25
+    ll = -1.5 * p
+    box = _box(sp, (ll, ll, 0.0), (-ll, -ll, 10.0), "reflect")
+    mats = _pwr_materials(sp, uniform=(0.0, 0.0) if void else None)
+    pin = sp.csg("pin")
+    cz = [sp.surf("CZ", [0.0, 0.0, r]) for r in (0.4096, 0.475)]
+    px = sp.surf("PX", [0.5 * p - gap])
+    sp.cell(pin, [-(cz[0] + 1)], material=mats["uo2"])
+    sp.cell(pin, [cz[0] + 1, -(cz[1] + 1)], material=mats["zr"])
+    sp.cell(pin, [cz[1] + 1, -(px + 1)], material=mats["water"])
+    sp.cell(pin, [cz[1] + 1, px + 1], material=mats["water"])
+    lat = sp.rect("lat", (ll, ll, 0.0), (p, p, 0.0), (3, 3, 1), [pin] * 9, None)
+    sp.cell(root, box, fill=lat)
+    sp.root = root
+    sp.source = {"lo": [ll, ll, 0.0], "hi": [-ll, -ll, 10.0]}
+    return sp.to_dict()
+
+
 CONFIGS = {
     "c1": (c1_pincell, 10_000),
     "c2": (c2_assembly, 10_000_000),
