@@ -67,7 +67,9 @@ typedef enum { NT_BC_NONE = 0, NT_BC_VACUUM = 1, NT_BC_REFLECT = 2 } nt_bc;
 typedef enum { NT_FILL_MATERIAL = 0, NT_FILL_UNIVERSE = 1 } nt_fill_kind;
 typedef enum { NT_HEX_POINTY = 0, NT_HEX_FLAT = 1 } nt_hex_orient;
 /* GENERIC: any nesting of CSG (BIH), rect and hex universes.  RECT: the
- * rect-specialised comparison tracker of §3.3 (Alg. 9-10). */
+ * rect-specialised comparison tracker of §3.3 (Alg. 9-10).  The rect tracker runs on
+ * the ring event queues by default (the generic tracker's default scheduler, so the two compare
+ * like for like) or history-based with NT_HISTORY; NT_WARPQ / NT_ROUNDS / NT_DP with it: NT_E_ARG. */
 typedef enum { NT_TRACKER_GENERIC = 0, NT_TRACKER_RECT = 1 } nt_tracker;
 
 /* nt_run.flags */

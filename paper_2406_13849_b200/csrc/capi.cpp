@@ -336,6 +336,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     coef_table(coef);
     if (e == cudaSuccess) e = f0::upload_coefficients(coef, 30);
     if (e == cudaSuccess) e = f7::upload_coefficients(coef, 30);
+    if (e == cudaSuccess) e = f0r::upload_coefficients(coef, 30);
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_err(e, "nt_finalize: upload");
     char* b = static_cast<char*>(m->blob);
@@ -517,6 +518,9 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
     return err(NT_E_ARG, std::string(who) + ": bad tracker");
   if (run->tracker == NT_TRACKER_RECT && !m->F.rect_ok)
     return err(NT_E_UNSUPPORTED, std::string(who) + ": model is not rect-specialisable: " + m->F.rect_why);
+  if (run->tracker == NT_TRACKER_RECT && (run->flags & (NT_WARPQ | NT_ROUNDS | NT_DP)))
+    return err(NT_E_ARG, std::string(who) + ": the rect tracker runs on the ring queues (default) or history-based "
+               "(NT_HISTORY)");
   if (run->max_segments > 0xFFFFFFFFull) return err(NT_E_ARG, std::string(who) + ": max_segments >= 2^32");
   const int block = run->block_dim > 0 ? run->block_dim : 256;
   if (block % 32 || block > 256) return err(NT_E_ARG, std::string(who) + ": block_dim must be a multiple of 32, <= 256");
@@ -589,8 +593,10 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
   int grid = 0;
   if (e == cudaSuccess) {
     const bool st = d_states != nullptr, f0 = m->g.features == 0;
-    if (run->tracker == NT_TRACKER_RECT)
+    if (run->tracker == NT_TRACKER_RECT && (run->flags & NT_HISTORY))
       e = f0::launch_rect(m->g, m->rg, R, trace, st, block, run->blocks_per_sm, s, &grid);
+    else if (run->tracker == NT_TRACKER_RECT)
+      e = f0r::launch_rect_event(m->g, m->rg, R, trace, st, run->blocks_per_sm, s, &grid);
     else if (run->flags & NT_HISTORY)
       e = f0 ? f0::launch_generic(m->g, R, trace, st, block, run->blocks_per_sm, s, &grid)
              : f7::launch_generic(m->g, R, trace, st, block, run->blocks_per_sm, s, &grid);

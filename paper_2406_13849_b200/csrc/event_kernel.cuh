@@ -89,9 +89,12 @@ __device__ __forceinline__ void ring_publish(uint16_t* e, int slot) {
 // ends when the pids are exhausted and no history is live.
 // S = particle slots per block (ASYNC only: S may exceed B, so that a warp finishing its chunk finds
 // other slots queued instead of waiting for the chunks other warps hold; rounds need S == B).
-template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false, int S = B>
-__global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGeom g, const KRun R) {
+// RTK = 0: generic tracker; 1 / 2: the rect-specialised tracker (rect_geom.cuh, Alg. 9-10) with a box /
+// CZ-annuli root, run by the same scheduler (rg describes the model; unused when RTK = 0).
+template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false, int S = B, int RTK = 0>
+__global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGeom g, const KRun R, const RectGeom rg) {
   static_assert(ASYNC || S == B, "round-based queues need one slot per thread");
+  static_assert(RTK == 0 || (!DP && !(TALLY & 2)), "RTK: SP dispatch, no instance tallies");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmc = g.n_mc, maxd = g.max_depth;
@@ -360,6 +363,15 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           }
           if constexpr (DP) ok = du >= 0 && descend_dp(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh >= 0 ? hs_sid(ld(&g.hsr[fh].e)) : -1,
                                                        fsense, L, mc, flags);
+          else if constexpr (RTK != 0) {
+            // RTK: a CSG crossing's key is the surface id itself; an array step stores the new
+            // tile's daughter and frame, then the unrolled descent continues below it
+            if (kind == 1 && du >= 0) {
+              st.set_u(l0, du, l0 <= rg.K ? U_RECT : U_CSG);
+              st.setT(l0, 0, Tx); st.setT(l0, 1, Ty); st.setT(l0, 2, Tz);
+            }
+            ok = du >= 0 && rect_descend<RTK == 1>(g, rg, st, l0, fh, fsense, rx, ry, rz, L, mc, flags);
+          }
           else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh, fsense, L, mc, flags);
           done = true;
           if (!ok) flags |= NT_F3;
@@ -415,9 +427,13 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
           } else {
             Best b;
             b.init();
-            for (int l = 0; l < L; ++l) {
-              if constexpr (DP) level_distances_dp(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
-              else level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+            if constexpr (RTK != 0) {
+              rect_distances<RTK == 1>(g, rg, st, L, rx, ry, rz, u, v, w, os_l, os_s, b);
+            } else {
+              for (int l = 0; l < L; ++l) {
+                if constexpr (DP) level_distances_dp(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+                else level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+              }
             }
             const double sig = ld(g.mc_st + mc);
             const double ds = b.d;
@@ -444,9 +460,11 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
                 const double tt = tau - sig * s;
                 tau = tt > 0.0 ? tt : 0.0;
                 const int l = b.l(), jb = b.j();
-                const int uk = st.ukind(l);
-                int meta;
-                const int j = winner_surface(g, uk == U_CSG, jb, meta);
+                const bool csg_l = RTK != 0 ? (l == 0 || l == rg.K + 1) : st.ukind(l) == U_CSG;
+                int meta = 0;
+                int j = jb;
+                if constexpr (RTK != 0) meta = l == 0 ? ld(g.surf_meta + jb) : 0;
+                else j = winner_surface(g, csg_l, jb, meta);
                 const int bc = l == 0 ? meta >> 4 : 0;
                 if (bc == NT_BC_VACUUM) {
                   atomicAdd(s_exit + mc, 1u);
@@ -464,7 +482,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
                 } else {
                   atomicAdd(s_exit + mc, 1u);
                   lcross = l;
-                  if (uk == U_CSG) {
+                  if (csg_l) {
                     sdesc[slot] = l | ((b.sense() ^ 1) << 4) | ((jb + 1) << 5);
                     os_l = l; os_s = j;
                     outc = 3;

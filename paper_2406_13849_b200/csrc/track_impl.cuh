@@ -458,6 +458,7 @@ __global__ void __launch_bounds__(256, 3) k_track_generic(const DevGeom g, const
 
 NT_DEV_END
 #include "dp_tracker.cuh"
+#include "rect_geom.cuh"
 #include "event_kernel.cuh"
 #include "wq_kernel.cuh"
 #if NT_FEAT == 0
@@ -465,6 +466,7 @@ NT_DEV_END
 #endif
 NT_DEV_BEGIN
 
+#ifndef NT_RECT_TU
 // point location for unit parity (Alg. 7)
 __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const double* xyz, uint64_t n,
                                                     int32_t* cell_out, uint8_t* flag_out) {
@@ -482,6 +484,8 @@ __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const doubl
     if (flag_out) flag_out[i] = static_cast<uint8_t>(fl | (ok ? 0u : NT_F3));
   }
 }
+
+#endif  // !NT_RECT_TU
 
 // ---------------------------------------------------------------- host launchers
 size_t generic_smem_bytes(const DevGeom& g, int block) {
@@ -503,6 +507,70 @@ static cudaError_t with_slices(const DevGeom& g, KRun R, uint64_t grid, cudaStre
 cudaError_t upload_coefficients(const double* host, int n) {
   return cudaMemcpyToSymbol(c_coef, host, sizeof(double) * n);
 }
+
+// Slots per block of the ring scheduler (block 256, SP): 320 when three such blocks still fit an SM
+// (a warp that finishes its chunk then finds queued slots instead of waiting for the chunks the
+// other seven warps hold), else 256.  NESTRACK_SLOTS=256|320 overrides (tuning).
+static int ring_slots(const DevGeom& g, bool trace) {
+  static const int env = [] { const char* e = getenv("NESTRACK_SLOTS"); return e ? atoi(e) : 0; }();
+  if (env == 256 || env == 320) return env;
+  int dev = 0, smem_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+  const size_t need = 3 * (event_smem_bytes(g, 320, trace, true) + 1024);
+  return need <= (size_t)smem_sm ? 320 : 256;
+}
+
+// persistent launch of a ring / event-queue kernel: grid = SMs x occupancy (capped by the batch)
+template <class Kern>
+static cudaError_t launch_event_kernel(Kern kern, const DevGeom& g, const RectGeom& rg, const KRun& R, int block,
+                                       size_t smem, int blocks_per_sm, cudaStream_t stream, int* grid_out) {
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, occ = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
+  if (e != cudaSuccess) return e;
+  if (occ < 1) return cudaErrorInvalidConfiguration;
+  const int bps = blocks_per_sm > 0 ? (blocks_per_sm < occ ? blocks_per_sm : occ) : occ;
+  uint64_t need = (R.n + block - 1) / block, grid = (uint64_t)nsm * bps;
+  if (need < grid) grid = need ? need : 1;
+  *grid_out = (int)grid;
+  return with_slices(g, R, grid, stream, [&](const KRun& Rs) {
+    kern<<<(unsigned)grid, block, smem, stream>>>(g, Rs, rg);
+    return cudaGetLastError();
+  });
+}
+
+#ifdef NT_RECT_TU
+// Rect-specialised tracker (Alg. 9-10) under the ring scheduler: the same k_track_event as the
+// generic tracker, with the RTK's find_cell / distance code (rect_geom.cuh).  320 slots per block
+// when three blocks fit an SM (depth <= 4), else 256; trace and mesh runs use 256.
+cudaError_t launch_rect_event(const DevGeom& g, const RectGeom& rg, const KRun& R, bool trace, bool states,
+                              int blocks_per_sm, cudaStream_t stream, int* grid_out) {
+  if (R.inst) return cudaErrorNotSupported;
+  const bool mesh = R.mesh != nullptr;
+  if (mesh && trace) return cudaErrorNotSupported;
+  const bool s320 = !trace && !mesh && ring_slots(g, false) == 320;
+  const size_t smem = event_smem_bytes(g, s320 ? 320 : 256, trace, true);
+  auto go = [&](auto kern) {
+    return launch_event_kernel(kern, g, rg, R, 256, smem, blocks_per_sm, stream, grid_out);
+  };
+  auto pick = [&](auto box) -> cudaError_t {
+    constexpr int RT = decltype(box)::value ? 1 : 2;
+    if (mesh) return states ? go(k_track_event<256, false, true, false, 1, true, 256, RT>)
+                            : go(k_track_event<256, false, false, false, 1, true, 256, RT>);
+    if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 256, RT>)
+                             : go(k_track_event<256, true, false, false, 0, true, 256, RT>);
+    if (s320) return states ? go(k_track_event<256, false, true, false, 0, true, 320, RT>)
+                            : go(k_track_event<256, false, false, false, 0, true, 320, RT>);
+    return states ? go(k_track_event<256, false, true, false, 0, true, 256, RT>)
+                  : go(k_track_event<256, false, false, false, 0, true, 256, RT>);
+  };
+  return rg.root_box ? pick(std::true_type{}) : pick(std::false_type{});
+}
+#else
 
 cudaError_t launch_generic(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
                            int blocks_per_sm, cudaStream_t stream, int* grid_out) {
@@ -593,39 +661,12 @@ cudaError_t launch_rect(const DevGeom&, const RectGeom&, const KRun&, bool, bool
 }
 #endif
 
-// Slots per block of the ring scheduler (block 256, SP): 320 when three such blocks still fit an SM
-// (a warp that finishes its chunk then finds queued slots instead of waiting for the chunks the
-// other seven warps hold), else 256.  NESTRACK_SLOTS=256|320 overrides (tuning).
-static int ring_slots(const DevGeom& g, bool trace) {
-  static const int env = [] { const char* e = getenv("NESTRACK_SLOTS"); return e ? atoi(e) : 0; }();
-  if (env == 256 || env == 320) return env;
-  int dev = 0, smem_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  const size_t need = 3 * (event_smem_bytes(g, 320, trace, true) + 1024);
-  return need <= (size_t)smem_sm ? 320 : 256;
-}
-
 cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
                          int blocks_per_sm, cudaStream_t stream, int* grid_out, bool async) {
   size_t smem = event_smem_bytes(g, block, trace, async);
+  const RectGeom no_rg{};
   auto go = [&](auto kern) -> cudaError_t {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    int dev = 0, nsm = 0, occ = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, block, smem);
-    if (e != cudaSuccess) return e;
-    if (occ < 1) return cudaErrorInvalidConfiguration;
-    const int bps = blocks_per_sm > 0 ? (blocks_per_sm < occ ? blocks_per_sm : occ) : occ;
-    uint64_t need = (R.n + block - 1) / block, grid = (uint64_t)nsm * bps;
-    if (need < grid) grid = need ? need : 1;
-    *grid_out = (int)grid;
-    return with_slices(g, R, grid, stream, [&](const KRun& Rs) {
-      kern<<<(unsigned)grid, block, smem, stream>>>(g, Rs);
-      return cudaGetLastError();
-    });
+    return launch_event_kernel(kern, g, no_rg, R, block, smem, blocks_per_sm, stream, grid_out);
   };
   const int tally = (R.mesh ? 1 : 0) | (R.inst ? 2 : 0);
   if (tally && trace) return cudaErrorNotSupported;
@@ -895,4 +936,5 @@ cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, i
   return cudaGetLastError();
 }
 
+#endif  // NT_RECT_TU
 NT_DEV_END

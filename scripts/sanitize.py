@@ -21,13 +21,13 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", default="c1")
     ap.add_argument("--n", type=int, default=200000)
-    ap.add_argument("--scheds", default="block,rounds,warp,history,dp,rect")
+    ap.add_argument("--scheds", default="block,rounds,warp,history,dp,rect,rect-ring")
     ap.add_argument("--blocks-per-sm", type=int, default=0)
     a = ap.parse_args()
     spec, _ = workloads.config(a.cfg)
     m = nt.Model.from_spec(spec, device=0)
     for s in a.scheds.split(","):
-        tracker, sched = ("rect", "history") if s == "rect" else ("generic", s)
+        tracker, sched = {"rect": ("rect", "history"), "rect-ring": ("rect", "block")}.get(s, ("generic", s))
         res = m.track(a.n, seed=7, pflags=True, per_history=True, scheduler=sched, tracker=tracker,
                       blocks_per_sm=a.blocks_per_sm)
         torch.cuda.synchronize()

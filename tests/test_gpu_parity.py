@@ -66,6 +66,9 @@ def _compare(nt, orc, spec, n, seed, pid_begin=0, max_segments=0, states=None, t
     return m, g, o, res
 
 
+# the rect-specialised tracker: history-based ("rect") and on the ring event queues ("rect-ring")
+RECT_KW = {"rect": dict(tracker="rect", scheduler="history"), "rect-ring": dict(tracker="rect", scheduler="block")}
+
 CONFIG_N = {"c1": 2000, "c2": 600, "c3": 600, "c4": 600, "c5m": 600, "c5r": 600}
 
 
@@ -160,18 +163,18 @@ MESHED = {
 }
 
 
-@pytest.mark.parametrize("sched", ["block", "warp", "history", "dp", "rounds", "rect"])
+@pytest.mark.parametrize("sched", ["block", "warp", "history", "dp", "rounds", "rect", "rect-ring"])
 @pytest.mark.parametrize("name", list(MESHED))
 def test_mesh_tally_parity(nt, orc, name, sched):
     """Superimposed mesh track-length tally (NEXT-2, reading M1): per-voxel totals vs the oracle's
     sort-the-cuts definition, within 1e-9 relative (summation order), under every scheduler."""
     spec = MESHED[name]()
     m = nt.Model.from_spec(spec, device=0)
-    if sched == "rect" and not m.info["rect_specialisable"]:
+    if sched.startswith("rect") and not m.info["rect_specialisable"]:
         pytest.skip("not rect-specialisable")
     om = orc.OracleModel.from_spec(spec)
     n = 400
-    kw = dict(tracker="rect", scheduler="history") if sched == "rect" else dict(scheduler=sched)
+    kw = RECT_KW.get(sched, dict(scheduler=sched))
     res = m.track(n, seed=4, mesh=True, **kw)
     torch.cuda.synchronize()
     o = om.run(n, seed=4, mesh=True)
@@ -250,7 +253,7 @@ FISSILE = {
 }
 
 
-@pytest.mark.parametrize("sched", ["block", "rounds", "warp", "history", "dp", "rect"])
+@pytest.mark.parametrize("sched", ["block", "rounds", "warp", "history", "dp", "rect", "rect-ring"])
 @pytest.mark.parametrize("cfg", list(FISSILE))
 def test_fission_bank_parity(nt, orc, cfg, sched):
     """F1 fission bank: sites per history and site coordinates bit-exact vs the oracle."""
@@ -259,7 +262,7 @@ def test_fission_bank_parity(nt, orc, cfg, sched):
     om = orc.OracleModel.from_spec(spec)
     assert m.info["max_sites"] == om.max_sites()
     n = 700
-    kw = dict(tracker="rect", scheduler="history") if sched == "rect" else dict(scheduler=sched)
+    kw = RECT_KW.get(sched, dict(scheduler=sched))
     res = m.track(n, seed=12, bank=True, **kw)
     torch.cuda.synchronize()
     o = om.run(n, seed=12, bank=True)
@@ -467,21 +470,24 @@ def test_full_size_c3_sampled(nt, orc):
 
 
 @pytest.mark.parametrize("cfg", ["c1", "c2", "c3", "c5r"])
-def test_rect_tracker_bit_identical(nt, orc, cfg):
-    """P13: the rect-specialised tracker (Alg. 9-10 analogue) reproduces the generic tracker
-    and the oracle bit for bit on every rect-shaped config."""
+@pytest.mark.parametrize("sched", ["history", "block"])
+def test_rect_tracker_bit_identical(nt, orc, cfg, sched):
+    """P13: the rect-specialised tracker (Alg. 9-10 analogue), history-based and on the ring event
+    queues, reproduces the generic tracker and the oracle bit for bit on every rect-shaped config."""
     spec, _ = workloads.config(cfg)
-    _compare(nt, orc, spec, 600, seed=8, tracker="rect")
+    _compare(nt, orc, spec, 600, seed=8, tracker="rect", scheduler=sched)
+    _compare(nt, orc, spec, 40, seed=9, tracker="rect", scheduler=sched, max_segments=25)
 
 
 def test_rect_tracker_full_counters_match_generic(nt):
     spec, _ = workloads.config("c3")
     m = nt.Model.from_spec(spec, device=0)
     a = m.unpack(m.track(300000, seed=13)["out"])
-    b = m.unpack(m.track(300000, seed=13, tracker="rect")["out"])
-    assert a["counters"] == b["counters"]
-    assert np.array_equal(a["exits"], b["exits"])
-    assert np.allclose(a["len"], b["len"], rtol=1e-11, atol=0)
+    for sched in ("history", "block"):
+        b = m.unpack(m.track(300000, seed=13, tracker="rect", scheduler=sched)["out"])
+        assert a["counters"] == b["counters"]
+        assert np.array_equal(a["exits"], b["exits"])
+        assert np.allclose(a["len"], b["len"], rtol=1e-11, atol=0)
 
 
 @pytest.mark.parametrize("cfg", ["c4", "c5m"])

@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 
 LARGE_N = {"c1": 2_000_000, "c2": 10_000_000, "c3": 10_000_000, "c4": 2_000_000, "c5m": 2_000_000,
            "c5r": 2_000_000}
-SCHEDS = ["block", "rounds", "warp", "history", "dp", "rect"]
+SCHEDS = ["block", "rounds", "warp", "history", "dp", "rect", "rect-ring"]
+RECT_KW = {"rect": dict(tracker="rect", scheduler="history"), "rect-ring": dict(tracker="rect", scheduler="block")}
 SEED = 77
 PID0 = 5_000_000_000          # pids above 2^32: the counter's high word is live
 
@@ -55,11 +56,11 @@ def _oracle_run(oracle_mod, cfg):
 def test_large_batch_tally_parity(nt, oracle_mod, cfg, sched):
     spec, _ = workloads.config(cfg)
     m = nt.Model.from_spec(spec, device=0)
-    if sched == "rect" and not m.info["rect_specialisable"]:
+    if sched.startswith("rect") and not m.info["rect_specialisable"]:
         pytest.skip("rect tracker: rect-only models (C1, C2, C3, C5r)")
     om, o_out, o_pf = _oracle_run(oracle_mod, cfg)
     n = LARGE_N[cfg]
-    kw = dict(tracker="rect", scheduler="history") if sched == "rect" else dict(scheduler=sched)
+    kw = RECT_KW.get(sched, dict(scheduler=sched))
     g_run = gpu_side(m, SEED, kw)
     o_full = oracle_side(om, SEED)
 
