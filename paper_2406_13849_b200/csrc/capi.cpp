@@ -51,6 +51,7 @@ struct nt_model {
   std::mutex host_mu;
   int last_launches = 0;
   void* dp_objs = nullptr;                  // DP dispatch: tracker objects + pointer table (lazy)
+  cudaMemPool_t pool = nullptr;             // per-launch scratch (stream-ordered), owned by the model
   bool mesh_on = false;                     // superimposed mesh (M1)
   double mesh_lo[3] = {0, 0, 0}, mesh_d[3] = {0, 0, 0};
   int32_t mesh_n[3] = {0, 0, 0};
@@ -90,16 +91,24 @@ nt_status nt_model_create(nt_model** out) {
   return NT_OK;
 }
 
+// frees every device resource of the model (on its device; the caller selects it)
+static void release_device(nt_model* m) {
+  if (m->blob) cudaFree(m->blob);
+  if (m->counters) cudaFree(m->counters);
+  if (m->host_scratch_dev) cudaFree(m->host_scratch_dev);
+  if (m->dp_objs) cudaFree(m->dp_objs);
+  if (m->pool) cudaMemPoolDestroy(m->pool);    // outstanding stream-ordered frees complete first
+  m->blob = nullptr; m->counters = nullptr; m->host_scratch_dev = nullptr; m->dp_objs = nullptr;
+  m->pool = nullptr;
+}
+
 void nt_model_destroy(nt_model* m) {
   if (!m) return;
-  if (m->blob || m->counters || m->host_scratch_dev || m->dp_objs) {
+  if (m->blob || m->counters || m->host_scratch_dev || m->dp_objs || m->pool) {
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(m->device);
-    if (m->blob) cudaFree(m->blob);
-    if (m->counters) cudaFree(m->counters);
-    if (m->host_scratch_dev) cudaFree(m->host_scratch_dev);
-    if (m->dp_objs) cudaFree(m->dp_objs);
+    release_device(m);
     cudaSetDevice(prev);
   }
   delete m;
@@ -319,16 +328,23 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     cudaGetDevice(&prev);
     cudaError_t e = cudaSetDevice(o->device);
     if (e != cudaSuccess) return cuda_err(e, "nt_finalize: cudaSetDevice");
-    {   // per-launch scratch is stream-ordered (cudaMallocAsync); let the device's default pool keep up
-        // to 64 MB across synchronisations instead of unmapping and remapping it every launch
-      cudaMemPool_t pool;
-      if (cudaDeviceGetDefaultMemPool(&pool, o->device) == cudaSuccess) {
-        uint64_t keep = 64ull << 20;
-        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-      }
+    {   // per-launch scratch is stream-ordered, from a memory pool the model owns (not the device's
+        // default pool, which other users of cudaMallocAsync share): it keeps up to 64 MB across
+        // synchronisations instead of unmapping and remapping the scratch every launch
+      cudaMemPoolProps props{};
+      props.allocType = cudaMemAllocationTypePinned;
+      props.location.type = cudaMemLocationTypeDevice;
+      props.location.id = o->device;
+      cudaMemPool_t pool = nullptr;
+      e = cudaMemPoolCreate(&pool, &props);
+      if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_err(e, "nt_finalize: cudaMemPoolCreate"); }
+      uint64_t keep = 64ull << 20;
+      e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+      if (e != cudaSuccess) { cudaMemPoolDestroy(pool); cudaSetDevice(prev); return cuda_err(e, "nt_finalize: pool"); }
+      m->pool = pool;
     }
     e = cudaMalloc(&m->blob, blob.size());
-    if (e != cudaSuccess) { cudaSetDevice(prev); return cuda_err(e, "nt_finalize: cudaMalloc"); }
+    if (e != cudaSuccess) { release_device(m); cudaSetDevice(prev); return cuda_err(e, "nt_finalize: cudaMalloc"); }
     e = cudaMemcpy(m->blob, blob.data(), blob.size(), cudaMemcpyHostToDevice);
     if (e == cudaSuccess) e = cudaMalloc(&m->counters, sizeof(unsigned long long) * kSlots);
     if (e == cudaSuccess) e = cudaMemset(m->counters, 0, sizeof(unsigned long long) * kSlots);
@@ -337,10 +353,12 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     if (e == cudaSuccess) e = f0::upload_coefficients(coef, 30);
     if (e == cudaSuccess) e = f7::upload_coefficients(coef, 30);
     if (e == cudaSuccess) e = f0r::upload_coefficients(coef, 30);
+    if (e != cudaSuccess) release_device(m);     // a failed finalize leaves nothing behind
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_err(e, "nt_finalize: upload");
     char* b = static_cast<char*>(m->blob);
     DevGeom& g = m->g;
+    g.pool = m->pool;
     g.surf = (const DSurf*)(b + o_surf);
     g.surf_tol = (const double*)(b + o_tol);
     g.surf_meta = (const uint8_t*)(b + o_meta);

@@ -107,6 +107,7 @@ struct DevGeom {
   int32_t root, n_mc, max_depth, n_univ;
   int32_t n_cells, n_surf, root_kind, features;   // features: F_* bits present in the model
   const void* const* trk;     // DP dispatch only: per-universe tracker object pointers (dp_tracker.cuh)
+  void* pool;                 // host use only: the model's own cudaMemPool_t for per-launch scratch
   double mesh_lo[3], mesh_d[3];   // superimposed mesh (M1): voxel edges lo + i d
   int32_t mesh_n[3], mesh_on;
   int32_t max_sites;              // F1: sites one absorption can bank

@@ -492,11 +492,22 @@ size_t generic_smem_bytes(const DevGeom& g, int block) {
   return (size_t)block * ((g.max_depth - 1) * 3 * 8 + g.max_depth * 4 * 4) + (kNC + (size_t)g.n_mc) * 4;
 }
 
+// stream-ordered scratch from the model's own memory pool (capi.cpp: nt_finalize creates it with a
+// 64 MB release threshold, so synchronised launches do not re-map it), else the device default pool
+template <class T>
+static cudaError_t scratch_alloc(const DevGeom& g, T** p, size_t bytes, cudaStream_t stream) {
+  void* v = nullptr;
+  const cudaError_t e = g.pool ? cudaMallocFromPoolAsync(&v, bytes, static_cast<cudaMemPool_t>(g.pool), stream)
+                               : cudaMallocAsync(&v, bytes, stream);
+  *p = static_cast<T*>(v);
+  return e;
+}
+
 // per-launch scratch: per-block track-length slices (stream-ordered allocation, zeroed)
 template <class Launch>
 static cudaError_t with_slices(const DevGeom& g, KRun R, uint64_t grid, cudaStream_t stream, Launch launch) {
   const size_t bytes = (size_t)grid * (size_t)g.n_mc * sizeof(double);
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&R.slices), bytes, stream);
+  cudaError_t e = scratch_alloc(g, &R.slices, bytes, stream);
   if (e != cudaSuccess) return e;
   e = cudaMemsetAsync(R.slices, 0, bytes, stream);
   if (e == cudaSuccess) e = launch(R);
@@ -874,7 +885,7 @@ cudaError_t bank_compact(const DevGeom& g, const double* bank, const uint8_t* ba
   if (n == 0) return cudaSuccess;
   const uint64_t nb = (n + kScanB - 1) / kScanB;
   unsigned long long* scratch = nullptr;             // sums[nb] | total | prefix[n]
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&scratch), (nb + 1 + n) * sizeof(unsigned long long), stream);
+  cudaError_t e = scratch_alloc(g, &scratch, (nb + 1 + n) * sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   unsigned long long *sums = scratch, *total = scratch + nb, *prefix = scratch + nb + 1;
   k_bank_block_sums<<<(unsigned)nb, kScanB, 0, stream>>>(bank_n, n, sums);
@@ -900,7 +911,7 @@ cudaError_t fission_source(const DevGeom& g, const double* bank, const uint8_t* 
   *M_host = 0;
   if (n_prev == 0) return cudaSuccess;
   double* sites = nullptr;
-  cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&sites), n_prev * (uint64_t)g.max_sites * 3 * sizeof(double), stream);
+  cudaError_t e = scratch_alloc(g, &sites, n_prev * (uint64_t)g.max_sites * 3 * sizeof(double), stream);
   if (e != cudaSuccess) return e;
   e = bank_compact(g, bank, bank_n, n_prev, sites, M_host, stream);
   if (e == cudaSuccess) e = source_from_sites(sites, *M_host, seed, cycle, 0, n_next, states, stream);
