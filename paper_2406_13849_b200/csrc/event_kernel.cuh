@@ -51,8 +51,10 @@ __device__ __forceinline__ void warp_count(bool pred, unsigned int* counter, int
   if (lane == 0 && m) atomicAdd(counter, (unsigned)__popc(m));
 }
 
-// ring capacity: the power of two >= the slot count (a slot is in at most one ring at a time)
-__host__ __device__ constexpr int ring_size(int S) { return S <= 128 ? 128 : S <= 256 ? 256 : 512; }
+// ring capacity: the smallest power of two ABOVE the slot count.  A slot is in at most one ring at
+// a time, so at most S positions of a ring are allocated and unclaimed (tail - head <= S); with
+// RB > S, two of them never share an entry (see ring_publish / ring_take).
+__host__ __device__ constexpr int ring_size(int S) { return S < 128 ? 128 : S < 256 ? 256 : 512; }
 
 size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false) {
   const size_t nmc = g.n_mc, d = g.max_depth;
@@ -72,12 +74,32 @@ __device__ __forceinline__ uint32_t vload(const uint16_t* p) { return *reinterpr
 __device__ __forceinline__ void vstore(uint16_t* p, uint32_t v) {
   *reinterpret_cast<volatile uint16_t*>(p) = static_cast<uint16_t>(v);
 }
-// Publish `slot` into ring entry e (ASYNC form).  The entry's previous lap may still be unread, and
-// two producers a full lap apart map to the same entry, so the empty check and the write are one
-// shared-memory CAS: a producer can never overwrite an entry another producer filled.
+// Ring entries (ASYNC form): 0 = empty, else slot + 1.  Position p of a ring maps to entry p mod RB,
+// so a producer (or consumer) of position p and one of p + RB can meet at the same entry when the
+// older party is slow.  Both sides therefore act with one shared-memory CAS:
+//  * ring_publish: empty -> slot + 1 (a producer never overwrites a value another producer put);
+//  * ring_take:    value -> empty (every value is taken by exactly one consumer).
+// A cell then holds at most one value at a time, and every value is consumed exactly once.  Two
+// positions of the same ring may swap values (a consumer of lap n + 1 can take lap n's value and
+// the lap-n consumer the next one), which is harmless: both wait for the same event.  Progress: a
+// producer waits only on a full cell, and the position holding that value has already been claimed
+// (otherwise more than S < RB positions of the ring would be pending, one per slot), so its
+// consumer lane is polling and takes it.  In detail, for one entry X: the allocated-but-unclaimed
+// positions of a ring lie in [head, tail), fewer than RB of them, so at most one maps to X.  With X
+// full, (claimed - taken) = (unpublished producers) - (unclaimed) + 1 >= 1: a claimed consumer of X
+// is still polling.  With X empty and a consumer polling, an allocated producer of X has not yet
+// published, and its CAS on the empty entry succeeds.
 __device__ __forceinline__ void ring_publish(uint16_t* e, int slot) {
   const unsigned short v = static_cast<unsigned short>(slot + 1);
   while (atomicCAS(reinterpret_cast<unsigned short*>(e), static_cast<unsigned short>(0), v) != 0) {}
+}
+__device__ __forceinline__ int ring_take(uint16_t* e) {
+  for (;;) {
+    const uint32_t v = vload(e);
+    if (v != 0u && atomicCAS(reinterpret_cast<unsigned short*>(e), static_cast<unsigned short>(v),
+                             static_cast<unsigned short>(0)) == v)
+      return static_cast<int>(v) - 1;
+  }
 }
 
 // DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh).
@@ -132,14 +154,14 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
 
   for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
-  if (tid < 3 * NQ) s_qn[tid] = 0;
+  if (tid < 3 * NQ) s_qn[tid] = (!ASYNC && tid == 0 * NQ + Q_F) ? B : 0;   // rounds: round 0 reads set 0, all free
   if (ASYNC) {
     for (int i = tid; i < NQ * RB; i += B) ring[i] = 0u;
     __syncthreads();
     for (int i = tid; i < S; i += B) ring[Q_F * RB + i] = static_cast<uint16_t>(i + 1);    // all slots free
     if (tid == 0) { a_tail[Q_F] = S; s_flag[0] = 0; s_flag[1] = 0; }
   } else {
-    if (tid == 0) { s_flag[0] = 0; s_qn[0 * NQ + Q_F] = B; }
+    if (tid == 0) s_flag[0] = 0;
     for (int i = tid; i < B; i += B) sq[(0 * NQ + Q_F) * B + i] = static_cast<QIdx>(i);   // round 0 reads set 0: all slots free
   }
   __syncthreads();
@@ -203,11 +225,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
         if (q < 0) break;
         valid = static_cast<uint32_t>(lane) < take;
         if (valid) {
-          uint16_t* e = ring + q * RB + ((h + lane) & (RB - 1));
-          uint32_t v;
-          while ((v = vload(e)) == 0u) {}
-          vstore(e, 0u);
-          slot = static_cast<int>(v) - 1;
+          slot = ring_take(ring + q * RB + ((h + lane) & (RB - 1)));
           kind = (0x21045 >> (4 * q)) & 15;          // Q_M, Q_C, Q_DC, Q_DA, Q_F -> kinds 5, 4, 0, 1, 2
         }
         __threadfence_block();
