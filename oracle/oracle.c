@@ -635,21 +635,22 @@ static double tile_centre(const Univ *U, int a, int i) {
     return U->e[a] ? nu_centre(U, a, i) : U->ll[a] + ((double)i + 0.5) * U->p[a];
 }
 
-/* hex t-space (O9) */
-static void hex_t(const Univ *U, const double rl[3], double t[3]) {
+/* hex s-space (reading O9): s_k = n_k . (x - C), the signed distance along face normal k in the
+ * lattice frame; tile (q, r) spans p (m_k - 1/2) <= s_k < p (m_k + 1/2) */
+static void hex_s(const Univ *U, const double rl[3], double t[3]) {
     double x = rl[0] - U->C[0], y = rl[1] - U->C[1];
-    for (int k = 0; k < 3; ++k) t[k] = (U->nrm[k][0] * x + U->nrm[k][1] * y) / U->pitch;
+    for (int k = 0; k < 3; ++k) t[k] = U->nrm[k][0] * x + U->nrm[k][1] * y;
 }
 static void hex_m(int q, int r, double mm[3]) {
     mm[0] = (double)q + (double)r * 0.5;
     mm[1] = (double)q * 0.5 + (double)r;
     mm[2] = -((double)q * 0.5) + (double)r * 0.5;
 }
-static int hex_owns(int q, int r, const double t[3]) {
+static int hex_owns(const Univ *U, int q, int r, const double t[3]) {
     double mm[3];
     hex_m(q, r, mm);
     for (int k = 0; k < 3; ++k)
-        if (!(mm[k] - 0.5 <= t[k] && t[k] < mm[k] + 0.5)) return 0;
+        if (!(U->pitch * (mm[k] - 0.5) <= t[k] && t[k] < U->pitch * (mm[k] + 0.5))) return 0;
     return 1;
 }
 /* cube rounding of fractional axial coords: the GPU-visible fallback tile (O9) */
@@ -703,20 +704,20 @@ static int locate(const Model *m, int u, const double rl[3], int fsid, int fsens
             o->t[a] = (a < na) ? tile_centre(U, a, ijk[a]) : 0.0;
     } else {
         double t[3];
-        hex_t(U, rl, t);
+        hex_s(U, rl, t);
         int qc, rc;
         hex_cube_round(U, rl, &qc, &rc);
         /* brute force: every tile in a window around the guess; the owner must be unique */
         int nown = 0, qo = 0, ro = 0;
         for (int dq = -3; dq <= 3; ++dq)
             for (int dr = -3; dr <= 3; ++dr)
-                if (hex_owns(qc + dq, rc + dr, t)) { nown++; qo = qc + dq; ro = rc + dr; }
+                if (hex_owns(U, qc + dq, rc + dr, t)) { nown++; qo = qc + dq; ro = rc + dr; }
         if (nown != 1) { qo = qc; ro = rc; *near |= F1; }
         double mm[3];
         hex_m(qo, ro, mm);
         for (int k = 0; k < 3; ++k)
-            if (U->pitch * fabs(t[k] - (mm[k] - 0.5)) <= FLAG_DIST ||
-                U->pitch * fabs(t[k] - (mm[k] + 0.5)) <= FLAG_DIST) *near |= F1;
+            if (fabs(t[k] - U->pitch * (mm[k] - 0.5)) <= FLAG_DIST ||
+                fabs(t[k] - U->pitch * (mm[k] + 0.5)) <= FLAG_DIST) *near |= F1;
         int kz = 0;
         if (U->nz > 0) {
             kz = rect_axis_index(U->zlo, U->zp, rl[2]);
@@ -793,13 +794,13 @@ static void level_distances(const Model *m, const Level *L, int l, const double 
         }
     } else {
         double t[3], mm[3];
-        hex_t(U, rl, t);
+        hex_s(U, rl, t);
         hex_m(L->i, L->j, mm);
         if (ev) ev[E_HEX]++;
         for (int k = 0; k < 3; ++k) {
             double g = U->nrm[k][0] * om[0] + U->nrm[k][1] * om[1];
-            if (g > 0.0) consider(b, clamp0((U->pitch * ((mm[k] + 0.5) - t[k])) / g), l, k);
-            else if (g < 0.0) consider(b, clamp0((U->pitch * ((mm[k] - 0.5) - t[k])) / g), l, k + 3);
+            if (g > 0.0) consider(b, clamp0((U->pitch * (mm[k] + 0.5) - t[k]) / g), l, k);
+            else if (g < 0.0) consider(b, clamp0((U->pitch * (mm[k] - 0.5) - t[k]) / g), l, k + 3);
         }
         if (U->nz > 0) {
             double w = om[2];
@@ -1336,12 +1337,12 @@ int orc_locate_array(void *vm, int uid, const double *rl, int32_t *ijk, int32_t 
     return ok;
 }
 
-/* unit: hex ownership test in t-space for tile (q, r) */
+/* unit: hex ownership test in s-space for tile (q, r) */
 int orc_hex_owns(void *vm, int uid, int q, int r, const double *rl) {
     Model *m = vm;
     double t[3];
-    hex_t(&m->u[uid], rl, t);
-    return hex_owns(q, r, t);
+    hex_s(&m->u[uid], rl, t);
+    return hex_owns(&m->u[uid], q, r, t);
 }
 
 /* O15 direction of a scatter / birth draw pair, exposed for its statistical pins */

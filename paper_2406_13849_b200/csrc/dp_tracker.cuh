@@ -112,7 +112,7 @@ struct HexTracker final : UnivTracker {
       const double gk = ld(&U->d[10 + 2 * k]) * u + ld(&U->d[11 + 2 * k]) * v;
       if (gk != 0.0) {
         const double bnd = gk > 0.0 ? mk[k] + 0.5 : mk[k] - 0.5;
-        b.consider(clamp0(fdiv(p * (bnd - tk[k]), gk)), l, gk > 0.0 ? k : k + 3, 0);
+        b.consider(clamp0(fdiv(p * bnd - tk[k], gk)), l, gk > 0.0 ? k : k + 3, 0);
       }
     }
     if (ld(&U->i1) > 0 && w != 0.0)

@@ -476,12 +476,13 @@ __device__ __forceinline__ int array_daughter(const DevGeom& g, const DUniv* U, 
   return idx >= 0 ? idx : ld(&U->outer);
 }
 
-// hex t-space coordinates t_k = (n_k . (x - C)) / p  (O9)
+// hex s-space coordinates s_k = n_k . (x - C) (reading O9): tile (q, r) spans
+// p (m_k - 1/2) <= s_k < p (m_k + 1/2); no division
 __device__ __forceinline__ void hex_t(const DUniv* U, double x, double y, double& t0, double& t1, double& t2) {
-  const double xp = x - ld(&U->d[0]), yp = y - ld(&U->d[1]), p = ld(&U->d[2]);
-  t0 = fdiv(ld(&U->d[10]) * xp + ld(&U->d[11]) * yp, p);
-  t1 = fdiv(ld(&U->d[12]) * xp + ld(&U->d[13]) * yp, p);
-  t2 = fdiv(ld(&U->d[14]) * xp + ld(&U->d[15]) * yp, p);
+  const double xp = x - ld(&U->d[0]), yp = y - ld(&U->d[1]);
+  t0 = ld(&U->d[10]) * xp + ld(&U->d[11]) * yp;
+  t1 = ld(&U->d[12]) * xp + ld(&U->d[13]) * yp;
+  t2 = ld(&U->d[14]) * xp + ld(&U->d[15]) * yp;
 }
 
 __device__ __forceinline__ void hex_m(int q, int r, double& m0, double& m1, double& m2) {
@@ -491,7 +492,7 @@ __device__ __forceinline__ void hex_m(int q, int r, double& m0, double& m1, doub
   m2 = -(qd * 0.5) + rd * 0.5;
 }
 
-// hex tile owning (x,y): cube rounding then fix-up moves in t-space (O9); falls back to the
+// hex tile owning (x,y): cube rounding then fix-up moves in s-space (O9); falls back to the
 // cube-rounded tile with F1 if the fix-up does not converge.  Sets F1 on proximity.
 __device__ __forceinline__ void hex_locate(const DUniv* U, double x, double y, int& qo, int& ro, uint32_t& flags) {
   const double xp = x - ld(&U->d[0]), yp = y - ld(&U->d[1]);
@@ -513,21 +514,21 @@ __device__ __forceinline__ void hex_locate(const DUniv* U, double x, double y, i
   for (int it = 0; it < 4; ++it) {
     double m0, m1, m2;
     hex_m(q, r, m0, m1, m2);
-    if (t0 < m0 - 0.5) { q -= 1; continue; }            // face 3: delta (-1, 0)
-    if (!(t0 < m0 + 0.5)) { q += 1; continue; }         // face 0: delta (+1, 0)
-    if (t1 < m1 - 0.5) { r -= 1; continue; }            // face 4: delta (0, -1)
-    if (!(t1 < m1 + 0.5)) { r += 1; continue; }         // face 1: delta (0, +1)
-    if (t2 < m2 - 0.5) { q += 1; r -= 1; continue; }    // face 5: delta (+1, -1)
-    if (!(t2 < m2 + 0.5)) { q -= 1; r += 1; continue; } // face 2: delta (-1, +1)
+    if (t0 < p * (m0 - 0.5)) { q -= 1; continue; }            // face 3: delta (-1, 0)
+    if (!(t0 < p * (m0 + 0.5))) { q += 1; continue; }         // face 0: delta (+1, 0)
+    if (t1 < p * (m1 - 0.5)) { r -= 1; continue; }            // face 4: delta (0, -1)
+    if (!(t1 < p * (m1 + 0.5))) { r += 1; continue; }         // face 1: delta (0, +1)
+    if (t2 < p * (m2 - 0.5)) { q += 1; r -= 1; continue; }    // face 5: delta (+1, -1)
+    if (!(t2 < p * (m2 + 0.5))) { q -= 1; r += 1; continue; } // face 2: delta (-1, +1)
     ok = true;
     break;
   }
   if (!ok) { q = qc; r = rc; flags |= 1u; }
   double m0, m1, m2;
   hex_m(q, r, m0, m1, m2);
-  if (p * fabs(t0 - (m0 - 0.5)) <= kFlagDist || p * fabs(t0 - (m0 + 0.5)) <= kFlagDist ||
-      p * fabs(t1 - (m1 - 0.5)) <= kFlagDist || p * fabs(t1 - (m1 + 0.5)) <= kFlagDist ||
-      p * fabs(t2 - (m2 - 0.5)) <= kFlagDist || p * fabs(t2 - (m2 + 0.5)) <= kFlagDist)
+  if (fabs(t0 - p * (m0 - 0.5)) <= kFlagDist || fabs(t0 - p * (m0 + 0.5)) <= kFlagDist ||
+      fabs(t1 - p * (m1 - 0.5)) <= kFlagDist || fabs(t1 - p * (m1 + 0.5)) <= kFlagDist ||
+      fabs(t2 - p * (m2 - 0.5)) <= kFlagDist || fabs(t2 - p * (m2 + 0.5)) <= kFlagDist)
     flags |= 1u;
   qo = q;
   ro = r;

@@ -187,7 +187,7 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
     for (int k = 0; k < 3; ++k) {
       const double gk = ld(&U->d[10 + 2 * k]) * u + ld(&U->d[11 + 2 * k]) * v;
       const double bnd = dsel(gk > 0.0, mk[k] + 0.5, mk[k] - 0.5);
-      b.consider(dsel(gk != 0.0, clamp0(fdiv(p * (bnd - tk[k]), gk)), NT_INF), l, gk > 0.0 ? k : k + 3, 0);
+      b.consider(dsel(gk != 0.0, clamp0(fdiv(p * bnd - tk[k], gk)), NT_INF), l, gk > 0.0 ? k : k + 3, 0);
     }
     if (ld(&U->i1) > 0)
       b.consider(dsel(w != 0.0, rect_wall(ld(&U->d[4]), ld(&U->d[5]), ic, z, w), NT_INF), l, w > 0.0 ? 7 : 6, 0);

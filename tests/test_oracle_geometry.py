@@ -291,3 +291,32 @@ def test_p16_partition(oracle_mod, cfg):
     pts = rng.uniform(lo, hi, size=(2000, 3)).T.copy()
     cells, fl = m.find_cells(pts)
     assert (cells >= 0).all()
+
+
+@pytest.mark.parametrize("orient", ["pointy", "flat"])
+@pytest.mark.parametrize("pitch", [2.0, 1.26, 9.0, 30.0])
+def test_o9_hex_faces_exact_partition(oracle_mod, orient, pitch):
+    """O9 s-space membership is an exact partition on faces: adjacent tiles compare s_k with the
+    same rounded bound p (m_k + 1/2), so a point on (or an ulp off) a shared face belongs to exactly
+    one tile of the window.  Points up to 0.28 p from the face's mid-point (the half side is p / (2 sqrt 3)
+    = 0.2887 p, so vertices are excluded)."""
+    C = (0.37, -0.21)
+    m, lat, pins, outer = _hex_model(oracle_mod, orient, pitch, C)
+    deltas = [(1, 0), (0, 1), (-1, 1), (-1, 0), (0, -1), (1, -1)]
+    rng = np.random.default_rng(11)
+    n = 0
+    for (q0, r0) in workloads.hex_tiles(3):
+        cx, cy = _hex_centre(orient, pitch, q0, r0, C)
+        for (dq, dr) in deltas:
+            nx, ny = _hex_centre(orient, pitch, q0 + dq, r0 + dr, C)
+            ux, uy = (nx - cx) / pitch, (ny - cy) / pitch
+            for a in rng.uniform(-0.28, 0.28, size=6) * pitch:
+                x = cx + 0.5 * pitch * ux - a * uy
+                y = cy + 0.5 * pitch * uy + a * ux
+                for xx in (x, np.nextafter(x, np.inf), np.nextafter(x, -np.inf)):
+                    owners = [(q, r) for q in range(q0 - 3, q0 + 4) for r in range(r0 - 3, r0 + 4)
+                              if m.hex_owns(lat, q, r, (xx, y, 0.0))]
+                    assert len(owners) == 1, (orient, pitch, (q0, r0), (dq, dr), owners)
+                    assert owners[0] in ((q0, r0), (q0 + dq, r0 + dr))
+                    n += 1
+    assert n > 1000
