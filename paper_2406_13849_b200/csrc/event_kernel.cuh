@@ -14,8 +14,8 @@
 // Two forms of the queues:
 //  * ASYNC (the default, `NT_ROUNDS` unset): each queue is a ring in shared memory with a head and
 //    a tail counter and no block barrier.  A warp reads the five heads, claims up to 32 entries of
-//    the fullest ring (CAS on its head), and publishes every slot it appends to a ring entry after
-//    a block fence (ring_publish).  S may exceed the thread count (320 slots for 256 threads), so a
+//    the fullest ring (CAS on its head), and publishes every slot it appends to a lap-tagged ring
+//    entry after a block fence (ring_publish / ring_take).  S may exceed the thread count (320 slots for 256 threads), so a
 //    warp that finishes its chunk finds queued slots instead of waiting for other warps' chunks.
 //  * rounds (`NT_ROUNDS`): one queue set per round sorted by event type, warps take consecutive
 //    32-slot chunks, one block barrier per round, triple-buffered uint8 queues (S == B <= 256).
@@ -53,7 +53,8 @@ __device__ __forceinline__ void warp_count(bool pred, unsigned int* counter, int
 
 // ring capacity: the smallest power of two ABOVE the slot count.  A slot is in at most one ring at
 // a time, so at most S positions of a ring are allocated and unclaimed (tail - head <= S); with
-// RB > S, two of them never share an entry (see ring_publish / ring_take).
+// RB > S, two of them never share an entry (see ring_publish / ring_take).  Positions are 32-bit
+// counters; 2^32 is a multiple of 128 RB, so lap tags stay consistent across the wrap.
 __host__ __device__ constexpr int ring_size(int S) { return S < 128 ? 128 : S < 256 ? 256 : 512; }
 
 size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false) {
@@ -74,32 +75,35 @@ __device__ __forceinline__ uint32_t vload(const uint16_t* p) { return *reinterpr
 __device__ __forceinline__ void vstore(uint16_t* p, uint32_t v) {
   *reinterpret_cast<volatile uint16_t*>(p) = static_cast<uint16_t>(v);
 }
-// Ring entries (ASYNC form): 0 = empty, else slot + 1.  Position p of a ring maps to entry p mod RB,
-// so a producer (or consumer) of position p and one of p + RB can meet at the same entry when the
-// older party is slow.  Both sides therefore act with one shared-memory CAS:
-//  * ring_publish: empty -> slot + 1 (a producer never overwrites a value another producer put);
-//  * ring_take:    value -> empty (every value is taken by exactly one consumer).
-// A cell then holds at most one value at a time, and every value is consumed exactly once.  Two
-// positions of the same ring may swap values (a consumer of lap n + 1 can take lap n's value and
-// the lap-n consumer the next one), which is harmless: both wait for the same event.  Progress: a
-// producer waits only on a full cell, and the position holding that value has already been claimed
-// (otherwise more than S < RB positions of the ring would be pending, one per slot), so its
-// consumer lane is polling and takes it.  In detail, for one entry X: the allocated-but-unclaimed
-// positions of a ring lie in [head, tail), fewer than RB of them, so at most one maps to X.  With X
-// full, (claimed - taken) = (unpublished producers) - (unclaimed) + 1 >= 1: a claimed consumer of X
-// is still polling.  With X empty and a consumer polling, an allocated producer of X has not yet
-// published, and its CAS on the empty entry succeeds.
-__device__ __forceinline__ void ring_publish(uint16_t* e, int slot) {
-  const unsigned short v = static_cast<unsigned short>(slot + 1);
-  while (atomicCAS(reinterpret_cast<unsigned short*>(e), static_cast<unsigned short>(0), v) != 0) {}
+// Ring entries (ASYNC form) carry a lap tag, so that producers and consumers of different laps of
+// the same entry can never act on each other's state (a sequence-numbered MPMC ring with plain
+// 16-bit loads and stores, no atomics on the entries).  Position p of a ring maps to entry
+// p mod RB and belongs to lap L = p / RB; tag(L) = L mod 128.  An entry is
+//   FREE(L) = tag(L) << 9 | 511   : empty, next to be filled by the producer of lap L;
+//   FULL(L) = tag(L) << 9 | slot  : holds the slot pushed at lap L (slot <= 510).
+// The producer of position p waits for FREE(L) and stores FULL(L); the consumer of p waits for
+// FULL(L) and stores FREE(L + 1).  So each value is put by the one producer of its position and
+// taken by the one consumer of its position, in lap order.  Tags alias only if two parties of the
+// same entry were 128 laps apart.  They cannot be: at any moment the positions of one entry that
+// are in progress (allocated but not yet consumed) are the at most one allocated-unclaimed position
+// (tail - head <= S < RB) plus one per warp (a warp takes and pushes consecutive positions of a ring,
+// so it holds at most one position per entry), i.e. at most warps + 1 < 128 laps apart.
+// Progress: the lap-L producer of an entry waits only for the lap-(L-1) consumer, which has claimed
+// its position (see above) and waits only for the lap-(L-1) producer: by induction the oldest
+// in-progress position of every entry can always advance.
+constexpr uint32_t kRingFree = 511u;
+__device__ __forceinline__ uint32_t ring_tag(uint32_t pos, int log2rb) { return ((pos >> log2rb) & 127u) << 9; }
+__device__ __forceinline__ void ring_publish(uint16_t* e, uint32_t pos, int log2rb, int slot) {
+  const uint32_t tag = ring_tag(pos, log2rb);
+  while (vload(e) != (tag | kRingFree)) {}
+  vstore(e, tag | static_cast<uint32_t>(slot));
 }
-__device__ __forceinline__ int ring_take(uint16_t* e) {
-  for (;;) {
-    const uint32_t v = vload(e);
-    if (v != 0u && atomicCAS(reinterpret_cast<unsigned short*>(e), static_cast<unsigned short>(v),
-                             static_cast<unsigned short>(0)) == v)
-      return static_cast<int>(v) - 1;
-  }
+__device__ __forceinline__ int ring_take(uint16_t* e, uint32_t pos, int log2rb) {
+  const uint32_t tag = ring_tag(pos, log2rb);
+  uint32_t v;
+  while (((v = vload(e)) & ~kRingFree) != tag || (v & kRingFree) == kRingFree) {}
+  vstore(e, ring_tag(pos + (1u << log2rb), log2rb) | kRingFree);
+  return static_cast<int>(v & kRingFree);
 }
 
 // DP = true: the tracking operations go through the virtual tracker objects (dp_tracker.cuh).
@@ -142,7 +146,9 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
   off = (off + 15) & ~size_t(15);
   QIdx* sq = reinterpret_cast<QIdx*>(smem + off);            // [3][NQ][S]        (rounds)
   constexpr int RB = ring_size(S);
-  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + off);  // [NQ][RB] slot + 1, 0 = empty (ASYNC)
+  constexpr int kLog2RB = RB == 128 ? 7 : RB == 256 ? 8 : 9;
+  static_assert(S <= 510 && (1 << kLog2RB) == RB, "ring entries hold slot <= 510");
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + off);  // [NQ][RB] lap-tagged entries (ASYNC)
   unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NQ * RB)
                                : reinterpret_cast<unsigned int*>(sq + 3 * NQ * S);
   unsigned int* s_cnt = s_exit + nmc;
@@ -156,9 +162,9 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
   if (tid < 3 * NQ) s_qn[tid] = (!ASYNC && tid == 0 * NQ + Q_F) ? B : 0;   // rounds: round 0 reads set 0, all free
   if (ASYNC) {
-    for (int i = tid; i < NQ * RB; i += B) ring[i] = 0u;
+    for (int i = tid; i < NQ * RB; i += B) ring[i] = static_cast<uint16_t>(kRingFree);     // FREE(lap 0)
     __syncthreads();
-    for (int i = tid; i < S; i += B) ring[Q_F * RB + i] = static_cast<uint16_t>(i + 1);    // all slots free
+    for (int i = tid; i < S; i += B) ring[Q_F * RB + i] = static_cast<uint16_t>(i);        // FULL(lap 0): all slots free
     if (tid == 0) { a_tail[Q_F] = S; s_flag[0] = 0; s_flag[1] = 0; }
   } else {
     if (tid == 0) s_flag[0] = 0;
@@ -225,7 +231,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
         if (q < 0) break;
         valid = static_cast<uint32_t>(lane) < take;
         if (valid) {
-          slot = ring_take(ring + q * RB + ((h + lane) & (RB - 1)));
+          slot = ring_take(ring + q * RB + ((h + lane) & (RB - 1)), h + lane, kLog2RB);
           kind = (0x21045 >> (4 * q)) & 15;          // Q_M, Q_C, Q_DC, Q_DA, Q_F -> kinds 5, 4, 0, 1, 2
         }
         __threadfence_block();
@@ -247,7 +253,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             base2 = __shfl_sync(0xffffffffu, base2, leader);
             if (pred) {
               __threadfence_block();                               // slot state before the entry
-              ring_publish(ring + qq * RB + ((base2 + __popc(m & ((1u << lane) - 1u))) & (RB - 1)), slot);
+              const uint32_t pos = base2 + __popc(m & ((1u << lane) - 1u));
+              ring_publish(ring + qq * RB + (pos & (RB - 1)), pos, kLog2RB, slot);
             }
           }
         } else {
@@ -266,7 +273,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
         base2 = __shfl_sync(0xffffffffu, base2, leader);
         if (qq >= 0) {
           __threadfence_block();                                   // slot state before the entry
-          ring_publish(ring + qq * RB + ((base2 + __popc(grp & ((1u << lane) - 1u))) & (RB - 1)), slot);
+          const uint32_t pos = base2 + __popc(grp & ((1u << lane) - 1u));
+          ring_publish(ring + qq * RB + (pos & (RB - 1)), pos, kLog2RB, slot);
         }
       };
       // ---------------- EVENT: change_direction / descent / birth of this chunk's slots
