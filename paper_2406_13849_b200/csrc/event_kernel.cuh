@@ -51,16 +51,24 @@ __device__ __forceinline__ void warp_count(bool pred, unsigned int* counter, int
   if (lane == 0 && m) atomicAdd(counter, (unsigned)__popc(m));
 }
 
-// ring capacity: the smallest power of two ABOVE the slot count.  A slot is in at most one ring at
-// a time, so at most S positions of a ring are allocated and unclaimed (tail - head <= S); with
-// RB > S, two of them never share an entry (see ring_publish / ring_take).  Positions are 32-bit
+// ring capacity: the smallest power of two >= the slot count.  A slot is in at most one ring at a
+// time, so at most S <= RB positions of a ring are allocated and unclaimed (tail - head <= S): when
+// position p is allocated, position p - RB has already been claimed (see ring_publish / ring_take).  Positions are 32-bit
 // counters; 2^32 is a multiple of 128 RB, so lap tags stay consistent across the wrap.
-__host__ __device__ constexpr int ring_size(int S) { return S < 128 ? 128 : S < 256 ? 256 : 512; }
+__host__ __device__ constexpr int ring_size(int S) { return S <= 128 ? 128 : S <= 256 ? 256 : 512; }
 
-size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false) {
+// Frames T_l of the universe stack: stored per slot (3 doubles per level >= 1), or recomputed from
+// the stack's cells / tiles with the descent's own arithmetic (NT_FRAMES_RECOMPUTE: 72 B less per
+// slot at depth 4, so that four 256-thread blocks fit an SM).  Bit-identical either way.
+#ifndef NT_FRAMES_RECOMPUTE
+#define NT_FRAMES_RECOMPUTE 0
+#endif
+constexpr bool kFramesRecompute = NT_FRAMES_RECOMPUTE != 0;
+
+size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false, bool store_t = true) {
   const size_t nmc = g.n_mc, d = g.max_depth;
   size_t s = 0;
-  s += (7 + 3 * (d - 1) + (trace ? 1 : 0)) * 8 * (size_t)B;           // doubles (T from level 1)
+  s += (7 + (store_t ? 3 * (d - 1) : 0) + (trace ? 1 : 0)) * 8 * (size_t)B;   // doubles (T from level 1)
   s += (6 + 4 * d + (trace ? 2 : 0)) * 4 * (size_t)B;                 // ints
   s += (3 + (trace ? 1 : 0)) * (size_t)B;                             // bytes
   s = (s + 15) & ~size_t(15);
@@ -86,11 +94,12 @@ __device__ __forceinline__ void vstore(uint16_t* p, uint32_t v) {
 // taken by the one consumer of its position, in lap order.  Tags alias only if two parties of the
 // same entry were 128 laps apart.  They cannot be: at any moment the positions of one entry that
 // are in progress (allocated but not yet consumed) are the at most one allocated-unclaimed position
-// (tail - head <= S < RB) plus one per warp (a warp takes and pushes consecutive positions of a ring,
+// (tail - head <= S <= RB) plus one per warp (a warp takes and pushes consecutive positions of a ring,
 // so it holds at most one position per entry), i.e. at most warps + 1 < 128 laps apart.
 // Progress: the lap-L producer of an entry waits only for the lap-(L-1) consumer, which has claimed
 // its position (see above) and waits only for the lap-(L-1) producer: by induction the oldest
-// in-progress position of every entry can always advance.
+// in-progress position of every entry can always advance.  (tail - head <= S <= RB, so when p is
+// allocated the head is past p - RB.)
 constexpr uint32_t kRingFree = 511u;
 __device__ __forceinline__ uint32_t ring_tag(uint32_t pos, int log2rb) { return ((pos >> log2rb) & 127u) << 9; }
 __device__ __forceinline__ void ring_publish(uint16_t* e, uint32_t pos, int log2rb, int slot) {
@@ -117,19 +126,23 @@ __device__ __forceinline__ int ring_take(uint16_t* e, uint32_t pos, int log2rb) 
 // other slots queued instead of waiting for the chunks other warps hold; rounds need S == B).
 // RTK = 0: generic tracker; 1 / 2: the rect-specialised tracker (rect_geom.cuh, Alg. 9-10) with a box /
 // CZ-annuli root, run by the same scheduler (rg describes the model; unused when RTK = 0).
+#ifndef NT_EVENT_MINB
+#define NT_EVENT_MINB 3     // blocks per SM the 256-thread kernels are compiled for (tuning builds)
+#endif
 template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false, int S = B, int RTK = 0>
-__global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGeom g, const KRun R, const RectGeom rg) {
+__global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event(const DevGeom g, const KRun R, const RectGeom rg) {
   static_assert(ASYNC || S == B, "round-based queues need one slot per thread");
   static_assert(RTK == 0 || (!DP && !(TALLY & 2)), "RTK: SP dispatch, no instance tallies");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmc = g.n_mc, maxd = g.max_depth;
+  constexpr bool kStoreT = RTK != 0 || DP || !kFramesRecompute;   // frames in shared memory
   // ---- carve shared memory (see event_smem_bytes)
   double* sx = reinterpret_cast<double*>(smem);
   double* sy = sx + S; double* sz = sy + S; double* su = sz + S; double* sv = su + S; double* sw = sv + S;
   double* stau = sw + S;
   double* sTb = stau + S;                           // [maxd-1][3][S] (T_0 = 0)
-  double* sps = sTb + 3 * (maxd - 1) * S;           // TRACE: pending segment length
+  double* sps = sTb + (kStoreT ? 3 * (maxd - 1) * S : 0);   // TRACE: pending segment length
   uint32_t* sidx = reinterpret_cast<uint32_t*>(sps + (TRACE ? S : 0));
   uint32_t* sepoch = sidx + S; uint32_t* snseg = sepoch + S;
   int32_t* smc = reinterpret_cast<int32_t*>(snseg + S);
@@ -357,9 +370,13 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             l0 = dsc & 15;
             fsense = (dsc >> 4) & 1;
             fh = (dsc >> 5) - 1;
+            if constexpr (kStoreT) {
+              Tx = st.T(l0, 0); Ty = st.T(l0, 1); Tz = st.T(l0, 2);
+            } else {
+              frame_of(g, st, l0, Tx, Ty, Tz);
+            }
             if (kind == 0) {
               du = st.u(l0);
-              Tx = st.T(l0, 0); Ty = st.T(l0, 1); Tz = st.T(l0, 2);
             } else {                                     // Alg. 6: tile +- 1 at level l0, then daughter
               const int j = fh;
               int ta = st.a(l0), tb = st.b(l0), tc = st.c(l0);
@@ -381,7 +398,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
                 du = array_daughter(g, U, uk, ta, tb, tc, tx, ty, tz);
               }
               st.a(l0) = ta; st.b(l0) = tb; st.c(l0) = tc;
-              Tx = st.T(l0, 0) + tx; Ty = st.T(l0, 1) + ty; Tz = st.T(l0, 2) + tz;
+              Tx = Tx + tx; Ty = Ty + ty; Tz = Tz + tz;
               l0 = l0 + 1;
               fh = -1;
               fsense = 0;
@@ -398,7 +415,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             }
             ok = du >= 0 && rect_descend<RTK == 1>(g, rg, st, l0, fh, fsense, rx, ry, rz, L, mc, flags);
           }
-          else ok = du >= 0 && descend(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh, fsense, L, mc, flags);
+          else ok = du >= 0 && descend<kStoreT>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh, fsense, L, mc, flags);
           done = true;
           if (!ok) flags |= NT_F3;
           sflags[slot] = static_cast<uint8_t>(flags);
@@ -456,9 +473,23 @@ __global__ void __launch_bounds__(B, B >= 256 ? 3 : 5) k_track_event(const DevGe
             if constexpr (RTK != 0) {
               rect_distances<RTK == 1>(g, rg, st, L, rx, ry, rz, u, v, w, os_l, os_s, b);
             } else {
-              for (int l = 0; l < L; ++l) {
-                if constexpr (DP) level_distances_dp(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
-                else level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+              if constexpr (DP) {
+                for (int l = 0; l < L; ++l) level_distances_dp(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+              } else if constexpr (kStoreT) {
+                for (int l = 0; l < L; ++l) level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+              } else {
+                // frames accumulated level by level (T_0 = 0), as the descent built them
+                double Tx = 0.0, Ty = 0.0, Tz = 0.0;
+                for (int l = 0; l < L; ++l) {
+                  const DUniv* U = g.univ + st.u(l);
+                  const int kind_l = st.ukind(l), ia = st.a(l), ib = st.b(l), ic = st.c(l);
+                  level_candidates(g, U, kind_l, ia, ib, ic, l, rx - Tx, ry - Ty, rz - Tz, u, v, w, os_l, os_s, b);
+                  if (l + 1 < L) {
+                    double tx, ty, tz;
+                    level_translation(g, U, kind_l, ia, ib, ic, tx, ty, tz);
+                    Tx = Tx + tx; Ty = Ty + ty; Tz = Tz + tz;
+                  }
+                }
               }
             }
             const double sig = ld(g.mc_st + mc);

@@ -214,6 +214,17 @@ __device__ __forceinline__ void level_translation(const DevGeom& g, const DUniv*
   }
 }
 
+// frame T_l of level l of the stack, accumulated from level 0 (T_0 = 0) with the descent's arithmetic
+__device__ __forceinline__ void frame_of(const DevGeom& g, Stack& st, int l, double& Tx, double& Ty, double& Tz) {
+  Tx = 0.0; Ty = 0.0; Tz = 0.0;
+#pragma unroll 1
+  for (int k = 0; k < l; ++k) {
+    double tx, ty, tz;
+    level_translation(g, g.univ + st.u(k), st.ukind(k), st.a(k), st.b(k), st.c(k), tx, ty, tz);
+    Tx = Tx + tx; Ty = Ty + ty; Tz = Tz + tz;
+  }
+}
+
 template <bool TRACE>
 __device__ __forceinline__ void emit(const KRun& R, uint64_t pid, uint32_t seg, int kind, int level, int j,
                                      int cb, int ca, double s, int terminal, uint32_t flags) {
@@ -519,16 +530,16 @@ cudaError_t upload_coefficients(const double* host, int n) {
   return cudaMemcpyToSymbol(c_coef, host, sizeof(double) * n);
 }
 
-// Slots per block of the ring scheduler (block 256, SP): 320 when three such blocks still fit an SM
-// (a warp that finishes its chunk then finds queued slots instead of waiting for the chunks the
-// other seven warps hold), else 256.  NESTRACK_SLOTS=256|320 overrides (tuning).
-static int ring_slots(const DevGeom& g, bool trace) {
+// Slots per block of the ring scheduler (block 256, SP): 320 when NT_EVENT_MINB such blocks still
+// fit an SM (a warp that finishes its chunk then finds queued slots instead of waiting for the
+// chunks the other seven warps hold), else 256.  NESTRACK_SLOTS=256|320 overrides (tuning).
+static int ring_slots(const DevGeom& g, bool trace, bool store_t) {
   static const int env = [] { const char* e = getenv("NESTRACK_SLOTS"); return e ? atoi(e) : 0; }();
   if (env == 256 || env == 320) return env;
   int dev = 0, smem_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  const size_t need = 3 * (event_smem_bytes(g, 320, trace, true) + 1024);
+  const size_t need = NT_EVENT_MINB * (event_smem_bytes(g, 320, trace, true, store_t) + 1024);
   return need <= (size_t)smem_sm ? 320 : 256;
 }
 
@@ -563,7 +574,7 @@ cudaError_t launch_rect_event(const DevGeom& g, const RectGeom& rg, const KRun& 
   if (R.inst) return cudaErrorNotSupported;
   const bool mesh = R.mesh != nullptr;
   if (mesh && trace) return cudaErrorNotSupported;
-  const bool s320 = !trace && !mesh && ring_slots(g, false) == 320;
+  const bool s320 = !trace && !mesh && ring_slots(g, false, true) == 320;
   const size_t smem = event_smem_bytes(g, s320 ? 320 : 256, trace, true);
   auto go = [&](auto kern) {
     return launch_event_kernel(kern, g, rg, R, 256, smem, blocks_per_sm, stream, grid_out);
@@ -674,7 +685,8 @@ cudaError_t launch_rect(const DevGeom&, const RectGeom&, const KRun&, bool, bool
 
 cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool states, int block,
                          int blocks_per_sm, cudaStream_t stream, int* grid_out, bool async) {
-  size_t smem = event_smem_bytes(g, block, trace, async);
+  const bool st_t = g.trk != nullptr || !kFramesRecompute;     // DP kernels keep frames in smem
+  size_t smem = event_smem_bytes(g, block, trace, async, st_t);
   const RectGeom no_rg{};
   auto go = [&](auto kern) -> cudaError_t {
     return launch_event_kernel(kern, g, no_rg, R, block, smem, blocks_per_sm, stream, grid_out);
@@ -690,8 +702,8 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
     if (block != 256) return cudaErrorInvalidValue;
     auto pick = [&](auto dp) -> cudaError_t {
       constexpr bool D = decltype(dp)::value;
-      if (!D && tally && ring_slots(g, false) == 320) {   // mesh / instance tallies: 320 slots as well
-        smem = event_smem_bytes(g, 320, false, true);
+      if (!D && tally && ring_slots(g, false, st_t) == 320) {   // mesh / instance tallies: 320 slots as well
+        smem = event_smem_bytes(g, 320, false, true, st_t);
         if (tally == 1) return states ? go(k_track_event<256, false, true, false, 1, true, 320>) : go(k_track_event<256, false, false, false, 1, true, 320>);
         if (tally == 2) return states ? go(k_track_event<256, false, true, false, 2, true, 320>) : go(k_track_event<256, false, false, false, 2, true, 320>);
         return states ? go(k_track_event<256, false, true, false, 3, true, 320>) : go(k_track_event<256, false, false, false, 3, true, 320>);
@@ -699,8 +711,8 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
       if (tally == 1) return states ? go(k_track_event<256, false, true, D, 1, true>) : go(k_track_event<256, false, false, D, 1, true>);
       if (tally == 2) return states ? go(k_track_event<256, false, true, D, 2, true>) : go(k_track_event<256, false, false, D, 2, true>);
       if (tally == 3) return states ? go(k_track_event<256, false, true, D, 3, true>) : go(k_track_event<256, false, false, D, 3, true>);
-      if (!D && ring_slots(g, trace) == 320) {
-        smem = event_smem_bytes(g, 320, trace, true);
+      if (!D && ring_slots(g, trace, st_t) == 320) {
+        smem = event_smem_bytes(g, 320, trace, true, st_t);
         if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 320>) : go(k_track_event<256, true, false, false, 0, true, 320>);
         return states ? go(k_track_event<256, false, true, false, 0, true, 320>) : go(k_track_event<256, false, false, false, 0, true, 320>);
       }

@@ -11,6 +11,13 @@ for c in ${CONFIGS:-c1 c2 c3 c4 c5m c5r}; do
     python bench.py --config $c --steps 1 --warmup 1 --no-e2e --no-ratio --no-cpu-baseline \
     > gpurun_out/ncu_traffic_${c}_$R.csv 2> gpurun_out/ncu_traffic_${c}_$R.err
 done
+# DRAM traffic vs batch size (is the write traffic per launch or per history?)
+for n in 1e6 1e7; do
+  timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,lts__t_sectors_srcunit_tex_op_write.sum,lts__t_sectors_srcunit_tex_op_red.sum,l1tex__t_bytes_pipe_lsu_mem_local_op_st.sum,l1tex__t_bytes_pipe_lsu_mem_local_op_ld.sum \
+    --clock-control none -k regex:k_track_event -s 1 -c 1 --csv \
+    python bench.py --particles $n --steps 1 --warmup 1 --no-e2e --no-ratio --no-cpu-baseline \
+    > gpurun_out/ncu_traffic_c3_n${n}_$R.csv 2> gpurun_out/ncu_traffic_c3_n${n}_$R.err
+done
 if [ -z "$SKIP_FULL" ]; then
 for c in c3 c4; do
   timeout 2400 ncu --set full --clock-control none --import-source on -k regex:k_track_event -s 3 -c 1 -o /tmp/prof_${c}_$R \
