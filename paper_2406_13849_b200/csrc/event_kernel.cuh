@@ -30,6 +30,12 @@ NT_DEV_BEGIN
 // Queue layout (uint8 slot indices), triple-buffered by round:
 //   Q_M[p] move-ready, Q_C[p] collide, Q_DC[p] CSG descents, Q_DA[p] array descents, Q_F[p] free
 enum { Q_M = 0, Q_C = 1, Q_DC = 2, Q_DA = 3, Q_F = 4, NQ = 5 };
+// ASYNC with NR = 7 rings (models whose histories sit at different depths, e.g. a hex core inside a
+// CSG reflector): reflected / collide / CSG-descent slots of histories above the deepest level go
+// to rings of their own, so that a warp's MOVE runs slots with the same number of levels (the
+// level loop otherwise diverges).  Ring q serves event kind kRingKind[q].
+enum { Q_M2 = 5, Q_C2 = 6, Q_DC2 = 7 };
+__host__ __device__ constexpr int ring_kind(int q) { return (0x04521045 >> (4 * q)) & 15; }   // 5 4 0 1 2 5 4 0
 #ifndef NT_RING_SLEEP_NS
 #define NT_RING_SLEEP_NS 64     // back-off of a warp that found every ring empty
 #endif
@@ -64,15 +70,18 @@ __host__ __device__ constexpr int ring_size(int S) { return S <= 128 ? 128 : S <
 #define NT_FRAMES_RECOMPUTE 0
 #endif
 constexpr bool kFramesRecompute = NT_FRAMES_RECOMPUTE != 0;
+#ifndef NT_DEPTH_RINGS
+#define NT_DEPTH_RINGS 0     // 1: depth-class rings (NR = 7) for the f7 feature set (tuning builds)
+#endif
 
-size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false, bool store_t = true) {
+size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false, bool store_t = true, int nr = NQ) {
   const size_t nmc = g.n_mc, d = g.max_depth;
   size_t s = 0;
   s += (7 + (store_t ? 3 * (d - 1) : 0) + (trace ? 1 : 0)) * 8 * (size_t)B;   // doubles (T from level 1)
   s += (6 + 4 * d + (trace ? 2 : 0)) * 4 * (size_t)B;                 // ints
   s += (3 + (trace ? 1 : 0)) * (size_t)B;                             // bytes
   s = (s + 15) & ~size_t(15);
-  if (async) s += NQ * sizeof(uint16_t) * (size_t)ring_size(B);        // ring queues
+  if (async) s += nr * sizeof(uint16_t) * (size_t)ring_size(B);        // ring queues
   else s += 3 * NQ * sizeof(QIdx) * (size_t)B;                        // queues (triple-buffered)
   s += (nmc + kNC + 3 * NQ + 4) * 4;                                    // exits, counters, queue counts
   return (s + 15) & ~size_t(15);
@@ -129,10 +138,12 @@ __device__ __forceinline__ int ring_take(uint16_t* e, uint32_t pos, int log2rb) 
 #ifndef NT_EVENT_MINB
 #define NT_EVENT_MINB 3     // blocks per SM the 256-thread kernels are compiled for (tuning builds)
 #endif
-template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false, int S = B, int RTK = 0>
+template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false, int S = B, int RTK = 0,
+          int NR = NQ>
 __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event(const DevGeom g, const KRun R, const RectGeom rg) {
   static_assert(ASYNC || S == B, "round-based queues need one slot per thread");
   static_assert(RTK == 0 || (!DP && !(TALLY & 2)), "RTK: SP dispatch, no instance tallies");
+  static_assert(NR == NQ || (ASYNC && NR == 7), "depth-class rings: ring scheduler only, 7 rings");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmc = g.n_mc, maxd = g.max_depth;
@@ -161,21 +172,21 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
   constexpr int RB = ring_size(S);
   constexpr int kLog2RB = RB == 128 ? 7 : RB == 256 ? 8 : 9;
   static_assert(S <= 510 && (1 << kLog2RB) == RB, "ring entries hold slot <= 510");
-  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + off);  // [NQ][RB] lap-tagged entries (ASYNC)
-  unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NQ * RB)
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + off);  // [NR][RB] lap-tagged entries (ASYNC)
+  unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NR * RB)
                                : reinterpret_cast<unsigned int*>(sq + 3 * NQ * S);
   unsigned int* s_cnt = s_exit + nmc;
   int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [3][NQ]
   int* s_flag = s_qn + 3 * NQ;                              // [0] = pids exhausted, [1] live (ASYNC)
-  uint32_t* a_head = reinterpret_cast<uint32_t*>(s_qn);      // ASYNC: [NQ] heads, [NQ] tails
-  uint32_t* a_tail = a_head + NQ;
+  uint32_t* a_head = reinterpret_cast<uint32_t*>(s_qn);      // ASYNC: [NR] heads, [NR] tails (2 NR <= 3 NQ)
+  uint32_t* a_tail = a_head + NR;
   double* gl = R.slices + (size_t)blockIdx.x * nmc;         // per-block track-length tally (global)
 
   for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
   if (tid < 3 * NQ) s_qn[tid] = (!ASYNC && tid == 0 * NQ + Q_F) ? B : 0;   // rounds: round 0 reads set 0, all free
   if (ASYNC) {
-    for (int i = tid; i < NQ * RB; i += B) ring[i] = static_cast<uint16_t>(kRingFree);     // FREE(lap 0)
+    for (int i = tid; i < NR * RB; i += B) ring[i] = static_cast<uint16_t>(kRingFree);     // FREE(lap 0)
     __syncthreads();
     for (int i = tid; i < S; i += B) ring[Q_F * RB + i] = static_cast<uint16_t>(i);        // FULL(lap 0): all slots free
     if (tid == 0) { a_tail[Q_F] = S; s_flag[0] = 0; s_flag[1] = 0; }
@@ -226,7 +237,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         for (;;) {
           const bool births = vload(reinterpret_cast<uint32_t*>(s_flag)) == 0u;
           uint32_t hk = 0, av = 0;
-          if (lane < NQ && (lane != Q_F || births)) { hk = vload(a_head + lane); av = vload(a_tail + lane) - hk; }
+          if (lane < NR && (lane != Q_F || births)) { hk = vload(a_head + lane); av = vload(a_tail + lane) - hk; }
           const uint32_t mx = __reduce_max_sync(0xffffffffu, (av << 8) | static_cast<uint32_t>(255 - lane));
           const uint32_t bav = mx >> 8;                  // av <= S slots (< 2^24): fits above the lane byte
           if (bav > 0u) {
@@ -245,7 +256,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         valid = static_cast<uint32_t>(lane) < take;
         if (valid) {
           slot = ring_take(ring + q * RB + ((h + lane) & (RB - 1)), h + lane, kLog2RB);
-          kind = (0x21045 >> (4 * q)) & 15;          // Q_M, Q_C, Q_DC, Q_DA, Q_F -> kinds 5, 4, 0, 1, 2
+          kind = ring_kind(q);                       // Q_M, Q_C, Q_DC, Q_DA, Q_F (, Q_M2, Q_C2, Q_DC2) -> 5 4 0 1 2 (5 4 0)
         }
         __threadfence_block();
       } else if (valid) {
@@ -570,8 +581,10 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         if (lcross >= 0) atomicAdd(s_cnt + C_CBL0 + lcross, 1u);   // crossings = leaks + sum over levels (flush)
         // enqueue for the next event
         if constexpr (ASYNC) {
-          push_all(ended_at_event || outc == 5 ? Q_F : outc == 1 ? Q_M : outc == 2 ? Q_C : outc == 3 ? Q_DC
-                   : outc == 4 ? Q_DA : -1);
+          // NR = 7: histories above the deepest level take the second set of rings (depth class)
+          const int cls = (NR == 7 && ready && sL[slot] < maxd) ? Q_M2 : 0;
+          push_all(ended_at_event || outc == 5 ? Q_F : outc == 1 ? (cls ? Q_M2 : Q_M) : outc == 2 ? (cls ? Q_C2 : Q_C)
+                   : outc == 3 ? (cls ? Q_DC2 : Q_DC) : outc == 4 ? Q_DA : -1);
         } else {
           push(Q_M, outc == 1);
           push(Q_C, outc == 2);

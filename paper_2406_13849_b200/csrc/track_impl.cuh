@@ -533,13 +533,13 @@ cudaError_t upload_coefficients(const double* host, int n) {
 // Slots per block of the ring scheduler (block 256, SP): 320 when NT_EVENT_MINB such blocks still
 // fit an SM (a warp that finishes its chunk then finds queued slots instead of waiting for the
 // chunks the other seven warps hold), else 256.  NESTRACK_SLOTS=256|320 overrides (tuning).
-static int ring_slots(const DevGeom& g, bool trace, bool store_t) {
+static int ring_slots(const DevGeom& g, bool trace, bool store_t, int nr = NQ) {
   static const int env = [] { const char* e = getenv("NESTRACK_SLOTS"); return e ? atoi(e) : 0; }();
   if (env == 256 || env == 320) return env;
   int dev = 0, smem_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  const size_t need = NT_EVENT_MINB * (event_smem_bytes(g, 320, trace, true, store_t) + 1024);
+  const size_t need = NT_EVENT_MINB * (event_smem_bytes(g, 320, trace, true, store_t, nr) + 1024);
   return need <= (size_t)smem_sm ? 320 : 256;
 }
 
@@ -711,6 +711,18 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
       if (tally == 1) return states ? go(k_track_event<256, false, true, D, 1, true>) : go(k_track_event<256, false, false, D, 1, true>);
       if (tally == 2) return states ? go(k_track_event<256, false, true, D, 2, true>) : go(k_track_event<256, false, false, D, 2, true>);
       if (tally == 3) return states ? go(k_track_event<256, false, true, D, 3, true>) : go(k_track_event<256, false, false, D, 3, true>);
+#if NT_FEAT != 0 && NT_DEPTH_RINGS
+      if (!D) {                    // hex / plane / sphere models: depth-class rings (NR = 7)
+        if (ring_slots(g, trace, st_t, 7) == 320) {
+          smem = event_smem_bytes(g, 320, trace, true, st_t, 7);
+          if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 320, 0, 7>) : go(k_track_event<256, true, false, false, 0, true, 320, 0, 7>);
+          return states ? go(k_track_event<256, false, true, false, 0, true, 320, 0, 7>) : go(k_track_event<256, false, false, false, 0, true, 320, 0, 7>);
+        }
+        smem = event_smem_bytes(g, 256, trace, true, st_t, 7);
+        if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 256, 0, 7>) : go(k_track_event<256, true, false, false, 0, true, 256, 0, 7>);
+        return states ? go(k_track_event<256, false, true, false, 0, true, 256, 0, 7>) : go(k_track_event<256, false, false, false, 0, true, 256, 0, 7>);
+      }
+#endif
       if (!D && ring_slots(g, trace, st_t) == 320) {
         smem = event_smem_bytes(g, 320, trace, true, st_t);
         if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 320>) : go(k_track_event<256, true, false, false, 0, true, 320>);
