@@ -31,11 +31,11 @@ NT_DEV_BEGIN
 //   Q_M[p] move-ready, Q_C[p] collide, Q_DC[p] CSG descents, Q_DA[p] array descents, Q_F[p] free
 enum { Q_M = 0, Q_C = 1, Q_DC = 2, Q_DA = 3, Q_F = 4, NQ = 5 };
 // ASYNC with NR = 7 rings (models whose histories sit at different depths, e.g. a hex core inside a
-// CSG reflector): reflected / collide / CSG-descent slots of histories above the deepest level go
-// to rings of their own, so that a warp's MOVE runs slots with the same number of levels (the
-// level loop otherwise diverges).  Ring q serves event kind kRingKind[q].
-enum { Q_M2 = 5, Q_C2 = 6, Q_DC2 = 7 };
-__host__ __device__ constexpr int ring_kind(int q) { return (0x04521045 >> (4 * q)) & 15; }   // 5 4 0 1 2 5 4 0
+// CSG reflector): collide and CSG-descent slots of histories above the deepest level go to rings
+// of their own, so that a warp's MOVE runs slots with the same number of levels (the level loop
+// otherwise diverges).  Ring q serves event kind ring_kind(q).
+enum { Q_C2 = 5, Q_DC2 = 6 };
+__host__ __device__ constexpr int ring_kind(int q) { return (0x0421045 >> (4 * q)) & 15; }   // 5 4 0 1 2 4 0
 #ifndef NT_RING_SLEEP_NS
 #define NT_RING_SLEEP_NS 64     // back-off of a warp that found every ring empty
 #endif
@@ -144,6 +144,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
   static_assert(ASYNC || S == B, "round-based queues need one slot per thread");
   static_assert(RTK == 0 || (!DP && !(TALLY & 2)), "RTK: SP dispatch, no instance tallies");
   static_assert(NR == NQ || (ASYNC && NR == 7), "depth-class rings: ring scheduler only, 7 rings");
+  static_assert(ring_kind(Q_C2) == 4 && ring_kind(Q_DC2) == 0 && ring_kind(Q_F) == 2 && Q_DC2 < 7, "ring table");
   extern __shared__ __align__(16) unsigned char smem[];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmc = g.n_mc, maxd = g.max_depth;
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         valid = static_cast<uint32_t>(lane) < take;
         if (valid) {
           slot = ring_take(ring + q * RB + ((h + lane) & (RB - 1)), h + lane, kLog2RB);
-          kind = ring_kind(q);                       // Q_M, Q_C, Q_DC, Q_DA, Q_F (, Q_M2, Q_C2, Q_DC2) -> 5 4 0 1 2 (5 4 0)
+          kind = ring_kind(q);                       // Q_M, Q_C, Q_DC, Q_DA, Q_F (, Q_C2, Q_DC2) -> 5 4 0 1 2 (4 0)
         }
         __threadfence_block();
       } else if (valid) {
@@ -582,8 +583,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         // enqueue for the next event
         if constexpr (ASYNC) {
           // NR = 7: histories above the deepest level take the second set of rings (depth class)
-          const int cls = (NR == 7 && ready && sL[slot] < maxd) ? Q_M2 : 0;
-          push_all(ended_at_event || outc == 5 ? Q_F : outc == 1 ? (cls ? Q_M2 : Q_M) : outc == 2 ? (cls ? Q_C2 : Q_C)
+          const bool cls = NR == 7 && ready && sL[slot] < maxd;
+          push_all(ended_at_event || outc == 5 ? Q_F : outc == 1 ? Q_M : outc == 2 ? (cls ? Q_C2 : Q_C)
                    : outc == 3 ? (cls ? Q_DC2 : Q_DC) : outc == 4 ? Q_DA : -1);
         } else {
           push(Q_M, outc == 1);

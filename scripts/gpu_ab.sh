@@ -5,6 +5,8 @@ mkdir -p gpurun_out
 TAG=${TAG:-ab}
 for v in base ${VARIANTS}; do
   if [ "$v" = base ]; then unset NESTRACK_LIB; else export NESTRACK_LIB=$PWD/tune/libnestrack_$v.so; fi
+  timeout 240 python scripts/stress_ring.py 2 > gpurun_out/${TAG}_${v}_stress.log 2>&1
+  if [ $? -ne 0 ]; then echo "stress failed: skipping $v" >> gpurun_out/${TAG}_${v}_stress.log; continue; fi
   timeout 600 python -m pytest tests/test_gpu_parity.py -x -q --timeout 300 --timeout_method thread \
     -k "config_trace_parity or rect_tracker or mesh_tally or instance or fission_bank" > gpurun_out/${TAG}_${v}_pytest.log 2>&1
   echo "pytest exit $?" >> gpurun_out/${TAG}_${v}_pytest.log
