@@ -71,7 +71,7 @@ __host__ __device__ constexpr int ring_size(int S) { return S <= 128 ? 128 : S <
 #endif
 constexpr bool kFramesRecompute = NT_FRAMES_RECOMPUTE != 0;
 #ifndef NT_DEPTH_RINGS
-#define NT_DEPTH_RINGS 0     // 1: depth-class rings (NR = 7) for the f7 feature set (tuning builds)
+#define NT_DEPTH_RINGS 1     // depth-class rings (NR = 7) for the f7 feature set (0: five rings everywhere)
 #endif
 
 size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false, bool store_t = true, int nr = NQ) {
