@@ -7,8 +7,8 @@ P:1054-1080): the same walks tracked with
   ST   pseudo-array universes, all CSG + BIH            pseudo_array=True
 
 and reported as segments/s and as a fraction of the RTK rate (the paper's Table 2 metric), with
-the segment counts that prove the walks are the same.  All four share the block-queue scheduler
-except RTK (its own history-based kernel).
+the segment counts that prove the walks are the same.  All four share the ring (block-queue)
+scheduler; RTK-H is the rect-specialised tracker's own history-based kernel.
 
     python scripts/dispatch_study.py [--configs c2,c3,c5r,c4,c5m] [--reps 3] [--out gpurun_out/dispatch.json]
 """
@@ -34,7 +34,8 @@ ap.add_argument("--st-particles", type=float, default=2e6, help="ST runs are slo
 ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "dispatch.json"))
 a = ap.parse_args()
 
-VARIANTS = [("RTK", dict(tracker="rect", scheduler="history"), False),
+VARIANTS = [("RTK", dict(tracker="rect", scheduler="block"), False),
+            ("RTK-H", dict(tracker="rect", scheduler="history"), False),
             ("SP", dict(scheduler="block"), False),
             ("DP", dict(scheduler="dp"), False),
             ("ST", dict(scheduler="block"), True)]
