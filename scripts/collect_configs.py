@@ -6,6 +6,7 @@ kernel per workload), <round>_configs.json (the bench lines), and the BASELINE.m
 """
 import argparse
 import csv
+import sys
 import glob
 import io
 import json
@@ -13,6 +14,7 @@ import os
 import re
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
 OUT = os.path.join(ROOT, "gpurun_out")
 PROF = os.path.join(ROOT, "profiles")
 NAMES = {"c1": "C1 pincell", "c2": "C2 17x17 assembly", "c3": "C3 full-core PWR", "c4": "C4 hex microreactor",
@@ -44,7 +46,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--round", default="r02")
     ap.add_argument("--baseline", action="store_true", help="rewrite BASELINE.md §4")
+    ap.add_argument("--traffic-only", action="store_true",
+                    help="update profiles/traffic.json from the ncu captures alone (before the bench lines exist)")
     a = ap.parse_args()
+    import workloads
+    names = {c: workloads.config(c)[0]["name"] for c in NAMES}
     lines, traffic = {}, {}
     tpath = os.path.join(PROF, "traffic.json")
     if os.path.exists(tpath):
@@ -56,18 +62,22 @@ def main():
             if js:
                 lines[c] = json.loads(js[-1])
         tp = os.path.join(OUT, f"ncu_traffic_{c}_{a.round}.csv")
-        if os.path.exists(tp) and c in lines:
+        if os.path.exists(tp):
             m = ncu_metrics(tp)
             if "dram__bytes_read.sum" in m:
-                w = lines[c]["config"]["workload"]
+                w = names[c]
                 traffic[w] = m["dram__bytes_read.sum"] + m["dram__bytes_write.sum"]
                 traffic[w + ".read"] = m["dram__bytes_read.sum"]
                 traffic[w + ".write"] = m["dram__bytes_write.sum"]
-                traffic[w + ".thread_inst_per_segment"] = (
-                    m.get("smsp__thread_inst_executed.sum", 0.0) / max(lines[c]["value"] * lines[c]["ms_per_step"] / 1e3, 1.0))
+                if c in lines:
+                    traffic[w + ".thread_inst_per_segment"] = (
+                        m.get("smsp__thread_inst_executed.sum", 0.0)
+                        / max(lines[c]["value"] * lines[c]["ms_per_step"] / 1e3, 1.0))
     traffic["_doc"] = ("dram__bytes_read.sum + dram__bytes_write.sum per launch of the tracking kernel at each "
                        "workload's bench configuration (ncu --metrics, one launch after a warm-up), round " + a.round)
     json.dump(traffic, open(tpath, "w"), indent=1, sort_keys=True)
+    if a.traffic_only:
+        return
     json.dump(lines, open(os.path.join(PROF, f"{a.round}_configs.json"), "w"), indent=1)
     rows = []
     for c, d in lines.items():
@@ -88,7 +98,7 @@ def main():
         p = os.path.join(ROOT, "BASELINE.md")
         s = open(p).read()
         head = s[:s.index("## 4.")]
-        s4 = ("## 4. Results table (driver-run bench lines of this build, 1 B200; " + a.round + ")\n\n"
+        s4 = ("## 4. Results table (bench lines of this build, measured by the builder on 1 B200 via gpurun; " + a.round + ")\n\n"
               "Source: `python bench.py --config cN` (defaults: W = 3, K = 5, L2 flushed between steps), collected by "
               "`scripts/collect_configs.py` into `profiles/" + a.round + "_configs.json`.  fp64 frac = F_alg x "
               "segments/s / 37.2 TFLOP/s (derived peak); HBM frac = ncu DRAM bytes per launch / kernel time / "

@@ -4,12 +4,17 @@
 cd "$GRAFT_REPO_ROOT" 2>/dev/null || cd /root/repo
 mkdir -p gpurun_out
 R=${ROUND:-r02}
+# DRAM traffic per config first (ncu, one launch after a warm-up), so that the bench lines below
+# carry this build's HBM fraction
 for c in ${CONFIGS:-c1 c2 c3 c4 c5m c5r}; do
-  timeout 900 python bench.py --config $c --cpu-seconds 8 > gpurun_out/bench_${c}_$R.json 2> gpurun_out/bench_${c}_$R.err
   timeout 600 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,smsp__inst_executed.sum,smsp__thread_inst_executed.sum \
     --clock-control none -k regex:k_track_event -s 1 -c 1 --csv \
     python bench.py --config $c --steps 1 --warmup 1 --no-e2e --no-ratio --no-cpu-baseline \
     > gpurun_out/ncu_traffic_${c}_$R.csv 2> gpurun_out/ncu_traffic_${c}_$R.err
+done
+python scripts/collect_configs.py --round $R --traffic-only > /dev/null 2>&1
+for c in ${CONFIGS:-c1 c2 c3 c4 c5m c5r}; do
+  timeout 900 python bench.py --config $c --cpu-seconds 8 > gpurun_out/bench_${c}_$R.json 2> gpurun_out/bench_${c}_$R.err
 done
 # DRAM traffic vs batch size (is the write traffic per launch or per history?)
 for n in 1e6 1e7; do
