@@ -70,6 +70,14 @@ __host__ __device__ constexpr int ring_size(int S) { return S <= 128 ? 128 : S <
 #define NT_FRAMES_RECOMPUTE 0
 #endif
 constexpr bool kFramesRecompute = NT_FRAMES_RECOMPUTE != 0;
+// EVENT -> MOVE forwarding: the position a descent or birth just read or made, the flags / depth /
+// material cell a descent produced, and the direction and tau a birth or scatter drew stay in
+// registers for the MOVE of the same slot instead of a shared-memory store and reload (bank
+// conflicts on every per-slot access: profiles/r02_ncu_analysis.md).  0: always reload.
+#ifndef NT_FORWARD
+#define NT_FORWARD 0
+#endif
+constexpr bool kForward = NT_FORWARD != 0;
 #ifndef NT_DEPTH_RINGS
 #define NT_DEPTH_RINGS 1     // depth-class rings (NR = 7) for the f7 feature set (0: five rings everywhere)
 #endif
@@ -324,6 +332,11 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         bool ok = false, done = false, scat = false, absorbed = false;
         int iso_ep = -2;      // >= 0: isotropic direction from (epoch iso_ep, block 1) and tau; -1: tau only
         double xtau = 0.0;
+        // forwarded to MOVE (kForward): position, direction, tau, and a descent's flags / depth / cell
+        double fx = 0.0, fy = 0.0, fz = 0.0, fu = 0.0, fv = 0.0, fw = 0.0, ftau = 0.0;
+        uint32_t fflags = 0;
+        int fL = 0, fmc = 0;
+        bool f_pos = false, f_dir = false, f_tau = false, f_desc = false;
         if (kind == 4) {
           // ---- change_direction (O14, O15)
           const uint64_t pid = R.pid0 + sidx[slot];
@@ -361,7 +374,9 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
             if (STATES) {
               const uint64_t id = sidx[slot];
               rx = R.states[id]; ry = R.states[R.n + id]; rz = R.states[2 * R.n + id];
-              su[slot] = R.states[3 * R.n + id]; sv[slot] = R.states[4 * R.n + id]; sw[slot] = R.states[5 * R.n + id];
+              fu = R.states[3 * R.n + id]; fv = R.states[4 * R.n + id]; fw = R.states[5 * R.n + id];
+              su[slot] = fu; sv[slot] = fv; sw[slot] = fw;
+              f_dir = kForward;
               iso_ep = -1;                         // tau only
             } else {
               double xx, xy, xz, unused;
@@ -372,7 +387,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
               rz = R.lo[2] + R.w[2] * xz;
               iso_ep = 0;                          // epoch-0 direction (block 1) in the shared tail
             }
-            sx[slot] = rx; sy[slot] = ry; sz[slot] = rz;
+            if (!kForward) { sx[slot] = rx; sy[slot] = ry; sz[slot] = rz; }   // else MOVE stores it
             sepoch[slot] = 0; snseg[slot] = 0; sos[slot] = -1; sosl[slot] = -1;
             if (TRACE) spl[slot] = -2;
           } else {
@@ -430,8 +445,12 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
           else ok = du >= 0 && descend<kStoreT>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh, fsense, L, mc, flags);
           done = true;
           if (!ok) flags |= NT_F3;
-          sflags[slot] = static_cast<uint8_t>(flags);
+          if (!kForward || !ok) sflags[slot] = static_cast<uint8_t>(flags);   // ok + kForward: MOVE stores it
           if (ok) { sL[slot] = static_cast<uint8_t>(L); smc[slot] = mc; }
+          if (kForward) {
+            fx = rx; fy = ry; fz = rz; f_pos = true;
+            fflags = flags; fL = L; fmc = mc; f_desc = ok;
+          }
           if (TRACE) {
             const uint64_t pid = R.pid0 + sidx[slot];
             const int pl = spl[slot];
@@ -451,8 +470,10 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
           draw2(R.seed, R.pid0 + sidx[slot], static_cast<uint32_t>(iso_ep), 1, xmu, xphi);
           isotropic(xmu, xphi, u, v, w);
           su[slot] = u; sv[slot] = v; sw[slot] = w;
+          if (kForward) { fu = u; fv = v; fw = w; f_dir = true; }
         }
-        stau[slot] = -spec_log(xtau);
+        if (kForward) { ftau = -spec_log(xtau); f_tau = true; }   // MOVE stores it (the slot moves, or ends)
+        else stau[slot] = -spec_log(xtau);
       }
       const bool ready = kind == 5 || (done && ok) || scat;
       const bool ended_at_event = (done && !ok) || absorbed;
@@ -467,11 +488,15 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
           st.si = sib + slot;
           st.sT = sTb + slot;
           st.B = S;
-          double rx = sx[slot], ry = sy[slot], rz = sz[slot];
-          double u = su[slot], v = sv[slot], w = sw[slot];
-          double tau = stau[slot];
-          uint32_t flags = sflags[slot], nseg = snseg[slot];
-          const int L = sL[slot], mc = smc[slot];
+          double rx, ry, rz, u, v, w, tau;
+          uint32_t flags;
+          int L, mc;
+          if (f_pos) { rx = fx; ry = fy; rz = fz; } else { rx = sx[slot]; ry = sy[slot]; rz = sz[slot]; }
+          if (f_dir) { u = fu; v = fv; w = fw; } else { u = su[slot]; v = sv[slot]; w = sw[slot]; }
+          tau = f_tau ? ftau : stau[slot];
+          if (f_desc) { flags = fflags; L = fL; mc = fmc; }
+          else { flags = sflags[slot]; L = sL[slot]; mc = smc[slot]; }
+          uint32_t nseg = snseg[slot];
           int os_l = sosl[slot], os_s = sos[slot];
           if (nseg >= max_seg) {
             flags |= NT_F3;

@@ -31,6 +31,8 @@ ap.add_argument("--configs", default="c2,c3,c5r,c4,c5m")
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--max-particles", type=float, default=2e7)
 ap.add_argument("--st-particles", type=float, default=2e6, help="ST runs are slower; smaller batch")
+ap.add_argument("--min-particles", type=float, default=1e7,
+                help="rate batches at least this large (C1's BASELINE batch, 1e4, is launch-latency bound)")
 ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "dispatch.json"))
 a = ap.parse_args()
 
@@ -50,7 +52,7 @@ for cfg in a.configs.split(","):
         m = models[pseudo]
         if kw.get("tracker") == "rect" and not m.info["rect_specialisable"]:
             continue
-        n = int(min(n_cfg, a.st_particles if pseudo else a.max_particles))
+        n = int(a.st_particles if pseudo else min(max(n_cfg, a.min_particles), a.max_particles))
         out = torch.zeros(m.out_len, dtype=torch.float64, device="cuda")
         m.track(min(n, 100_000), seed=99, out=out, **kw)        # warm-up (module load, DP objects)
         torch.cuda.synchronize()

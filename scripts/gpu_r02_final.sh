@@ -17,5 +17,5 @@ timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/b
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu_launches_$R.csv \
     python bench.py --no-cpu-baseline --no-e2e --no-ratio > gpurun_out/ncu_launches_bench_$R.log 2>&1
 ROUND=$R bash scripts/gpu_r02_prof.sh
-timeout 1500 python scripts/dispatch_study.py --out gpurun_out/dispatch_$R.json > gpurun_out/dispatch_$R.log 2>&1
+timeout 1500 python scripts/dispatch_study.py --configs c1,c2,c3,c5r,c4,c5m --out gpurun_out/dispatch_$R.json > gpurun_out/dispatch_$R.log 2>&1
 echo done
