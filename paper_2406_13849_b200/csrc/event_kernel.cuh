@@ -75,7 +75,7 @@ constexpr bool kFramesRecompute = NT_FRAMES_RECOMPUTE != 0;
 // registers for the MOVE of the same slot instead of a shared-memory store and reload (bank
 // conflicts on every per-slot access: profiles/r02_ncu_analysis.md).  0: always reload.
 #ifndef NT_FORWARD
-#define NT_FORWARD 0
+#define NT_FORWARD 1
 #endif
 constexpr bool kForward = NT_FORWARD != 0;
 #ifndef NT_DEPTH_RINGS

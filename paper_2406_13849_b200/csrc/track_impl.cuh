@@ -108,11 +108,15 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
   for (int l = l0; l < kMaxDepth; ++l) {
     const DUniv* U = g.univ + u;
     const int kind = ld(&U->kind);
-    st.set_u(l, u, kind);
-    if (STORE_T) {
-      st.setT(l, 0, Tx);
-      st.setT(l, 1, Ty);
-      st.setT(l, 2, Tz);
+    // a CSG crossing re-descends from its own level: that level's universe and frame are already
+    // in the stack, unchanged
+    if (!(l == l0 && fh >= 0)) {
+      st.set_u(l, u, kind);
+      if (STORE_T) {
+        st.setT(l, 0, Tx);
+        st.setT(l, 1, Ty);
+        st.setT(l, 2, Tz);
+      }
     }
     const double x = rx - Tx, y = ry - Ty, z = rz - Tz;
     double tx, ty, tz;
