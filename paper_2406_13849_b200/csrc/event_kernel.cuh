@@ -70,6 +70,11 @@ __host__ __device__ constexpr int ring_size(int S) { return S <= 128 ? 128 : S <
 #define NT_FRAMES_RECOMPUTE 0
 #endif
 constexpr bool kFramesRecompute = NT_FRAMES_RECOMPUTE != 0;
+// Frames stored only below arrays; below a CSG level recomputed from the parent's frame and cell
+// translation (one uniform-ish load per axis instead of a bank-conflicted shared load).
+#ifndef NT_FRAMES_MIXED
+#define NT_FRAMES_MIXED 0
+#endif
 // EVENT -> MOVE forwarding: the position a descent or birth just read or made, the flags / depth /
 // material cell a descent produced, and the direction and tau a birth or scatter drew stay in
 // registers for the MOVE of the same slot instead of a shared-memory store and reload (bank
@@ -157,6 +162,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int nmc = g.n_mc, maxd = g.max_depth;
   constexpr bool kStoreT = RTK != 0 || DP || !kFramesRecompute;   // frames in shared memory
+  constexpr bool kMixedT = kStoreT && RTK == 0 && !DP && NT_FRAMES_MIXED != 0;
   // ---- carve shared memory (see event_smem_bytes)
   double* sx = reinterpret_cast<double*>(smem);
   double* sy = sx + S; double* sz = sy + S; double* su = sz + S; double* sv = su + S; double* sw = sv + S;
@@ -397,7 +403,9 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
             l0 = dsc & 15;
             fsense = (dsc >> 4) & 1;
             fh = (dsc >> 5) - 1;
-            if constexpr (kStoreT) {
+            if constexpr (kMixedT) {
+              frame_mixed(g, st, l0, Tx, Ty, Tz);
+            } else if constexpr (kStoreT) {
               Tx = st.T(l0, 0); Ty = st.T(l0, 1); Tz = st.T(l0, 2);
             } else {
               frame_of(g, st, l0, Tx, Ty, Tz);
@@ -442,7 +450,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
             }
             ok = du >= 0 && rect_descend<RTK == 1>(g, rg, st, l0, fh, fsense, rx, ry, rz, L, mc, flags);
           }
-          else ok = du >= 0 && descend<kStoreT>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh, fsense, L, mc, flags);
+          else ok = du >= 0 && descend<kStoreT, kMixedT>(g, st, l0, du, Tx, Ty, Tz, rx, ry, rz, fh, fsense, L, mc, flags);
           done = true;
           if (!ok) flags |= NT_F3;
           if (!kForward || !ok) sflags[slot] = static_cast<uint8_t>(flags);   // ok + kForward: MOVE stores it
@@ -512,6 +520,25 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
             } else {
               if constexpr (DP) {
                 for (int l = 0; l < L; ++l) level_distances_dp(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+              } else if constexpr (kMixedT) {
+                // stored frames below arrays, parent frame + cell translation below CSG levels
+                double Tx = 0.0, Ty = 0.0, Tz = 0.0;
+                int pkind = U_RECT, pcell = 0;
+                for (int l = 0; l < L; ++l) {
+                  if (l > 0) {
+                    if (pkind == U_CSG) {
+                      Tx = Tx + ld(g.cell_tr + 3 * pcell); Ty = Ty + ld(g.cell_tr + 3 * pcell + 1);
+                      Tz = Tz + ld(g.cell_tr + 3 * pcell + 2);
+                    } else {
+                      Tx = st.T(l, 0); Ty = st.T(l, 1); Tz = st.T(l, 2);
+                    }
+                  }
+                  const DUniv* U = g.univ + st.u(l);
+                  const int kind_l = st.ukind(l), ia = st.a(l), ib = st.b(l), ic = st.c(l);
+                  level_candidates(g, U, kind_l, ia, ib, ic, l, rx - Tx, ry - Ty, rz - Tz, u, v, w, os_l, os_s, b);
+                  pkind = kind_l;
+                  pcell = ia;
+                }
               } else if constexpr (kStoreT) {
                 for (int l = 0; l < L; ++l) level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
               } else {

@@ -91,7 +91,9 @@ __device__ __forceinline__ int winner_surface(const DevGeom& g, bool csg, int jb
 // out of the cell at level l0 through half-space entry fh; the crossed surface's sense is forced to
 // fsense at level l0 (O9') and the cells across it (hs_nb_off[fh]) are tested first.  Returns false
 // when a level has no cell (LOST).
-template <bool STORE_T = true>
+// MIXED (with STORE_T): frames are stored only for levels whose parent is an array; a level below a
+// CSG level has T_l = T_{l-1} + the parent cell's translation, recomputed by its readers (frame_mixed)
+template <bool STORE_T = true, bool MIXED = false>
 __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int u, double Tx, double Ty,
                                      double Tz, double rx, double ry, double rz, int fh, int fsense,
                                      int& L, int& mc, uint32_t& flags) {
@@ -104,6 +106,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
     nbl = g.nb_cells + k0;
     nnb = ld(g.hs_nb_off + fh + 1) - k0;
   }
+  bool parent_csg = false;           // MIXED: level l's parent is a CSG level (frame not stored)
 #pragma unroll 1
   for (int l = l0; l < kMaxDepth; ++l) {
     const DUniv* U = g.univ + u;
@@ -112,7 +115,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
     // in the stack, unchanged
     if (!(l == l0 && fh >= 0)) {
       st.set_u(l, u, kind);
-      if (STORE_T) {
+      if (STORE_T && !(MIXED && parent_csg)) {
         st.setT(l, 0, Tx);
         st.setT(l, 1, Ty);
         st.setT(l, 2, Tz);
@@ -132,6 +135,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
       st.c(l) = h1;
       if (f >= 0) { L = l + 1; mc = f; return true; }
       dau = -1 - f;
+      parent_csg = true;
       tx = ld(g.cell_tr + 3 * cell);
       ty = ld(g.cell_tr + 3 * cell + 1);
       tz = ld(g.cell_tr + 3 * cell + 2);
@@ -140,6 +144,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
       rect_locate(g, U, x, y, z, i, j, k, flags);
       st.a(l) = i; st.b(l) = j; st.c(l) = k;
       dau = array_daughter(g, U, U_RECT, i, j, k, tx, ty, tz);
+      parent_csg = false;
     } else {
       int q, r, k = 0;
       hex_locate(U, x, y, q, r, flags);
@@ -150,6 +155,7 @@ __device__ __forceinline__ bool descend(const DevGeom& g, Stack& st, int l0, int
       }
       st.a(l) = q; st.b(l) = r; st.c(l) = k;
       dau = array_daughter(g, U, U_HEX, q, r, k, tx, ty, tz);
+      parent_csg = false;
     }
     if (dau < 0) return false;
     Tx = Tx + tx;
@@ -215,6 +221,19 @@ __device__ __forceinline__ void level_translation(const DevGeom& g, const DUniv*
     tz = ld(g.cell_tr + 3 * ia + 2);
   } else {
     array_centre(g, U, kind, ia, ib, ic, tx, ty, tz);
+  }
+}
+
+// frame T_l under the MIXED policy: the nearest stored frame at or above l (or T_0 = 0), plus the
+// translations of the CSG cells below it, added in level order as the descent did
+__device__ __forceinline__ void frame_mixed(const DevGeom& g, Stack& st, int l, double& Tx, double& Ty, double& Tz) {
+  int k = l;
+  while (k > 0 && st.ukind(k - 1) == U_CSG) --k;       // level k's frame is stored (or k == 0)
+  Tx = st.T(k, 0); Ty = st.T(k, 1); Tz = st.T(k, 2);
+#pragma unroll 1
+  for (int m = k; m < l; ++m) {
+    const int c = st.a(m);
+    Tx = Tx + ld(g.cell_tr + 3 * c); Ty = Ty + ld(g.cell_tr + 3 * c + 1); Tz = Tz + ld(g.cell_tr + 3 * c + 2);
   }
 }
 
