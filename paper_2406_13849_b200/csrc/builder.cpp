@@ -701,6 +701,8 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
       F.hs.push_back(hs_pack(c.sid[k], S[c.sid[k]].kind, c.sense[k]));
       DHs r{};
       for (int q = 0; q < 4; ++q) r.c[q] = F.surf[c.sid[k]].c[q];
+      // CZ: c3 (unused by f and the distance) carries R for the safety bound |rho - R|
+      if (S[c.sid[k]].kind == S_CZ) r.c[3] = std::sqrt(r.c[2]);
       r.e = F.hs.back();
       r.meta = F.surf_meta[c.sid[k]];
       r.tol = F.surf_tol[c.sid[k]];

@@ -67,7 +67,7 @@ __host__ __device__ constexpr int ring_size(int S) { return S <= 128 ? 128 : S <
 // the stack's cells / tiles with the descent's own arithmetic (NT_FRAMES_RECOMPUTE: 72 B less per
 // slot at depth 4, so that four 256-thread blocks fit an SM).  Bit-identical either way.
 #ifndef NT_FRAMES_RECOMPUTE
-#define NT_FRAMES_RECOMPUTE 0
+#define NT_FRAMES_RECOMPUTE (NT_FEAT != 0)   // f7 (hex / plane / sphere models): recomputed, for more slots
 #endif
 constexpr bool kFramesRecompute = NT_FRAMES_RECOMPUTE != 0;
 // Frames stored only below arrays; below a CSG level recomputed from the parent's frame and cell
@@ -86,17 +86,47 @@ constexpr bool kForward = NT_FORWARD != 0;
 #ifndef NT_DEPTH_RINGS
 #define NT_DEPTH_RINGS 1     // depth-class rings (NR = 7) for the f7 feature set (0: five rings everywhere)
 #endif
+// depth-class rings for the f0 feature set as well (with the safety skip, a chunk that mixes depths
+// runs the shallow lanes' upper levels beside the deep lanes' lower ones)
+#ifndef NT_DEPTH_RINGS_F0
+#define NT_DEPTH_RINGS_F0 0
+#endif
+// Safety skip of the upper levels: MOVE evaluates levels [lk, L) with lk = L - 2 and
+// skips levels [0, lk) when the slot's stored safety bound proves that none of their candidates can
+// win, tie or near-tie; otherwise the slot is deferred with its partial winner to the U ring, whose
+// chunks evaluate the upper levels, merge, and refresh the bound.  Bit-identical to evaluating all
+// levels.  0: every MOVE evaluates every level.
+#ifndef NT_SAFETY
+#define NT_SAFETY 0          // measured slower on every config (profiles/r02_experiments.md rows 54-57)
+#endif
+constexpr bool kSafeSP = NT_SAFETY != 0 && !kFramesRecompute && NT_FRAMES_MIXED == 0;   // SP ring kernels
+// slots per block of the big-slot ring variant: 320 with stored frames (288 with the safety skip's 12
+// extra bytes per slot and its ring), 384 with recomputed frames (147 B per slot at depth 4), so that
+// three 256-thread blocks still fit an SM at depth <= 4
+#ifndef NT_SLOTS_BIG
+#define NT_SLOTS_BIG (kFramesRecompute ? 384 : kSafeSP ? 288 : 320)
+#endif
+constexpr int kSlotsBig = NT_SLOTS_BIG;
+// levels the safety skip covers at most: lk = min(NT_SAFE_K, L - 2) (the two deepest levels are
+// always evaluated)
+#ifndef NT_SAFE_K
+#define NT_SAFE_K 2
+#endif
+constexpr int kQN = 18;              // ints for ring heads / tails (2 * rings <= 16) or rounds queue counts (3 NQ)
+constexpr double kSafeRel = 1e-6;    // skip only if safety * (1 - kSafeRel) > d_lower + kSafeAbs
+constexpr double kSafeAbs = 1e-9;    // (cm) > kFlagDist: the F2 near-tie window stays exact
 
-size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false, bool store_t = true, int nr = NQ) {
+size_t event_smem_bytes(const DevGeom& g, int B, bool trace, bool async = false, bool store_t = true, int nr = NQ,
+                        bool safety = false) {
   const size_t nmc = g.n_mc, d = g.max_depth;
   size_t s = 0;
-  s += (7 + (store_t ? 3 * (d - 1) : 0) + (trace ? 1 : 0)) * 8 * (size_t)B;   // doubles (T from level 1)
-  s += (6 + 4 * d + (trace ? 2 : 0)) * 4 * (size_t)B;                 // ints
+  s += (7 + (store_t ? 3 * (d - 1) : 0) + (trace ? 1 : 0) + (safety ? 1 : 0)) * 8 * (size_t)B;   // doubles (T from level 1)
+  s += (6 + 4 * d + (trace ? 2 : 0) + (safety ? 1 : 0)) * 4 * (size_t)B;   // ints
   s += (3 + (trace ? 1 : 0)) * (size_t)B;                             // bytes
   s = (s + 15) & ~size_t(15);
-  if (async) s += nr * sizeof(uint16_t) * (size_t)ring_size(B);        // ring queues
+  if (async) s += (nr + (safety ? 1 : 0)) * sizeof(uint16_t) * (size_t)ring_size(B);   // ring queues
   else s += 3 * NQ * sizeof(QIdx) * (size_t)B;                        // queues (triple-buffered)
-  s += (nmc + kNC + 3 * NQ + 4) * 4;                                    // exits, counters, queue counts
+  s += (nmc + kNC + kQN + 4) * 4;                                       // exits, counters, queue counts
   return (s + 15) & ~size_t(15);
 }
 
@@ -122,6 +152,16 @@ __device__ __forceinline__ void vstore(uint16_t* p, uint32_t v) {
 // its position (see above) and waits only for the lap-(L-1) producer: by induction the oldest
 // in-progress position of every entry can always advance.  (tail - head <= S <= RB, so when p is
 // allocated the head is past p - RB.)
+// stored safety word: a float at or below the bound with the covered level count in its three low
+// mantissa bits.  v (1 - 2^-40) rounded down to float stays below the exact v despite the rounding of
+// the running subtraction that produced v; clearing the low bits and stepping 8 ulp down keeps the
+// value with the count OR-ed in below it.  0 = no bound.
+__device__ __forceinline__ uint32_t ss_pack(double v, int cov) {
+  const float f = __double2float_rd(v * (1.0 - 0x1p-40));
+  const uint32_t m = f > 1e-30f ? (__float_as_uint(f) & ~7u) - 8u : 0u;
+  return m | static_cast<uint32_t>(cov);
+}
+
 constexpr uint32_t kRingFree = 511u;
 __device__ __forceinline__ uint32_t ring_tag(uint32_t pos, int log2rb) { return ((pos >> log2rb) & 127u) << 9; }
 __device__ __forceinline__ void ring_publish(uint16_t* e, uint32_t pos, int log2rb, int slot) {
@@ -163,13 +203,19 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
   const int nmc = g.n_mc, maxd = g.max_depth;
   constexpr bool kStoreT = RTK != 0 || DP || !kFramesRecompute;   // frames in shared memory
   constexpr bool kMixedT = kStoreT && RTK == 0 && !DP && NT_FRAMES_MIXED != 0;
+  // safety skip of the upper levels: generic SP tracker on the ring scheduler with stored frames
+  constexpr bool kSafe = kSafeSP && ASYNC && !DP && RTK == 0 && kStoreT && !kMixedT;
+  constexpr int NRT = NR + (kSafe ? 1 : 0);     // rings, the U ring (deferred upper levels) last
+  constexpr int QU = NR;
+  static_assert(2 * NRT <= kQN, "ring heads and tails");
   // ---- carve shared memory (see event_smem_bytes)
   double* sx = reinterpret_cast<double*>(smem);
   double* sy = sx + S; double* sz = sy + S; double* su = sz + S; double* sv = su + S; double* sw = sv + S;
   double* stau = sw + S;
   double* sTb = stau + S;                           // [maxd-1][3][S] (T_0 = 0)
   double* sps = sTb + (kStoreT ? 3 * (maxd - 1) * S : 0);   // TRACE: pending segment length
-  uint32_t* sidx = reinterpret_cast<uint32_t*>(sps + (TRACE ? S : 0));
+  double* sdl = sps + (TRACE ? S : 0);              // kSafe: deferred slot's lower-level winner distance
+  uint32_t* sidx = reinterpret_cast<uint32_t*>(sdl + (kSafe ? S : 0));
   uint32_t* sepoch = sidx + S; uint32_t* snseg = sepoch + S;
   int32_t* smc = reinterpret_cast<int32_t*>(snseg + S);
   int32_t* sos = smc + S;                           // on-surface sid (-1 none)
@@ -177,7 +223,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
   int32_t* sib = sdesc + S;                         // [maxd][4][S]
   int32_t* spj = sib + 4 * maxd * S;                // TRACE: pending j, cell_before
   int32_t* spcb = spj + (TRACE ? S : 0);
-  uint8_t* sflags = reinterpret_cast<uint8_t*>(spcb + (TRACE ? S : 0));
+  uint32_t* sss = reinterpret_cast<uint32_t*>(spcb + (TRACE ? S : 0));   // kSafe: safety word (see ss_pack)
+  uint8_t* sflags = reinterpret_cast<uint8_t*>(sss + (kSafe ? S : 0));
   uint8_t* sL = sflags + S;
   int8_t* sosl = reinterpret_cast<int8_t*>(sL + S);
   int8_t* spl = sosl + S;                           // TRACE: pending level
@@ -187,21 +234,21 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
   constexpr int RB = ring_size(S);
   constexpr int kLog2RB = RB == 128 ? 7 : RB == 256 ? 8 : 9;
   static_assert(S <= 510 && (1 << kLog2RB) == RB, "ring entries hold slot <= 510");
-  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + off);  // [NR][RB] lap-tagged entries (ASYNC)
-  unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NR * RB)
+  uint16_t* ring = reinterpret_cast<uint16_t*>(smem + off);  // [NRT][RB] lap-tagged entries (ASYNC)
+  unsigned int* s_exit = ASYNC ? reinterpret_cast<unsigned int*>(ring + NRT * RB)
                                : reinterpret_cast<unsigned int*>(sq + 3 * NQ * S);
   unsigned int* s_cnt = s_exit + nmc;
-  int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [3][NQ]
-  int* s_flag = s_qn + 3 * NQ;                              // [0] = pids exhausted, [1] live (ASYNC)
-  uint32_t* a_head = reinterpret_cast<uint32_t*>(s_qn);      // ASYNC: [NR] heads, [NR] tails (2 NR <= 3 NQ)
-  uint32_t* a_tail = a_head + NR;
+  int* s_qn = reinterpret_cast<int*>(s_cnt + kNC);          // [3][NQ] (rounds)
+  int* s_flag = s_qn + kQN;                                 // [0] = pids exhausted, [1] live (ASYNC)
+  uint32_t* a_head = reinterpret_cast<uint32_t*>(s_qn);      // ASYNC: [NRT] heads, [NRT] tails (2 NRT <= kQN)
+  uint32_t* a_tail = a_head + NRT;
   double* gl = R.slices + (size_t)blockIdx.x * nmc;         // per-block track-length tally (global)
 
   for (int i = tid; i < nmc; i += B) s_exit[i] = 0u;
   for (int i = tid; i < kNC; i += B) s_cnt[i] = 0u;
-  if (tid < 3 * NQ) s_qn[tid] = (!ASYNC && tid == 0 * NQ + Q_F) ? B : 0;   // rounds: round 0 reads set 0, all free
+  if (tid < kQN) s_qn[tid] = (!ASYNC && tid == 0 * NQ + Q_F) ? B : 0;   // rounds: round 0 reads set 0, all free
   if (ASYNC) {
-    for (int i = tid; i < NR * RB; i += B) ring[i] = static_cast<uint16_t>(kRingFree);     // FREE(lap 0)
+    for (int i = tid; i < NRT * RB; i += B) ring[i] = static_cast<uint16_t>(kRingFree);     // FREE(lap 0)
     __syncthreads();
     for (int i = tid; i < S; i += B) ring[Q_F * RB + i] = static_cast<uint16_t>(i);        // FULL(lap 0): all slots free
     if (tid == 0) { a_tail[Q_F] = S; s_flag[0] = 0; s_flag[1] = 0; }
@@ -241,7 +288,8 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
     }
     for (int base = ASYNC ? 0 : warp * 32; base < total; base += B) {
       const int i = base + lane;
-      // kind: 5 move only (reflected), 4 collide, 0 CSG descent, 1 array descent, 2 birth, 3 none
+      // kind: 5 move only (reflected), 4 collide, 0 CSG descent, 1 array descent, 2 birth, 3 none,
+      // 6 deferred MOVE (kSafe: upper levels + merge)
       int slot = 0, kind = 3;
       bool valid = i < total;
       if constexpr (ASYNC) {
@@ -252,7 +300,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         for (;;) {
           const bool births = vload(reinterpret_cast<uint32_t*>(s_flag)) == 0u;
           uint32_t hk = 0, av = 0;
-          if (lane < NR && (lane != Q_F || births)) { hk = vload(a_head + lane); av = vload(a_tail + lane) - hk; }
+          if (lane < NRT && (lane != Q_F || births)) { hk = vload(a_head + lane); av = vload(a_tail + lane) - hk; }
           const uint32_t mx = __reduce_max_sync(0xffffffffu, (av << 8) | static_cast<uint32_t>(255 - lane));
           const uint32_t bav = mx >> 8;                  // av <= S slots (< 2^24): fits above the lane byte
           if (bav > 0u) {
@@ -271,7 +319,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         valid = static_cast<uint32_t>(lane) < take;
         if (valid) {
           slot = ring_take(ring + q * RB + ((h + lane) & (RB - 1)), h + lane, kLog2RB);
-          kind = ring_kind(q);                       // Q_M, Q_C, Q_DC, Q_DA, Q_F (, Q_C2, Q_DC2) -> 5 4 0 1 2 (4 0)
+          kind = kSafe && q == QU ? 6 : ring_kind(q);   // Q_M, Q_C, Q_DC, Q_DA, Q_F (, Q_C2, Q_DC2) (, Q_U) -> 5 4 0 1 2 (4 0) (6)
         }
         __threadfence_block();
       } else if (valid) {
@@ -483,12 +531,13 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
         if (kForward) { ftau = -spec_log(xtau); f_tau = true; }   // MOVE stores it (the slot moves, or ends)
         else stau[slot] = -spec_log(xtau);
       }
-      const bool ready = kind == 5 || (done && ok) || scat;
+      const bool ready = kind == 5 || kind == 6 || (done && ok) || scat;
       const bool ended_at_event = (done && !ok) || absorbed;
       if (!ASYNC) push(Q_F, ended_at_event);
       // ---------------- MOVE the same slots (no barrier between a slot's event and its move)
       {
-        // outcome: 0 none, 1 reflect (-> M), 2 collide, 3 CSG descent, 4 array descent, 5 ended
+        // outcome: 0 none, 1 reflect (-> M), 2 collide, 3 CSG descent, 4 array descent, 5 ended,
+        // 6 deferred to the U ring (kSafe: upper levels still to evaluate)
         int outc = 0, term = NT_T_NONE, lcross = -1;
         bool seg = false;
         if (ready) {
@@ -515,6 +564,13 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
           } else {
             Best b;
             b.init();
+            // kSafe modes: 0 LOWER (levels [lk, L), then skip or defer), 1 UPPER (U ring: levels [0, lk)
+            // merged with the deferred lower winner), 2 FULL (births: every level)
+            const int mode = !kSafe ? 2 : kind == 6 ? 1 : kind == 2 ? 2 : 0;
+            const int lk = kSafe && L >= 3 ? min(NT_SAFE_K, L - 2) : 0;   // upper levels [0, lk)
+            double lb = NT_INF;                                 // safety bound of [0, lk) (modes 1, 2)
+            uint32_t ssw = 0;                                   // stored safety word (mode 0)
+            bool near2 = false, defer = false;                  // O16 F2 runner-up test; mode 0 deferral
             if constexpr (RTK != 0) {
               rect_distances<RTK == 1>(g, rg, st, L, rx, ry, rz, u, v, w, os_l, os_s, b);
             } else {
@@ -539,6 +595,12 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
                   pkind = kind_l;
                   pcell = ia;
                 }
+              } else if constexpr (kSafe) {
+                // the main loop is the plain one over [la, lz); the upper levels' safety bound is a
+                // separate pass, run only by U-ring chunks and births (keeps the loop's registers)
+                for (int l = mode == 0 ? lk : 0; l < (mode == 1 ? lk : L); ++l)
+                  level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
+                if (mode != 0 && lk > 0) lb = upper_safety(g, st, lk, rx, ry, rz);
               } else if constexpr (kStoreT) {
                 for (int l = 0; l < L; ++l) level_distances(g, st, l, rx, ry, rz, u, v, w, os_l, os_s, b);
               } else {
@@ -556,11 +618,55 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
                 }
               }
             }
+            if (kSafe && mode == 1) {
+              // merge with the deferred lower winner (levels [lk, L), evaluated after [0, lk) in the
+              // canonical order: it wins only strictly).  F2: the runner-up of the union, via the
+              // lower part's code (0: tie, 1: runner-up gap in (0, 1e-10], 2: larger)
+              const double dl = sdl[slot];
+              const int kl = sdesc[slot];
+              const int code = (kl >> 30) & 3;
+              if (dl < b.d) {
+                near2 = code == 1 || (code == 2 && b.d - dl <= kFlagDist);
+                b.d = dl;
+                b.key = kl & 0x3FFFFFFF;
+              } else {
+                const double g2 = (dl < b.d2 ? dl : b.d2) - b.d;
+                near2 = g2 > 0.0 && g2 <= kFlagDist;
+              }
+            } else {
+              const double g2 = b.d2 - b.d;
+              near2 = g2 > 0.0 && g2 <= kFlagDist;
+              if (kSafe && mode == 0 && lk > 0) {
+                // skip [0, lk) iff the stored bound covers them and exceeds the lower winner by the margins
+                ssw = sss[slot];
+                const double ss = static_cast<double>(__uint_as_float(ssw));
+                defer = !(static_cast<int>(ssw & 7u) >= lk && (os_l < 0 || os_l >= lk) &&
+                          ss * (1.0 - kSafeRel) > b.d + kSafeAbs);
+              }
+            }
             const double sig = ld(g.mc_st + mc);
             const double ds = b.d;
             const double dc = sig > 0.0 ? fdiv(tau, sig) : NT_INF;
-            const double g2 = b.d2 - ds, gc = fabs(dc - ds);
-            if ((g2 > 0.0 && g2 <= kFlagDist) || (gc > 0.0 && gc <= kFlagDist)) flags |= NT_F2;
+            const double gc = fabs(dc - ds);
+#ifdef NT_SAFETY_STATS
+            // diagnostic build: cross_l4..l7 count mode-0 MOVEs with upper levels, deferrals, deferrals
+            // for lack of a covering bound, U-ring MOVEs (the crossing total is then off)
+            if (kSafe && mode == 0 && lk > 0) {
+              atomicAdd(s_cnt + C_CBL0 + 4, 1u);
+              if (defer) atomicAdd(s_cnt + C_CBL0 + 5, 1u);
+              if (defer && static_cast<int>(ssw & 7u) < lk) atomicAdd(s_cnt + C_CBL0 + 6, 1u);
+            }
+            if (kSafe && mode == 1) atomicAdd(s_cnt + C_CBL0 + 7, 1u);
+#endif
+            if (defer) {
+              // U ring: lower winner and its runner-up code; the slot's state is stored below unchanged
+              const double g2l = b.d2 - b.d;
+              const int code = g2l == 0.0 ? 0 : g2l <= kFlagDist ? 1 : 2;
+              sdl[slot] = b.d;
+              sdesc[slot] = (b.key & 0x3FFFFFFF) | (code << 30);
+              outc = 6;
+            } else {
+            if (near2 || (gc > 0.0 && gc <= kFlagDist)) flags |= NT_F2;
             const int cell_before = TRACE ? ld(g.mc_cell + mc) : 0;
             if (ds == NT_INF && dc == NT_INF) {
               flags |= NT_F3;
@@ -618,7 +724,19 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
                 os_l = -1; os_s = -1;
                 outc = 2;
               }
+              if constexpr (kSafe) {
+                // new safety of [0, cov): the bound at the pre-move point minus the path flown; a
+                // reflection or a crossing at a covered level changes those levels: no bound
+                uint32_t nw = 0;
+                if (lk > 0 && outc != 5) {
+                  const int cov = mode == 0 ? static_cast<int>(ssw & 7u) : lk;
+                  const double base = mode == 0 ? static_cast<double>(__uint_as_float(ssw)) : lb;
+                  if (!(outc == 1 || (cross && b.l() < cov))) nw = ss_pack(base - s, cov);
+                }
+                sss[slot] = nw;
+              }
             }
+            }   // not deferred
           }
           sx[slot] = rx; sy[slot] = ry; sz[slot] = rz;
           if (outc == 1) { su[slot] = u; sv[slot] = v; sw[slot] = w; }   // only a reflection turns the flight
@@ -637,7 +755,7 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
           // NR = 7: histories above the deepest level take the second set of rings (depth class)
           const bool cls = NR == 7 && ready && sL[slot] < maxd;
           push_all(ended_at_event || outc == 5 ? Q_F : outc == 1 ? Q_M : outc == 2 ? (cls ? Q_C2 : Q_C)
-                   : outc == 3 ? (cls ? Q_DC2 : Q_DC) : outc == 4 ? Q_DA : -1);
+                   : outc == 3 ? (cls ? Q_DC2 : Q_DC) : outc == 4 ? Q_DA : (kSafe && outc == 6) ? QU : -1);
         } else {
           push(Q_M, outc == 1);
           push(Q_C, outc == 2);

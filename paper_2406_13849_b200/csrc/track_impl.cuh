@@ -212,6 +212,80 @@ __device__ __forceinline__ void level_distances(const DevGeom& g, Stack& st, int
   level_candidates(g, g.univ + st.u(l), st.ukind(l), st.a(l), st.b(l), st.c(l), l, x, y, z, u, v, w, os_l, os_s, b);
 }
 
+// ---- safety bound of a level: a lower bound on the Euclidean distance from the local
+// point to every surface that can bound level l's current cell / tile.  Every distance candidate of
+// the level is a ray distance to one of these surfaces along a (unit) direction, hence >= it.  The
+// bound depends on the position only, so it stays valid (minus the path flown) across collisions.
+// Plain |f|-style distances: rounding errors are covered by the relative / absolute margin of the
+// skip test (kSafeRel, kSafeAbs in event_kernel.cuh).
+__device__ __forceinline__ double hs_safety(int kind, double c0, double c1, double c2, double c3, double x, double y,
+                                            double z) {
+  if (kind <= S_PZ) return fabs(sel3(kind, x, y, z) - c0);
+  if (kPlane && kind == S_PLANE) return fdiv(fabs(((c0 * x + c1 * y) + c2 * z) - c3), fsqrt((c0 * c0 + c1 * c1) + c2 * c2));
+  const double dx = x - c0, dy = y - c1;
+  if (!kSphere || kind == S_CZ) return fabs(fsqrt(dx * dx + dy * dy) - c3);        // CZ: c3 = R (builder)
+  const double dz = z - c2;
+  return fabs(fsqrt((dx * dx + dy * dy) + dz * dz) - fsqrt(c3));
+}
+
+// safety bound of level l in its local frame (the level's cell / tile as kept in the stack)
+__device__ __forceinline__ double level_safety(const DevGeom& g, const DUniv* U, int kind, int ia, int ib, int ic,
+                                               double x, double y, double z) {
+  double s = NT_INF;
+  if (kind == U_CSG) {
+#pragma unroll 1
+    for (int h = ib; h < ic; ++h) {
+      const DHs* r = g.hsr + h;
+      const double2 c01 = __ldg(reinterpret_cast<const double2*>(r->c));
+      const double2 c23 = __ldg(reinterpret_cast<const double2*>(r->c + 2));
+      s = fmin(s, hs_safety(hs_kind(ld(&r->e)), c01.x, c01.y, c23.x, c23.y, x, y, z));
+    }
+  } else if (!kHex || kind == U_RECT) {
+    if (kRectNU && ld(&U->ntile) >= 0) {
+      const int n0 = ld(&U->i0), n1 = ld(&U->i1);
+      const double* ex = g.edges + ld(&U->ntile);
+      const double* ey = ex + n0 + 1;
+      auto nu = [&](const double* e, int n, int i, double p) {
+        const double lo = i >= 0 ? p - ld(e + i) : NT_INF, hi = i + 1 <= n ? ld(e + i + 1) - p : NT_INF;
+        return fmin(lo, hi);
+      };
+      s = fmin(nu(ex, n0, ia, x), nu(ey, n1, ib, y));
+      if (!ld(&U->is2d)) s = fmin(s, nu(ey + n1 + 1, ld(&U->i2), ic, z));
+    } else {
+      const double llx = ld(&U->d[0]), lly = ld(&U->d[1]), px = ld(&U->d[3]), py = ld(&U->d[4]);
+      s = fmin(fmin(x - (llx + static_cast<double>(ia) * px), (llx + static_cast<double>(ia + 1) * px) - x),
+               fmin(y - (lly + static_cast<double>(ib) * py), (lly + static_cast<double>(ib + 1) * py) - y));
+      if (!ld(&U->is2d)) {
+        const double llz = ld(&U->d[2]), pz = ld(&U->d[5]);
+        s = fmin(s, fmin(z - (llz + static_cast<double>(ic) * pz), (llz + static_cast<double>(ic + 1) * pz) - z));
+      }
+    }
+  } else {
+    // hex faces: n_k . (x - C) = p (m_k +- 1/2) with unit n_k (builder), then the z walls
+    double t0, t1, t2, m0, m1, m2;
+    hex_t(U, x, y, t0, t1, t2);
+    hex_m(ia, ib, m0, m1, m2);
+    const double p = ld(&U->d[2]);
+    s = fmin(fmin(t0 - p * (m0 - 0.5), p * (m0 + 0.5) - t0),
+             fmin(fmin(t1 - p * (m1 - 0.5), p * (m1 + 0.5) - t1), fmin(t2 - p * (m2 - 0.5), p * (m2 + 0.5) - t2)));
+    if (ld(&U->i1) > 0) {
+      const double llz = ld(&U->d[4]), pz = ld(&U->d[5]);
+      s = fmin(s, fmin(z - (llz + static_cast<double>(ic) * pz), (llz + static_cast<double>(ic + 1) * pz) - z));
+    }
+  }
+  return s;
+}
+
+// safety bound of the levels [0, lk) of the stack at the global point r
+__device__ __forceinline__ double upper_safety(const DevGeom& g, Stack& st, int lk, double rx, double ry, double rz) {
+  double s = NT_INF;
+#pragma unroll 1
+  for (int l = 0; l < lk; ++l)
+    s = fmin(s, level_safety(g, g.univ + st.u(l), st.ukind(l), st.a(l), st.b(l), st.c(l), rx - st.T(l, 0),
+                             ry - st.T(l, 1), rz - st.T(l, 2)));
+  return s;
+}
+
 // translation from the frame of level l to the frame of level l+1 (same arithmetic as descend)
 __device__ __forceinline__ void level_translation(const DevGeom& g, const DUniv* U, int kind, int ia, int ib,
                                                   int ic, double& tx, double& ty, double& tz) {
@@ -556,14 +630,17 @@ cudaError_t upload_coefficients(const double* host, int n) {
 // Slots per block of the ring scheduler (block 256, SP): 320 when NT_EVENT_MINB such blocks still
 // fit an SM (a warp that finishes its chunk then finds queued slots instead of waiting for the
 // chunks the other seven warps hold), else 256.  NESTRACK_SLOTS=256|320 overrides (tuning).
-static int ring_slots(const DevGeom& g, bool trace, bool store_t, int nr = NQ) {
+// big = 320 for the RTK kernels, kSlotsBig for the SP generic kernels (sp = true).
+static int ring_slots(const DevGeom& g, bool trace, bool store_t, int nr = NQ, bool safety = false, bool sp = true) {
   static const int env = [] { const char* e = getenv("NESTRACK_SLOTS"); return e ? atoi(e) : 0; }();
-  if (env == 256 || env == 320) return env;
+  const int big = sp ? kSlotsBig : 320;
+  if (env == 256) return 256;
+  if (env > 256) return big;
   int dev = 0, smem_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
-  const size_t need = NT_EVENT_MINB * (event_smem_bytes(g, 320, trace, true, store_t, nr) + 1024);
-  return need <= (size_t)smem_sm ? 320 : 256;
+  const size_t need = NT_EVENT_MINB * (event_smem_bytes(g, big, trace, true, store_t, nr, safety) + 1024);
+  return need <= (size_t)smem_sm ? big : 256;
 }
 
 // persistent launch of a ring / event-queue kernel: grid = SMs x occupancy (capped by the batch)
@@ -597,7 +674,7 @@ cudaError_t launch_rect_event(const DevGeom& g, const RectGeom& rg, const KRun& 
   if (R.inst) return cudaErrorNotSupported;
   const bool mesh = R.mesh != nullptr;
   if (mesh && trace) return cudaErrorNotSupported;
-  const bool s320 = !trace && !mesh && ring_slots(g, false, true) == 320;
+  const bool s320 = !trace && !mesh && ring_slots(g, false, true, NQ, false, false) == 320;
   const size_t smem = event_smem_bytes(g, s320 ? 320 : 256, trace, true);
   auto go = [&](auto kern) {
     return launch_event_kernel(kern, g, rg, R, 256, smem, blocks_per_sm, stream, grid_out);
@@ -718,38 +795,42 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
   if (tally && trace) return cudaErrorNotSupported;
   if (async && block == 192) {     // ring queues, 6 warps per block (more blocks per SM)
     if (g.trk || tally) return cudaErrorNotSupported;
+    smem = event_smem_bytes(g, block, trace, async, st_t, NQ, kSafeSP);
     if (trace) return states ? go(k_track_event<192, true, true, false, 0, true>) : go(k_track_event<192, true, false, false, 0, true>);
     return states ? go(k_track_event<192, false, true, false, 0, true>) : go(k_track_event<192, false, false, false, 0, true>);
   }
   if (async) {                     // barrier-free ring queues (block 256), SP or DP dispatch
     if (block != 256) return cudaErrorInvalidValue;
+    constexpr int SB = kSlotsBig;
     auto pick = [&](auto dp) -> cudaError_t {
       constexpr bool D = decltype(dp)::value;
-      if (!D && tally && ring_slots(g, false, st_t) == 320) {   // mesh / instance tallies: 320 slots as well
-        smem = event_smem_bytes(g, 320, false, true, st_t);
-        if (tally == 1) return states ? go(k_track_event<256, false, true, false, 1, true, 320>) : go(k_track_event<256, false, false, false, 1, true, 320>);
-        if (tally == 2) return states ? go(k_track_event<256, false, true, false, 2, true, 320>) : go(k_track_event<256, false, false, false, 2, true, 320>);
-        return states ? go(k_track_event<256, false, true, false, 3, true, 320>) : go(k_track_event<256, false, false, false, 3, true, 320>);
+      const bool sf = !D && kSafeSP;   // SP kernels carry the safety skip's per-slot state and U ring
+      smem = event_smem_bytes(g, 256, trace, true, st_t, NQ, sf);
+      if (!D && tally && ring_slots(g, false, st_t, NQ, sf) == SB) {   // mesh / instance tallies: big slots as well
+        smem = event_smem_bytes(g, SB, false, true, st_t, NQ, sf);
+        if (tally == 1) return states ? go(k_track_event<256, false, true, false, 1, true, SB>) : go(k_track_event<256, false, false, false, 1, true, SB>);
+        if (tally == 2) return states ? go(k_track_event<256, false, true, false, 2, true, SB>) : go(k_track_event<256, false, false, false, 2, true, SB>);
+        return states ? go(k_track_event<256, false, true, false, 3, true, SB>) : go(k_track_event<256, false, false, false, 3, true, SB>);
       }
       if (tally == 1) return states ? go(k_track_event<256, false, true, D, 1, true>) : go(k_track_event<256, false, false, D, 1, true>);
       if (tally == 2) return states ? go(k_track_event<256, false, true, D, 2, true>) : go(k_track_event<256, false, false, D, 2, true>);
       if (tally == 3) return states ? go(k_track_event<256, false, true, D, 3, true>) : go(k_track_event<256, false, false, D, 3, true>);
-#if NT_FEAT != 0 && NT_DEPTH_RINGS
+#if (NT_FEAT != 0 || NT_DEPTH_RINGS_F0) && NT_DEPTH_RINGS
       if (!D) {                    // hex / plane / sphere models: depth-class rings (NR = 7)
-        if (ring_slots(g, trace, st_t, 7) == 320) {
-          smem = event_smem_bytes(g, 320, trace, true, st_t, 7);
-          if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 320, 0, 7>) : go(k_track_event<256, true, false, false, 0, true, 320, 0, 7>);
-          return states ? go(k_track_event<256, false, true, false, 0, true, 320, 0, 7>) : go(k_track_event<256, false, false, false, 0, true, 320, 0, 7>);
+        if (ring_slots(g, trace, st_t, 7, sf) == SB) {
+          smem = event_smem_bytes(g, SB, trace, true, st_t, 7, sf);
+          if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, SB, 0, 7>) : go(k_track_event<256, true, false, false, 0, true, SB, 0, 7>);
+          return states ? go(k_track_event<256, false, true, false, 0, true, SB, 0, 7>) : go(k_track_event<256, false, false, false, 0, true, SB, 0, 7>);
         }
-        smem = event_smem_bytes(g, 256, trace, true, st_t, 7);
+        smem = event_smem_bytes(g, 256, trace, true, st_t, 7, sf);
         if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 256, 0, 7>) : go(k_track_event<256, true, false, false, 0, true, 256, 0, 7>);
         return states ? go(k_track_event<256, false, true, false, 0, true, 256, 0, 7>) : go(k_track_event<256, false, false, false, 0, true, 256, 0, 7>);
       }
 #endif
-      if (!D && ring_slots(g, trace, st_t) == 320) {
-        smem = event_smem_bytes(g, 320, trace, true, st_t);
-        if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, 320>) : go(k_track_event<256, true, false, false, 0, true, 320>);
-        return states ? go(k_track_event<256, false, true, false, 0, true, 320>) : go(k_track_event<256, false, false, false, 0, true, 320>);
+      if (!D && ring_slots(g, trace, st_t, NQ, sf) == SB) {
+        smem = event_smem_bytes(g, SB, trace, true, st_t, NQ, sf);
+        if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, SB>) : go(k_track_event<256, true, false, false, 0, true, SB>);
+        return states ? go(k_track_event<256, false, true, false, 0, true, SB>) : go(k_track_event<256, false, false, false, 0, true, SB>);
       }
       if (trace) return states ? go(k_track_event<256, true, true, D, 0, true>) : go(k_track_event<256, true, false, D, 0, true>);
       return states ? go(k_track_event<256, false, true, D, 0, true>) : go(k_track_event<256, false, false, D, 0, true>);
