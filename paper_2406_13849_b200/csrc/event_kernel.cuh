@@ -107,6 +107,24 @@ constexpr bool kSafeSP = NT_SAFETY != 0 && !kFramesRecompute && NT_FRAMES_MIXED 
 #define NT_SLOTS_BIG (kFramesRecompute ? 384 : kSafeSP ? 288 : 320)
 #endif
 constexpr int kSlotsBig = NT_SLOTS_BIG;
+// threads per block of the big-slot SP ring kernel without trace (tuning: fewer warps per block
+// leave more queued slots per warp)
+#ifndef NT_RING_THREADS
+#define NT_RING_THREADS 256
+#endif
+constexpr int kRingThreads = NT_RING_THREADS;
+// queues one chunk may draw from (1: the fullest only; 2: topped up from the next fullest)
+#ifndef NT_CLAIM_RINGS
+#define NT_CLAIM_RINGS 1     // 2 measured slower on C2 / C3 / C5r (profiles/r02_experiments.md row 62)
+#endif
+// a chunk smaller than NT_CLAIM_MIN waits (back-off) up to NT_CLAIM_WAIT times for its queue to fill
+#ifndef NT_CLAIM_MIN
+#define NT_CLAIM_MIN 0
+#endif
+#ifndef NT_CLAIM_WAIT
+#define NT_CLAIM_WAIT 0
+#endif
+constexpr int kClaimRings = NT_CLAIM_RINGS;
 // levels the safety skip covers at most: lk = min(NT_SAFE_K, L - 2) (the two deepest levels are
 // always evaluated)
 #ifndef NT_SAFE_K
@@ -193,7 +211,7 @@ __device__ __forceinline__ int ring_take(uint16_t* e, uint32_t pos, int log2rb) 
 #endif
 template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false, int S = B, int RTK = 0,
           int NR = NQ>
-__global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event(const DevGeom g, const KRun R, const RectGeom rg) {
+__global__ void __launch_bounds__(B, B >= 256 || S > B ? NT_EVENT_MINB : 5) k_track_event(const DevGeom g, const KRun R, const RectGeom rg) {
   static_assert(ASYNC || S == B, "round-based queues need one slot per thread");
   static_assert(RTK == 0 || (!DP && !(TALLY & 2)), "RTK: SP dispatch, no instance tallies");
   static_assert(NR == NQ || (ASYNC && NR == 7), "depth-class rings: ring scheduler only, 7 rings");
@@ -294,32 +312,60 @@ __global__ void __launch_bounds__(B, B >= 256 ? NT_EVENT_MINB : 5) k_track_event
       bool valid = i < total;
       if constexpr (ASYNC) {
         // ---- claim up to 32 entries of the fullest queue (lane 0), or finish
-        // lane k < NQ reads queue k; the fullest queue (lowest index on ties) wins a warp max-reduction
-        int q = -1;
-        uint32_t h = 0, take = 0;
+        // lane k < NQ reads queue k; the fullest queue (lowest index on ties) wins a warp max-reduction.
+        // Top-up (kClaimRings > 1): a chunk short of 32 takes the rest from the next fullest queue(s);
+        // lanes then run different EVENT kinds (each kind's code runs once, as in separate chunks),
+        // but one MOVE serves all of them.
+        int q = -1, q2 = -1;
+        uint32_t h = 0, take = 0, h2 = 0, take2 = 0;
+        int waits = 0;
         for (;;) {
           const bool births = vload(reinterpret_cast<uint32_t*>(s_flag)) == 0u;
           uint32_t hk = 0, av = 0;
           if (lane < NRT && (lane != Q_F || births)) { hk = vload(a_head + lane); av = vload(a_tail + lane) - hk; }
           const uint32_t mx = __reduce_max_sync(0xffffffffu, (av << 8) | static_cast<uint32_t>(255 - lane));
           const uint32_t bav = mx >> 8;                  // av <= S slots (< 2^24): fits above the lane byte
+          if (NT_CLAIM_MIN > 0 && bav > 0u && bav < NT_CLAIM_MIN && waits < NT_CLAIM_WAIT) {
+            ++waits;
+            __nanosleep(NT_RING_SLEEP_NS);
+            continue;
+          }
           if (bav > 0u) {
             const int best = 255 - static_cast<int>(mx & 255u);
             const uint32_t bh = __shfl_sync(0xffffffffu, hk, best);
             const uint32_t tk = bav < 32u ? bav : 32u;
             int won = 0;
             if (lane == 0) won = atomicCAS(a_head + best, bh, bh + tk) == bh;
-            if (__shfl_sync(0xffffffffu, won, 0)) { q = best; h = bh; take = tk; break; }
+            if (__shfl_sync(0xffffffffu, won, 0)) {
+              q = best; h = bh; take = tk;
+              if (kClaimRings > 1 && tk < 32u) {
+                // second fullest queue (availability as read above; the head CAS validates it)
+                const uint32_t a2 = lane == best ? 0u : av;
+                const uint32_t mx2 = __reduce_max_sync(0xffffffffu, (a2 << 8) | static_cast<uint32_t>(255 - lane));
+                if ((mx2 >> 8) > 0u) {
+                  const int b2 = 255 - static_cast<int>(mx2 & 255u);
+                  const uint32_t hb2 = __shfl_sync(0xffffffffu, hk, b2);
+                  const uint32_t want = 32u - tk, tk2 = (mx2 >> 8) < want ? (mx2 >> 8) : want;
+                  int won2 = 0;
+                  if (lane == 0) won2 = atomicCAS(a_head + b2, hb2, hb2 + tk2) == hb2;
+                  if (__shfl_sync(0xffffffffu, won2, 0)) { q2 = b2; h2 = hb2; take2 = tk2; }
+                }
+              }
+              break;
+            }
             continue;
           }
           if (!births && vload(reinterpret_cast<uint32_t*>(s_flag + 1)) == 0u) break;   // all done
           __nanosleep(NT_RING_SLEEP_NS);
         }
         if (q < 0) break;
-        valid = static_cast<uint32_t>(lane) < take;
+        valid = static_cast<uint32_t>(lane) < take + take2;
         if (valid) {
-          slot = ring_take(ring + q * RB + ((h + lane) & (RB - 1)), h + lane, kLog2RB);
-          kind = kSafe && q == QU ? 6 : ring_kind(q);   // Q_M, Q_C, Q_DC, Q_DA, Q_F (, Q_C2, Q_DC2) (, Q_U) -> 5 4 0 1 2 (4 0) (6)
+          const bool second = static_cast<uint32_t>(lane) >= take;
+          const int ql = second ? q2 : q;
+          const uint32_t pos = second ? h2 + (lane - take) : h + lane;
+          slot = ring_take(ring + ql * RB + (pos & (RB - 1)), pos, kLog2RB);
+          kind = kSafe && ql == QU ? 6 : ring_kind(ql);   // Q_M, Q_C, Q_DC, Q_DA, Q_F (, Q_C2, Q_DC2) (, Q_U) -> 5 4 0 1 2 (4 0) (6)
         }
         __threadfence_block();
       } else if (valid) {

@@ -830,6 +830,13 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
       if (!D && ring_slots(g, trace, st_t, NQ, sf) == SB) {
         smem = event_smem_bytes(g, SB, trace, true, st_t, NQ, sf);
         if (trace) return states ? go(k_track_event<256, true, true, false, 0, true, SB>) : go(k_track_event<256, true, false, false, 0, true, SB>);
+        if constexpr (kRingThreads != 256) {
+          auto gt = [&](auto kern) -> cudaError_t {
+            return launch_event_kernel(kern, g, no_rg, R, kRingThreads, smem, blocks_per_sm, stream, grid_out);
+          };
+          return states ? gt(k_track_event<kRingThreads, false, true, false, 0, true, SB>)
+                        : gt(k_track_event<kRingThreads, false, false, false, 0, true, SB>);
+        }
         return states ? go(k_track_event<256, false, true, false, 0, true, SB>) : go(k_track_event<256, false, false, false, 0, true, SB>);
       }
       if (trace) return states ? go(k_track_event<256, true, true, D, 0, true>) : go(k_track_event<256, true, false, D, 0, true>);
