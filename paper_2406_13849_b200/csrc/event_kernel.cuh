@@ -113,6 +113,9 @@ constexpr int kSlotsBig = NT_SLOTS_BIG;
 #define NT_RING_THREADS 256
 #endif
 constexpr int kRingThreads = NT_RING_THREADS;
+// deep models whose 320-slot blocks do not fit three to an SM (f0, depth 5): two blocks of 320 threads
+// with 400 slots each (the same 20 warps' worth of queued slots per warp as 320 / 256) instead of 256 slots
+constexpr int kDeepThreads = 320, kDeepSlots = 400;
 // queues one chunk may draw from (1: the fullest only; 2: topped up from the next fullest)
 #ifndef NT_CLAIM_RINGS
 #define NT_CLAIM_RINGS 1     // 2 measured slower on C2 / C3 / C5r (profiles/r02_experiments.md row 62)
@@ -211,7 +214,8 @@ __device__ __forceinline__ int ring_take(uint16_t* e, uint32_t pos, int log2rb) 
 #endif
 template <int B, bool TRACE, bool STATES, bool DP = false, int TALLY = 0, bool ASYNC = false, int S = B, int RTK = 0,
           int NR = NQ>
-__global__ void __launch_bounds__(B, B >= 256 || S > B ? NT_EVENT_MINB : 5) k_track_event(const DevGeom g, const KRun R, const RectGeom rg) {
+__global__ void __launch_bounds__(B, B == kDeepThreads && S == kDeepSlots ? 2 : B >= 256 || S > B ? NT_EVENT_MINB : 5)
+k_track_event(const DevGeom g, const KRun R, const RectGeom rg) {
   static_assert(ASYNC || S == B, "round-based queues need one slot per thread");
   static_assert(RTK == 0 || (!DP && !(TALLY & 2)), "RTK: SP dispatch, no instance tallies");
   static_assert(NR == NQ || (ASYNC && NR == 7), "depth-class rings: ring scheduler only, 7 rings");

@@ -839,6 +839,20 @@ cudaError_t launch_event(const DevGeom& g, const KRun& R, bool trace, bool state
         }
         return states ? go(k_track_event<256, false, true, false, 0, true, SB>) : go(k_track_event<256, false, false, false, 0, true, SB>);
       }
+      if (!D && !trace && !sf) {   // deep models: two 320-thread blocks of 400 slots per SM, if they fit
+        int dev = 0, smem_sm = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&smem_sm, cudaDevAttrMaxSharedMemoryPerMultiprocessor, dev);
+        const size_t sd = event_smem_bytes(g, kDeepSlots, false, true, st_t, NQ);
+        if (2 * (sd + 1024) <= (size_t)smem_sm) {
+          smem = sd;
+          auto gd = [&](auto kern) -> cudaError_t {
+            return launch_event_kernel(kern, g, no_rg, R, kDeepThreads, smem, blocks_per_sm, stream, grid_out);
+          };
+          return states ? gd(k_track_event<kDeepThreads, false, true, false, 0, true, kDeepSlots>)
+                        : gd(k_track_event<kDeepThreads, false, false, false, 0, true, kDeepSlots>);
+        }
+      }
       if (trace) return states ? go(k_track_event<256, true, true, D, 0, true>) : go(k_track_event<256, true, false, D, 0, true>);
       return states ? go(k_track_event<256, false, true, D, 0, true>) : go(k_track_event<256, false, false, D, 0, true>);
     };
