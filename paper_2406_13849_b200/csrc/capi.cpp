@@ -353,6 +353,7 @@ nt_status nt_finalize(nt_model* m, const nt_build_opts* o) {
     if (e == cudaSuccess) e = f0::upload_coefficients(coef, 30);
     if (e == cudaSuccess) e = f7::upload_coefficients(coef, 30);
     if (e == cudaSuccess) e = f0r::upload_coefficients(coef, 30);
+    if (e == cudaSuccess) e = fh::upload_coefficients(coef, 30);
     if (e != cudaSuccess) release_device(m);     // a failed finalize leaves nothing behind
     cudaSetDevice(prev);
     if (e != cudaSuccess) return cuda_err(e, "nt_finalize: upload");
@@ -621,6 +622,9 @@ static nt_status run_common(nt_model* m, const nt_run* run, const double* d_stat
     else if (run->flags & NT_WARPQ)
       e = f0 ? f0::launch_wq(m->g, R, trace, st, run->blocks_per_sm, s, &grid)
              : f7::launch_wq(m->g, R, trace, st, run->blocks_per_sm, s, &grid);
+    else if (!f0 && async && block == 256 && !trace && !R.mesh && !R.inst && !g.trk &&
+             (m->g.features & ~(F_HEX | F_PLANE)) == 0 && !getenv("NESTRACK_NO_FH"))
+      e = fh::launch_event_sp(g, R, st, run->blocks_per_sm, s, &grid);   // hex + plane models: smaller kernel
     else
       e = f0 ? f0::launch_event(g, R, trace, st, block, run->blocks_per_sm, s, &grid, async)
              : f7::launch_event(g, R, trace, st, block, run->blocks_per_sm, s, &grid, async);

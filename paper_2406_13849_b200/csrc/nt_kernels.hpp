@@ -55,6 +55,12 @@ cudaError_t launch_find_cells(const DevGeom& g, const double* xyz, uint64_t n, i
 
 namespace f0 { NT_LAUNCHERS }
 namespace f7 { NT_LAUNCHERS }
+// track_fh.cu: hex + general-plane models, default path only (own coefficient table)
+namespace fh {
+cudaError_t upload_coefficients(const double* host, int n);
+cudaError_t launch_event_sp(const DevGeom& g, const KRun& R, bool states, int blocks_per_sm, cudaStream_t stream,
+                            int* grid_out);
+}
 // track_rect.cu: the rect-specialised tracker under the ring scheduler (own coefficient table)
 namespace f0r {
 cudaError_t upload_coefficients(const double* host, int n);

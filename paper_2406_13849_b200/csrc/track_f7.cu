@@ -1,4 +1,7 @@
 // Kernels for models with any surface kind and hex arrays.
-#define NT_FEAT 15
+#ifndef NT_F7_FEAT
+#define NT_F7_FEAT 15
+#endif
+#define NT_FEAT NT_F7_FEAT
 #define NT_NS f7
 #include "track_impl.cuh"

@@ -574,7 +574,7 @@ NT_DEV_END
 #endif
 NT_DEV_BEGIN
 
-#ifndef NT_RECT_TU
+#if !defined(NT_RECT_TU) && !defined(NT_EVENT_TU)
 // point location for unit parity (Alg. 7)
 __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const double* xyz, uint64_t n,
                                                     int32_t* cell_out, uint8_t* flag_out) {
@@ -593,7 +593,7 @@ __global__ void __launch_bounds__(256) k_find_cells(const DevGeom g, const doubl
   }
 }
 
-#endif  // !NT_RECT_TU
+#endif  // !NT_RECT_TU && !NT_EVENT_TU
 
 // ---------------------------------------------------------------- host launchers
 size_t generic_smem_bytes(const DevGeom& g, int block) {
@@ -665,7 +665,28 @@ static cudaError_t launch_event_kernel(Kern kern, const DevGeom& g, const RectGe
   });
 }
 
-#ifdef NT_RECT_TU
+#ifdef NT_EVENT_TU
+// Feature set fh (track_fh.cu: hex arrays and general planes, no spheres or non-uniform rect
+// arrays): only the default path, the SP ring kernel without trace or tallies, so that its code is
+// ~15 % smaller than f7's (the f7 kernel stalls on instruction fetch: profiles/r02_ncu_analysis.md).
+// Everything else about such a model runs in f7.
+cudaError_t launch_event_sp(const DevGeom& g, const KRun& R, bool states, int blocks_per_sm, cudaStream_t stream,
+                            int* grid_out) {
+  if (g.trk || R.mesh || R.inst) return cudaErrorNotSupported;
+  const bool st_t = !kFramesRecompute;
+  const RectGeom no_rg{};
+  constexpr int SB = kSlotsBig;
+  auto go = [&](auto kern, int s) -> cudaError_t {
+    return launch_event_kernel(kern, g, no_rg, R, 256, event_smem_bytes(g, s, false, true, st_t, 7), blocks_per_sm,
+                               stream, grid_out);
+  };
+  if (ring_slots(g, false, st_t, 7) == SB)
+    return states ? go(k_track_event<256, false, true, false, 0, true, SB, 0, 7>, SB)
+                  : go(k_track_event<256, false, false, false, 0, true, SB, 0, 7>, SB);
+  return states ? go(k_track_event<256, false, true, false, 0, true, 256, 0, 7>, 256)
+                : go(k_track_event<256, false, false, false, 0, true, 256, 0, 7>, 256);
+}
+#elif defined(NT_RECT_TU)
 // Rect-specialised tracker (Alg. 9-10) under the ring scheduler: the same k_track_event as the
 // generic tracker, with the RTK's find_cell / distance code (rect_geom.cuh).  320 slots per block
 // when three blocks fit an SM (depth <= 4), else 256; trace and mesh runs use 256.
