@@ -26,7 +26,12 @@
 #include "nt_layout.hpp"
 #include "nt_math.cuh"
 
+#ifndef NT_HS_UNROLL
+#define NT_HS_UNROLL 1       // unroll of a CSG cell's half-space loop in distance_to_boundary (tuning)
+#endif
+
 NT_DEV_BEGIN
+constexpr int kHsUnroll = NT_HS_UNROLL;
 
 
 
@@ -172,7 +177,7 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
                                                  double v, double w, int os_l, int os_s, Best& b) {
   if (kind == U_CSG) {
     const int h0 = ib, h1 = ic;     // the cell's half-space range, kept in the stack by the descent
-#pragma unroll 1
+#pragma unroll kHsUnroll
     for (int h = h0; h < h1; ++h) {
       const DHs* r = g.hsr + h;
       const double2 c01 = __ldg(reinterpret_cast<const double2*>(r->c));

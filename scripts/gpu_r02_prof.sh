@@ -33,7 +33,7 @@ for c in c3 c4; do
 done
 cp paper_2406_13849_b200/libnestrack.so gpurun_out/libnestrack_$R.so
 fi
-for s in rounds dp rect-ring; do
+[ -n "$SKIP_SAN" ] || for s in rounds dp rect-ring; do
   timeout 600 compute-sanitizer --tool racecheck --print-limit 10 python scripts/sanitize.py --cfg c1 --n 200000 --scheds $s \
     > gpurun_out/racecheck_${R}_c1_$s.log 2>&1; echo "exit $?" >> gpurun_out/racecheck_${R}_c1_$s.log
 done

@@ -16,12 +16,12 @@ timeout 900 python bench.py > gpurun_out/bench_$R.json 2> gpurun_out/bench_$R.er
 timeout 900 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref_$R.json 2> gpurun_out/bench_ref_$R.err
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu_launches_$R.csv \
     python bench.py --no-cpu-baseline --no-e2e --no-ratio > gpurun_out/ncu_launches_bench_$R.log 2>&1
-ROUND=$R bash scripts/gpu_r02_prof.sh
-for c in c4 c5r; do
+ROUND=$R SKIP_SAN=1 bash scripts/gpu_r02_prof.sh
+[ -n "$SKIP_SAN" ] || for c in c4 c5r; do
   for t in memcheck synccheck; do
     timeout 900 compute-sanitizer --tool $t --print-limit 20 python scripts/sanitize.py --cfg $c --n 200000 --scheds block \
       > gpurun_out/sanitize_${t}_${c}_$R.log 2>&1; echo "exit $?" >> gpurun_out/sanitize_${t}_${c}_$R.log
   done
 done
-timeout 1500 python scripts/dispatch_study.py --configs c1,c2,c3,c5r,c4,c5m --out gpurun_out/dispatch_$R.json > gpurun_out/dispatch_$R.log 2>&1
+timeout 1500 python scripts/dispatch_study.py --configs ${DISPATCH:-c1,c2,c3,c5r,c4,c5m} --out gpurun_out/dispatch_$R.json > gpurun_out/dispatch_$R.log 2>&1
 echo done

@@ -553,3 +553,25 @@ def test_ring_slot_counts_agree(nt):
     la = np.array([float.fromhex(x) for x in a["len"]])
     lb = np.array([float.fromhex(x) for x in b["len"]])
     assert np.allclose(la, lb, rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("cfg", ["c4", "c5m"])
+def test_fh_kernel_equals_f7(nt, cfg, monkeypatch):
+    """Hex + general-plane models run the default path in the fh feature set (track_fh.cu, a smaller
+    kernel); NESTRACK_NO_FH=1 forces the f7 kernels.  Both must give identical walks: exact counters,
+    exits, per-history segment counts and terminals, bit-identical track-length totals."""
+    spec, _ = workloads.config(cfg)
+    m = nt.Model.from_spec(spec, device=0)
+    n = 300000   # >> resident slots: slots are recycled
+    outs = []
+    for off in (False, True):
+        if off:
+            monkeypatch.setenv("NESTRACK_NO_FH", "1")
+        res = m.track(n, seed=17, per_history=True)
+        torch.cuda.synchronize()
+        outs.append((m.unpack(res["out"]), res["pnseg"].cpu().numpy(), res["pterm"].cpu().numpy()))
+    (a, sa, ta), (b, sb, tb) = outs
+    assert a["counters"] == b["counters"]
+    assert np.array_equal(a["exits"], b["exits"])
+    assert np.array_equal(sa, sb) and np.array_equal(ta, tb)
+    assert np.allclose(a["len"], b["len"], rtol=1e-12, atol=0)
