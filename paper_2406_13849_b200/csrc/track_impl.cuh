@@ -681,15 +681,16 @@ cudaError_t launch_event_sp(const DevGeom& g, const KRun& R, bool states, int bl
   const bool st_t = !kFramesRecompute;
   const RectGeom no_rg{};
   constexpr int SB = kSlotsBig;
-  auto go = [&](auto kern, int s) -> cudaError_t {
-    return launch_event_kernel(kern, g, no_rg, R, 256, event_smem_bytes(g, s, false, true, st_t, 7), blocks_per_sm,
+  auto go = [&](auto kern, int s, int threads) -> cudaError_t {
+    return launch_event_kernel(kern, g, no_rg, R, threads, event_smem_bytes(g, s, false, true, st_t, 7), blocks_per_sm,
                                stream, grid_out);
   };
+  constexpr int T = kRingThreads;
   if (ring_slots(g, false, st_t, 7) == SB)
-    return states ? go(k_track_event<256, false, true, false, 0, true, SB, 0, 7>, SB)
-                  : go(k_track_event<256, false, false, false, 0, true, SB, 0, 7>, SB);
-  return states ? go(k_track_event<256, false, true, false, 0, true, 256, 0, 7>, 256)
-                : go(k_track_event<256, false, false, false, 0, true, 256, 0, 7>, 256);
+    return states ? go(k_track_event<T, false, true, false, 0, true, SB, 0, 7>, SB, T)
+                  : go(k_track_event<T, false, false, false, 0, true, SB, 0, 7>, SB, T);
+  return states ? go(k_track_event<256, false, true, false, 0, true, 256, 0, 7>, 256, 256)
+                : go(k_track_event<256, false, false, false, 0, true, 256, 0, 7>, 256, 256);
 }
 #elif defined(NT_RECT_TU)
 // Rect-specialised tracker (Alg. 9-10) under the ring scheduler: the same k_track_event as the
