@@ -708,6 +708,16 @@ void build_flat(const std::vector<HSurf>& s_in, const std::vector<HMat>& M,
       r.tol = F.surf_tol[c.sid[k]];
       F.hsr.push_back(r);
     }
+    // slab pairs: two consecutive half-spaces of the same axis plane kind with opposite senses (a cell
+    // between two PX / PY / PZ planes).  Only the one the flight heads towards can be exited, so the
+    // distance loop evaluates the pair with one division (kHsSlab on the first entry)
+    for (size_t k = F.cell_hs.back(); k + 1 < F.hsr.size(); ++k) {
+      const int e0 = F.hsr[k].e, e1 = F.hsr[k + 1].e;
+      if (hs_kind(e0) <= S_PZ && hs_kind(e1) == hs_kind(e0) && hs_sense(e0) != hs_sense(e1)) {
+        F.hsr[k].meta |= kHsSlab;
+        ++k;
+      }
+    }
     F.cell_hs.push_back((int32_t)F.hs.size());
     if (c.fill_kind == 0) {
       F.cell_fill.push_back(F.n_mc++);

@@ -47,6 +47,9 @@ struct alignas(16) DSurf { double c[4]; };
 // A CSG distance winner is identified by its half-space index h (Best::j), which also names the
 // crossed surface's neighbour list (hs_nb_off[h]) for the descent.
 struct alignas(16) DHs { double c[4]; int32_t e, meta; double tol; };
+// DHs::meta bit above surf_meta: this entry and the next form a slab (same axis plane kind, opposite
+// senses), evaluated together by the distance loop
+constexpr int32_t kHsSlab = 0x100;
 
 // Half-space entry of a cell: (sid << 4) | (kind << 1) | sense  (sense 1 = positive side).
 NT_HD int hs_sid(int h) { return h >> 4; }

@@ -32,6 +32,12 @@
 
 NT_DEV_BEGIN
 constexpr int kHsUnroll = NT_HS_UNROLL;
+// slab pairs of axis planes evaluated with one division (builder kHsSlab), in the f0 feature set: the
+// branch costs the hex models more than it saves (C4 −7 %; C1 +16 %, C2 +13 %, C3 +2.5 %, C5r +9.5 %)
+#ifndef NT_SLABS
+#define NT_SLABS (NT_FEAT == 0)
+#endif
+constexpr bool kSlabs = NT_SLABS != 0;
 
 
 
@@ -88,7 +94,7 @@ __device__ __forceinline__ int winner_surface(const DevGeom& g, bool csg, int jb
   meta = 0;
   if (!csg) return jb;
   const DHs* r = g.hsr + jb;
-  meta = ld(&r->meta);
+  meta = ld(&r->meta) & 0xFF;     // surf_meta (the slab bit above it is the distance loop's)
   return hs_sid(ld(&r->e));
 }
 
@@ -182,7 +188,23 @@ __device__ __forceinline__ void level_candidates(const DevGeom& g, const DUniv* 
       const DHs* r = g.hsr + h;
       const double2 c01 = __ldg(reinterpret_cast<const double2*>(r->c));
       const double2 c23 = __ldg(reinterpret_cast<const double2*>(r->c + 2));
-      const int e = ld(&r->e);
+      const int2 em = __ldg(reinterpret_cast<const int2*>(&r->e));
+      const int e = em.x;
+      if (kSlabs && (em.y & kHsSlab)) {
+        // slab: entries h and h+1 are the same axis plane kind with opposite senses.  A plane of sense
+        // 0 is exited only moving up the axis (den > 0), one of sense 1 only moving down, so at most
+        // one of the two candidates is finite: that one, with surf_dist's arithmetic, at h's turn
+        // (h and h+1 are adjacent in the canonical order, so ties resolve as before)
+        const int kind = hs_kind(e);
+        const double den = sel3(kind, u, v, w);
+        const bool second = (den > 0.0) != (hs_sense(e) == 0);   // the entry exited along den's sign
+        const double c0 = second ? ld(&r[1].c[0]) : c01.x;
+        const int sp = second ? hs_sense(e) ^ 1 : hs_sense(e);
+        const double d = dsel(den != 0.0, clamp0(fdiv(c0 - sel3(kind, x, y, z), den)), NT_INF);
+        b.consider(d, l, second ? h + 1 : h, sp);
+        ++h;
+        continue;
+      }
       const int sid = hs_sid(e);
       const double d = surf_dist(hs_kind(e), hs_sense(e), os_l == l && os_s == sid, c01.x, c01.y, c23.x, c23.y,
                                  x, y, z, u, v, w);
