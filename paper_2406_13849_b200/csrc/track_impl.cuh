@@ -656,7 +656,7 @@ cudaError_t upload_coefficients(const double* host, int n) {
 
 // Slots per block of the ring scheduler (block 256, SP): 320 when NT_EVENT_MINB such blocks still
 // fit an SM (a warp that finishes its chunk then finds queued slots instead of waiting for the
-// chunks the other seven warps hold), else 256.  NESTRACK_SLOTS=256|320 overrides (tuning).
+// chunks the other seven warps hold), else 256.  NESTRACK_SLOTS=256 forces 256, any larger value the big size (tuning).
 // big = 320 for the RTK kernels, kSlotsBig for the SP generic kernels (sp = true).
 static int ring_slots(const DevGeom& g, bool trace, bool store_t, int nr = NQ, bool safety = false, bool sp = true) {
   static const int env = [] { const char* e = getenv("NESTRACK_SLOTS"); return e ? atoi(e) : 0; }();
