@@ -105,7 +105,7 @@ def test_config_parity_untraced(nt, orc, cfg):
 
 @pytest.mark.parametrize("name", ["sphere_in_box", "hex_pins_small_pointy", "hex_pins_small_flat",
                                   "rect3d_small", "lattice3_nested", "lattice3_flat", "infinite_medium",
-                                  "c1_void_vacuum"])
+                                  "c1_void_vacuum", "slab_mix"])
 @pytest.mark.parametrize("sched", ["block", "dp", "rounds"])
 def test_test_models_parity(nt, orc, name, sched):
     """Planes, spheres, 3-D rect and hex z-stacks, translations, void + vacuum leakage."""
@@ -114,7 +114,7 @@ def test_test_models_parity(nt, orc, name, sched):
             "hex_pins_small_flat": lambda: M.hex_pins_small("flat"), "rect3d_small": M.rect3d_small,
             "lattice3_nested": M.lattice3_nested, "lattice3_flat": lambda: M.lattice3_nested(True),
             "infinite_medium": M.infinite_medium,
-            "c1_void_vacuum": lambda: M.c1_pincell(bc="vacuum", void=True)}[name]()
+            "c1_void_vacuum": lambda: M.c1_pincell(bc="vacuum", void=True), "slab_mix": M.slab_mix}[name]()
     _compare(nt, orc, spec, 700, seed=2, scheduler=sched)
 
 

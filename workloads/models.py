@@ -538,6 +538,33 @@ def sphere_in_box() -> dict:
     return sp.to_dict()
 
 
+def slab_mix() -> dict:
+    """Axis-plane pairings for the slab-pair evaluation (DESIGN §5 "Slab pairs"): adjacent
+    opposite-sense pairs of one axis (slabs), a same-axis pair that is not adjacent in the canonical
+    order, same-sense planes, four PX planes in one cell, a cylinder, reflective PX walls."""
+    sp = Spec("slab_mix")
+    root = sp.csg("root")
+    px0, px1 = sp.surf("PX", [-3.0], "reflect"), sp.surf("PX", [3.0], "reflect")
+    py0, py1 = sp.surf("PY", [-3.0], "vacuum"), sp.surf("PY", [3.0], "vacuum")
+    pz0, pz1 = sp.surf("PZ", [-3.0], "vacuum"), sp.surf("PZ", [3.0], "vacuum")
+    box = [px0 + 1, -(px1 + 1), py0 + 1, -(py1 + 1), pz0 + 1, -(pz1 + 1)]
+    x0 = sp.surf("PX", [0.0])
+    xm1 = sp.surf("PX", [-1.0])
+    y1 = sp.surf("PY", [1.0])
+    x15 = sp.surf("PX", [1.5])
+    cz = sp.surf("CZ", [2.0, 2.0, 0.5])
+    m = [sp.mat(f"m{k}", 0.3 + 0.25 * k, 0.05 + 0.02 * k) for k in range(6)]
+    sp.cell(root, box + [-(x0 + 1), xm1 + 1], material=m[0])                  # -1 <= x < 0: two PX slabs
+    sp.cell(root, box + [-(xm1 + 1)], material=m[1])                          # x < -1
+    sp.cell(root, box + [x0 + 1, -(y1 + 1), -(x15 + 1)], material=m[2])       # PX pair not adjacent
+    sp.cell(root, box + [x0 + 1, -(y1 + 1), x15 + 1], material=m[3])          # same-sense PX planes
+    sp.cell(root, box + [x0 + 1, y1 + 1, cz + 1], material=m[4])
+    sp.cell(root, box + [x0 + 1, y1 + 1, -(cz + 1)], material=m[5])
+    sp.root = root
+    sp.source = {"lo": [-3.0, -3.0, -3.0], "hi": [3.0, 3.0, 3.0]}
+    return sp.to_dict()
+
+
 def hex_pins_small(orient="pointy") -> dict:
     """Small 3-ring hex lattice of pins in a reflective box with a 3-D z stack."""
     sp = Spec("hex_small_" + orient)
